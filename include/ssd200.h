@@ -1,0 +1,127 @@
+/*
+ * ssd200 — C ABI of the B200 (sm_100a) Mamba-2 SSD inference hot path.
+ *
+ * The reference engine (/root/reference/pkg/src/ssd_engine) has no FFI: its
+ * boundary is the Python API re-exported in __init__.py:7-24.  Each entry
+ * point below replaces the arithmetic behind one of those calls; the Python
+ * package paper_2603_09555_b200 keeps the reference signatures and calls in
+ * here (see INTEGRATION.md for the ctypes binding a maintainer would add).
+ *
+ * Rules: raw device pointers + explicit dims + a cudaStream_t; the caller owns
+ * every buffer (workspace sizes via *_workspace()); no allocation, no host
+ * synchronisation, no exceptions across the ABI.  Every call returns 0 on
+ * success or a negative status; ssd200_last_error() gives a thread-local
+ * message.  All launches are enqueued on `stream` and are CUDA-graph
+ * capturable.
+ *
+ * Layouts (row-major, "row" = one token):
+ *   hidden       (rows, d_model)          residual stream, f32 (f64 in f64 mode)
+ *   hidden_lp    (rows, d_model)          bf16 shadow of hidden (bf16 mode only)
+ *   ssm state    (batch, H, P, N)         compute dtype (f32 in bf16 mode)
+ *   conv state   (batch, conv_dim, k-1)   newest column last (decode.py:49-69)
+ *   W_in         f32/f64: (d_model, d_in_proj)  [reference layout, model.py:76]
+ *                bf16:    (d_in_proj, d_model)  [K-major for tcgen05]
+ *   W_out        f32/f64: (d_inner, d_model);  bf16: (d_model, d_inner)
+ *   embedding    (vocab, d_model) weight dtype; the tied head reads it as-is.
+ */
+#ifndef SSD200_H
+#define SSD200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *ssd200_stream_t; /* a cudaStream_t */
+
+enum ssd200_dtype { SSD200_F32 = 0, SSD200_F64 = 1, SSD200_BF16 = 2 };
+
+enum ssd200_status {
+  SSD200_OK = 0,
+  SSD200_EINVAL = -1,       /* bad argument (shape, null pointer, range) */
+  SSD200_ELAUNCH = -2,      /* a CUDA launch failed */
+  SSD200_EUNSUPPORTED = -3, /* dims outside what this build supports */
+  SSD200_EWORKSPACE = -4    /* workspace too small */
+};
+
+/* Model widths + numerics (model.py:20-70).  a = -exp(A_log) is host-computed
+ * (ssd.py:99-112) so the bf16e ablation rounds exactly like the reference. */
+typedef struct ssd200_dims {
+  int dtype; /* enum ssd200_dtype: compute mode */
+  int d_model, d_inner, n_heads, head_dim, d_state, n_groups, conv_kernel, chunk_size;
+  double norm_eps, dt_min, dt_max;
+} ssd200_dims_t;
+
+typedef struct ssd200_layer {
+  const void *W_in, *conv_w, *conv_b, *dt_bias, *a, *D, *norm_w, *W_out;
+} ssd200_layer_t;
+
+int ssd200_abi_version(void);
+const char *ssd200_last_error(void);
+
+/* ---- ssd_forward (ssd.py:209-257): chunked SSD scan --------------------
+ * X (B,T,H,P), dt (B,T,H) [post-softplus, >=0], a (H) [<=0], Bmat/Cmat
+ * (B,T,G,N), D (H) or NULL (adds D*x, model.py:166), init_state (B,H,P,N) or
+ * NULL -> Y (B,T,H,P), final_state (B,H,P,N).  dtype F32 or F64. */
+size_t ssd200_chunk_scan_workspace(int dtype, int batch, int seqlen, int heads, int head_dim,
+                                   int d_state, int chunk);
+int ssd200_chunk_scan(int dtype, const void *X, const void *dt, const void *a, const void *Bmat,
+                      const void *Cmat, const void *D, const void *init_state, void *Y,
+                      void *final_state, int batch, int seqlen, int heads, int head_dim,
+                      int groups, int d_state, int chunk, void *workspace,
+                      size_t workspace_bytes, ssd200_stream_t stream);
+
+/* ---- embedding gather (model.py:198, decode.py:96) ----------------------
+ * tokens int64 (rows) already range-checked by the caller. */
+int ssd200_embed(const ssd200_dims_t *d, const int64_t *tokens, int rows, const void *embedding,
+                 void *hidden, void *hidden_lp, ssd200_stream_t stream);
+
+/* ---- block_forward (model.py:124-174) over (batch, seqlen) ---------------
+ * hidden/hidden_lp updated in place; writes the layer's final SSM state and
+ * conv tail (pre-activation, newest last, zero-padded when T<k-1). */
+size_t ssd200_prefill_layer_workspace(const ssd200_dims_t *d, int batch, int seqlen);
+int ssd200_prefill_layer(const ssd200_dims_t *d, const ssd200_layer_t *w, void *hidden,
+                         void *hidden_lp, void *ssm_out, void *conv_out, int batch, int seqlen,
+                         void *workspace, size_t workspace_bytes, ssd200_stream_t stream);
+
+/* ---- one decode_step layer (decode.py:99-140) ----------------------------
+ * ssm_out/conv_out may alias ssm_in/conv_in (in-place update for generate). */
+size_t ssd200_decode_layer_workspace(const ssd200_dims_t *d, int batch);
+int ssd200_decode_layer(const ssd200_dims_t *d, const ssd200_layer_t *w, void *hidden,
+                        void *hidden_lp, const void *ssm_in, void *ssm_out, const void *conv_in,
+                        void *conv_out, int batch, void *workspace, size_t workspace_bytes,
+                        ssd200_stream_t stream);
+
+/* ---- final RMSNorm + tied head (+ greedy argmax) (model.py:204-205,
+ * decode.py:72-74,142-143) -------------------------------------------------
+ * Reads `rows` rows of hidden spaced hidden_row_stride elements apart.
+ * logits (rows, vocab) f32 (f64 in f64 mode) or NULL; argmax_out (rows) int64
+ * or NULL (ties -> lowest id). */
+size_t ssd200_head_workspace(const ssd200_dims_t *d, int vocab, int rows);
+int ssd200_head(const ssd200_dims_t *d, int vocab, const void *hidden, int64_t hidden_row_stride,
+                const void *final_norm_w, const void *embedding, void *logits,
+                int64_t *argmax_out, int rows, void *workspace, size_t workspace_bytes,
+                ssd200_stream_t stream);
+
+/* ---- raw bf16 tensor-core GEMM (tcgen05 + TMA + TMEM), for tests/bench --
+ * C (M,N) f32 = A (M,K) bf16 row-major  x  B^T where B is (N,K) bf16 row-major.
+ * K % 8 == 0 (16-byte TMA row pitch); ragged M/N/K tiles are zero-filled. */
+int ssd200_gemm_bf16(const void *A, const void *B, void *C, int M, int N, int K,
+                     ssd200_stream_t stream);
+
+/* ---- instrumentation (bench.py) -----------------------------------------
+ * Number of kernels this library has launched from the calling thread. */
+uint64_t ssd200_launch_count(void);
+/* Phase timing: when set (non-NULL), ssd200_prefill_layer records
+ * events[2*p] before and events[2*p+1] after phase p on the call's stream
+ * (p: 0 in_proj, 1 conv, 2 scan, 3 gated norm, 4 out_proj); events are
+ * cudaEvent_t handles owned by the caller.  Pass NULL to disable. */
+int ssd200_set_phase_events(void *const *events, int n_phases);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SSD200_H */

@@ -1,0 +1,800 @@
+// C-ABI entry points (include/ssd200.h): validation, workspace carving and
+// the per-layer launch sequences.  No allocation, no host sync.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+#include <string>
+
+#include "../../include/ssd200.h"
+#include "common.cuh"
+#include "simt.cuh"
+#include "tc_gemm.cuh"
+
+using namespace ssd200;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local uint64_t g_launches = 0;
+thread_local void *const *g_phase_ev = nullptr;
+thread_local int g_nphase = 0;
+
+enum { PH_IN_PROJ = 0, PH_CONV = 1, PH_SCAN = 2, PH_NORM = 3, PH_OUT_PROJ = 4 };
+
+inline void phase_mark(int p, int end, cudaStream_t st) {
+  if (g_phase_ev && p < g_nphase)
+    cudaEventRecord(static_cast<cudaEvent_t>(g_phase_ev[2 * p + end]), st);
+}
+
+void set_err(const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+#define REQUIRE(cond, code, ...) \
+  do {                           \
+    if (!(cond)) {               \
+      set_err(__VA_ARGS__);      \
+      return code;               \
+    }                            \
+  } while (0)
+
+int check_launch(const char *what) {
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_err("%s: %s", what, cudaGetErrorString(e));
+    return SSD200_ELAUNCH;
+  }
+  return SSD200_OK;
+}
+
+#define LAUNCH_CHECK(what)             \
+  do {                                 \
+    int _rc = check_launch(what);      \
+    if (_rc) return _rc;               \
+  } while (0)
+
+inline size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
+
+// simple bump allocator over the caller's workspace
+struct Carve {
+  char *base;
+  size_t used = 0, cap;
+  Carve(void *p, size_t c) : base(static_cast<char *>(p)), cap(c) {}
+  template <typename T> T *take(size_t n) {
+    size_t off = used;
+    used = align_up(used + n * sizeof(T));
+    return reinterpret_cast<T *>(base ? base + off : nullptr);
+  }
+  bool ok() const { return used <= cap; }
+};
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// --------------------------------------------------------------- TMA maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 map over a row-major (rows, cols) matrix with leading dim ld,
+// box = (64 cols = 128 B, box_rows), SWIZZLE_128B.
+int make_map_2d(CUtensorMap *m, const void *ptr, long rows, long cols, long ld, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  REQUIRE(fn, SSD200_ELAUNCH, "cuTensorMapEncodeTiled unavailable");
+  REQUIRE(((uintptr_t)ptr & 15) == 0, SSD200_EINVAL, "TMA base pointer not 16-byte aligned");
+  REQUIRE((ld * 2) % 16 == 0, SSD200_EINVAL, "TMA row stride must be a multiple of 16 bytes");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  REQUIRE(r == CUDA_SUCCESS, SSD200_ELAUNCH, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return SSD200_OK;
+}
+
+template <int BN, int EPI>
+int launch_tc_gemm_bn(const bf16 *A, long lda, const bf16 *B, long ldb, int M, int N, int K,
+                      const TcEpilogue &ep, cudaStream_t st) {
+  using Cfg = TcCfg<BN>;
+  CUtensorMap ta, tb;
+  int rc = make_map_2d(&ta, A, M, K, lda, Cfg::BM);
+  if (rc) return rc;
+  rc = make_map_2d(&tb, B, N, K, ldb, BN);
+  if (rc) return rc;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(tc_gemm_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Cfg::SMEM);
+    attr_set = true;
+  }
+  const int tiles = ((M + Cfg::BM - 1) / Cfg::BM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  tc_gemm_kernel<BN, EPI><<<grid, 192, Cfg::SMEM, st>>>(ta, tb, M, N, K, ep);
+  LAUNCH_CHECK("tc_gemm_kernel");
+  return SSD200_OK;
+}
+
+// D (M,N) = A (M,K) . B (N,K)^T, bf16 operands, fused epilogue.
+template <int EPI>
+int tc_gemm(const bf16 *A, long lda, const bf16 *B, long ldb, int M, int N, int K,
+            const TcEpilogue &ep, cudaStream_t st) {
+  REQUIRE(M > 0 && N > 0 && K > 0, SSD200_EINVAL, "tc_gemm: empty problem");
+  REQUIRE(K % 8 == 0, SSD200_EINVAL, "tc_gemm: K must be a multiple of 8");
+  if (N <= 128) return launch_tc_gemm_bn<128, EPI>(A, lda, B, ldb, M, N, K, ep, st);
+  return launch_tc_gemm_bn<256, EPI>(A, lda, B, ldb, M, N, K, ep, st);
+}
+
+// --------------------------------------------------------------- SSD scan
+template <typename T, typename TI> struct ScanKernels {
+  static bool attrs_done;
+};
+template <typename T, typename TI> bool ScanKernels<T, TI>::attrs_done = false;
+
+inline size_t scan_ws_bytes(size_t elt, long B, long T, long H, long P, long N, long L) {
+  long Nc = (T + L - 1) / L;
+  return align_up(B * Nc * H * P * N * elt) + align_up(B * H * Nc * elt);
+}
+
+template <typename T, typename TI>
+int run_scan(SsdArgs<T, TI> a, void *ws, size_t ws_bytes, cudaStream_t st) {
+  REQUIRE(a.L >= 1 && a.L <= 2048, SSD200_EUNSUPPORTED, "chunk_size %d outside [1, 2048]", a.L);
+  REQUIRE((long)a.P * a.N <= 256L * SSD_MAX_PN_PER_THREAD, SSD200_EUNSUPPORTED,
+          "head_dim*d_state = %d exceeds %d", a.P * a.N, 256 * SSD_MAX_PN_PER_THREAD);
+  REQUIRE(a.P <= 256, SSD200_EUNSUPPORTED, "head_dim > 256");
+  REQUIRE(a.H % a.G == 0, SSD200_EINVAL, "head count %d not divisible by group count %d", a.H,
+          a.G);
+  a.Nc = (a.T_ + a.L - 1) / a.L;
+  Carve cv(ws, ws_bytes);
+  a.S = cv.take<T>((size_t)a.B * a.Nc * a.H * a.P * a.N);
+  a.cs_end = cv.take<T>((size_t)a.B * a.H * a.Nc);
+  REQUIRE(cv.ok(), SSD200_EWORKSPACE, "scan workspace %zu < %zu", ws_bytes, cv.used);
+  const size_t smem1 = (3 * (size_t)a.L + 16 * (size_t)a.P + 16 * (size_t)a.N) * sizeof(T);
+  const size_t smem3 =
+      (2 * (size_t)a.L + 16 * (size_t)a.N + 32 * (size_t)a.N + 32 * (size_t)a.P + 16 * 32) *
+      sizeof(T);
+  REQUIRE(smem1 <= 220 * 1024 && smem3 <= 220 * 1024, SSD200_EUNSUPPORTED,
+          "scan shared memory too large");
+  if (!ScanKernels<T, TI>::attrs_done) {
+    cudaFuncSetAttribute(ssd_chunk_state<T, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         220 * 1024);
+    cudaFuncSetAttribute(ssd_chunk_out<T, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         220 * 1024);
+    ScanKernels<T, TI>::attrs_done = true;
+  }
+  ssd_chunk_state<T, TI><<<dim3(a.Nc, a.H, a.B), 256, smem1, st>>>(a);
+  LAUNCH_CHECK("ssd_chunk_state");
+  const int PN = a.P * a.N;
+  ssd_state_pass<T><<<dim3((PN + 255) / 256, a.H, a.B), 256, 0, st>>>(a.S, a.cs_end, a.init,
+                                                                       a.final_state, a.H, PN,
+                                                                       a.Nc);
+  LAUNCH_CHECK("ssd_state_pass");
+  const int nRT = (a.L + 15) / 16;
+  ssd_chunk_out<T, TI><<<dim3(a.Nc * nRT, a.H, a.B), 256, smem3, st>>>(a);
+  LAUNCH_CHECK("ssd_chunk_out");
+  return SSD200_OK;
+}
+
+int check_dims(const ssd200_dims_t *d) {
+  REQUIRE(d, SSD200_EINVAL, "null dims");
+  REQUIRE(d->dtype == SSD200_F32 || d->dtype == SSD200_F64 || d->dtype == SSD200_BF16,
+          SSD200_EINVAL, "unknown dtype %d", d->dtype);
+  REQUIRE(d->d_model > 0 && d->d_inner > 0 && d->n_heads > 0 && d->head_dim > 0 &&
+              d->d_state > 0 && d->n_groups > 0 && d->conv_kernel >= 1 && d->chunk_size >= 1,
+          SSD200_EINVAL, "non-positive model dims");
+  REQUIRE(d->n_heads * d->head_dim == d->d_inner, SSD200_EINVAL, "n_heads*head_dim != d_inner");
+  REQUIRE(d->n_heads % d->n_groups == 0, SSD200_EINVAL, "n_heads %% n_groups != 0");
+  REQUIRE(d->conv_kernel <= 16, SSD200_EUNSUPPORTED, "conv_kernel > 16");
+  return SSD200_OK;
+}
+
+struct Widths {
+  long conv_dim, d_in_proj, gn;
+};
+inline Widths widths(const ssd200_dims_t *d) {
+  Widths w;
+  w.gn = (long)d->n_groups * d->d_state;
+  w.conv_dim = d->d_inner + 2 * w.gn;
+  w.d_in_proj = 2L * d->d_inner + 2 * w.gn + d->n_heads;
+  return w;
+}
+
+inline unsigned blocks_for(long n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+// ------------------------------------------------------------ prefill layer
+// workspace carve (identical in sizing and launch)
+template <typename T> struct PrefillWs {
+  void *u;     // f32/f64: (rows, d_in_proj) T;  bf16: (rows, d_inner+conv_dim) bf16
+  void *act;   // post-conv xBC: T or bf16 (rows, conv_dim); reused for the normed y
+  T *dt;       // (rows, H)
+  T *y;        // (rows, d_inner)
+  void *scan;  // scan workspace
+  size_t scan_bytes;
+};
+
+template <typename T>
+bool carve_prefill(const ssd200_dims_t *d, int B, int Tn, void *ws, size_t cap, PrefillWs<T> &o,
+                   size_t *need) {
+  Widths w = widths(d);
+  const long rows = (long)B * Tn;
+  const bool lp = d->dtype == SSD200_BF16;
+  Carve cv(ws, cap);
+  if (lp) {
+    o.u = cv.take<bf16>(rows * (d->d_inner + w.conv_dim));
+    o.act = cv.take<bf16>(rows * w.conv_dim);
+  } else {
+    o.u = cv.take<T>(rows * w.d_in_proj);
+    o.act = cv.take<T>(rows * w.conv_dim);
+  }
+  o.dt = cv.take<T>(rows * d->n_heads);
+  o.y = cv.take<T>(rows * d->d_inner);
+  o.scan_bytes = scan_ws_bytes(sizeof(T), B, Tn, d->n_heads, d->head_dim, d->d_state,
+                               d->chunk_size);
+  o.scan = cv.take<char>(o.scan_bytes);
+  if (need) *need = cv.used;
+  return cv.ok();
+}
+
+template <typename T>
+int prefill_layer_simt(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidden, T *ssm_out,
+                       T *conv_out, int B, int Tn, void *ws, size_t ws_bytes, cudaStream_t st) {
+  PrefillWs<T> o;
+  size_t need = 0;
+  REQUIRE(carve_prefill<T>(d, B, Tn, ws, ws_bytes, o, &need), SSD200_EWORKSPACE,
+          "prefill workspace %zu < %zu", ws_bytes, need);
+  Widths wd = widths(d);
+  const long rows = (long)B * Tn;
+  T *u = static_cast<T *>(o.u);
+  T *act = static_cast<T *>(o.act);
+  const int k = d->conv_kernel;
+  // in_proj: u = hidden . W_in   (model.py:141)
+  gemm_simt<T, false, EPI_STORE><<<dim3(blocks_for(wd.d_in_proj, 64), blocks_for(rows, 64)),
+                                   256, 0, st>>>(hidden, d->d_model,
+                                                 static_cast<const T *>(w->W_in), wd.d_in_proj,
+                                                 u, wd.d_in_proj, (int)rows, (int)wd.d_in_proj,
+                                                 d->d_model);
+  LAUNCH_CHECK("gemm_simt in_proj");
+  // conv tail (pre-activation) + conv/SiLU + dt
+  if (k > 1) {
+    conv_tail_kernel<T, T><<<blocks_for((long)B * wd.conv_dim * (k - 1)), 256, 0, st>>>(
+        u + d->d_inner, wd.d_in_proj, conv_out, B, Tn, (int)wd.conv_dim, k);
+    LAUNCH_CHECK("conv_tail");
+  }
+  conv_silu_prefill<T, T, T><<<blocks_for(rows * wd.conv_dim), 256, 0, st>>>(
+      u + d->d_inner, wd.d_in_proj, static_cast<const T *>(w->conv_w),
+      static_cast<const T *>(w->conv_b), act, wd.conv_dim, Tn, (int)wd.conv_dim, k,
+      rows * wd.conv_dim);
+  LAUNCH_CHECK("conv_silu_prefill");
+  dt_kernel<T, T><<<blocks_for(rows * d->n_heads), 256, 0, st>>>(
+      u + d->d_inner + wd.conv_dim, wd.d_in_proj, static_cast<const T *>(w->dt_bias), o.dt, rows,
+      d->n_heads, (T)d->dt_min, (T)d->dt_max);
+  LAUNCH_CHECK("dt_kernel");
+  // SSD (+ D skip)
+  SsdArgs<T, T> sa{};
+  sa.X = act;
+  sa.x_ts = wd.conv_dim;
+  sa.dt = o.dt;
+  sa.dt_ts = d->n_heads;
+  sa.a = static_cast<const T *>(w->a);
+  sa.Bm = act + d->d_inner;
+  sa.Cm = act + d->d_inner + wd.gn;
+  sa.bc_ts = wd.conv_dim;
+  sa.D = static_cast<const T *>(w->D);
+  sa.init = nullptr;
+  sa.Y = o.y;
+  sa.y_ts = d->d_inner;
+  sa.final_state = ssm_out;
+  sa.B = B;
+  sa.T_ = Tn;
+  sa.H = d->n_heads;
+  sa.P = d->head_dim;
+  sa.G = d->n_groups;
+  sa.N = d->d_state;
+  sa.L = d->chunk_size;
+  int rc = run_scan<T, T>(sa, o.scan, o.scan_bytes, st);
+  if (rc) return rc;
+  // gated norm -> act (reused), then out_proj + residual
+  gated_norm_kernel<T, T, T><<<(unsigned)rows, 256, 0, st>>>(
+      o.y, d->d_inner, u, wd.d_in_proj, static_cast<const T *>(w->norm_w), act, d->d_inner,
+      d->d_inner, (T)d->norm_eps);
+  LAUNCH_CHECK("gated_norm");
+  gemm_simt<T, false, EPI_ADD><<<dim3(blocks_for(d->d_model, 64), blocks_for(rows, 64)), 256, 0,
+                                 st>>>(act, d->d_inner, static_cast<const T *>(w->W_out),
+                                       d->d_model, hidden, d->d_model, (int)rows, d->d_model,
+                                       d->d_inner);
+  LAUNCH_CHECK("gemm_simt out_proj");
+  return SSD200_OK;
+}
+
+int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hidden,
+                       bf16 *hidden_lp, float *ssm_out, float *conv_out, int B, int Tn, void *ws,
+                       size_t ws_bytes, cudaStream_t st) {
+  REQUIRE(hidden_lp, SSD200_EINVAL, "bf16 mode needs the hidden_lp shadow");
+  PrefillWs<float> o;
+  size_t need = 0;
+  REQUIRE(carve_prefill<float>(d, B, Tn, ws, ws_bytes, o, &need), SSD200_EWORKSPACE,
+          "prefill workspace %zu < %zu", ws_bytes, need);
+  Widths wd = widths(d);
+  const long rows = (long)B * Tn;
+  const long n_split = d->d_inner + wd.conv_dim;
+  bf16 *u = static_cast<bf16 *>(o.u);
+  bf16 *act = static_cast<bf16 *>(o.act);
+  const int k = d->conv_kernel;
+  // in_proj on tensor cores, dt epilogue fused
+  TcEpilogue ep{};
+  ep.C = u;
+  ep.ldc = n_split;
+  ep.n_split = (int)n_split;
+  ep.dt = o.dt;
+  ep.H = d->n_heads;
+  ep.dt_bias = static_cast<const float *>(w->dt_bias);
+  ep.dt_lo = (float)d->dt_min;
+  ep.dt_hi = (float)d->dt_max;
+  phase_mark(PH_IN_PROJ, 0, st);
+  int rc = tc_gemm<TC_EPI_INPROJ>(hidden_lp, d->d_model, static_cast<const bf16 *>(w->W_in),
+                                  d->d_model, (int)rows, (int)wd.d_in_proj, d->d_model, ep, st);
+  if (rc) return rc;
+  phase_mark(PH_IN_PROJ, 1, st);
+  phase_mark(PH_CONV, 0, st);
+  if (k > 1) {
+    conv_tail_kernel<float, bf16><<<blocks_for((long)B * wd.conv_dim * (k - 1)), 256, 0, st>>>(
+        u + d->d_inner, n_split, conv_out, B, Tn, (int)wd.conv_dim, k);
+    LAUNCH_CHECK("conv_tail");
+  }
+  conv_silu_prefill<float, bf16, bf16><<<blocks_for(rows * wd.conv_dim), 256, 0, st>>>(
+      u + d->d_inner, n_split, static_cast<const float *>(w->conv_w),
+      static_cast<const float *>(w->conv_b), act, wd.conv_dim, Tn, (int)wd.conv_dim, k,
+      rows * wd.conv_dim);
+  LAUNCH_CHECK("conv_silu_prefill");
+  phase_mark(PH_CONV, 1, st);
+  SsdArgs<float, bf16> sa{};
+  sa.X = act;
+  sa.x_ts = wd.conv_dim;
+  sa.dt = o.dt;
+  sa.dt_ts = d->n_heads;
+  sa.a = static_cast<const float *>(w->a);
+  sa.Bm = act + d->d_inner;
+  sa.Cm = act + d->d_inner + wd.gn;
+  sa.bc_ts = wd.conv_dim;
+  sa.D = static_cast<const float *>(w->D);
+  sa.init = nullptr;
+  sa.Y = o.y;
+  sa.y_ts = d->d_inner;
+  sa.final_state = ssm_out;
+  sa.B = B;
+  sa.T_ = Tn;
+  sa.H = d->n_heads;
+  sa.P = d->head_dim;
+  sa.G = d->n_groups;
+  sa.N = d->d_state;
+  sa.L = d->chunk_size;
+  phase_mark(PH_SCAN, 0, st);
+  rc = run_scan<float, bf16>(sa, o.scan, o.scan_bytes, st);
+  if (rc) return rc;
+  phase_mark(PH_SCAN, 1, st);
+  phase_mark(PH_NORM, 0, st);
+  bf16 *normed = act;  // act is dead after the scan
+  gated_norm_kernel<float, bf16, bf16><<<(unsigned)rows, 256, 0, st>>>(
+      o.y, d->d_inner, u, n_split, static_cast<const float *>(w->norm_w), normed, d->d_inner,
+      d->d_inner, (float)d->norm_eps);
+  LAUNCH_CHECK("gated_norm");
+  phase_mark(PH_NORM, 1, st);
+  TcEpilogue er{};
+  er.C = hidden;
+  er.ldc = d->d_model;
+  er.C_lp = hidden_lp;
+  phase_mark(PH_OUT_PROJ, 0, st);
+  rc = tc_gemm<TC_EPI_RESID>(normed, d->d_inner, static_cast<const bf16 *>(w->W_out), d->d_inner,
+                             (int)rows, d->d_model, d->d_inner, er, st);
+  phase_mark(PH_OUT_PROJ, 1, st);
+  return rc;
+}
+
+// ------------------------------------------------------------- decode layer
+template <typename T> struct DecodeWs {
+  T *u, *act, *y, *normed_T;
+  bf16 *normed_lp;
+};
+
+template <typename T>
+bool carve_decode(const ssd200_dims_t *d, int B, void *ws, size_t cap, DecodeWs<T> &o,
+                  size_t *need) {
+  Widths w = widths(d);
+  Carve cv(ws, cap);
+  o.u = cv.take<T>((size_t)B * w.d_in_proj);
+  o.act = cv.take<T>((size_t)B * w.conv_dim);
+  o.y = cv.take<T>((size_t)B * d->d_inner);
+  o.normed_T = cv.take<T>((size_t)B * d->d_inner);
+  o.normed_lp = cv.take<bf16>((size_t)B * d->d_inner);
+  if (need) *need = cv.used;
+  return cv.ok();
+}
+
+constexpr int GEMV_MAX_ROWS = 16;
+
+template <typename T>
+int decode_layer_impl(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidden,
+                      bf16 *hidden_lp, const T *ssm_in, T *ssm_out, const T *conv_in,
+                      T *conv_out, int B, void *ws, size_t ws_bytes, cudaStream_t st) {
+  DecodeWs<T> o;
+  size_t need = 0;
+  REQUIRE(carve_decode<T>(d, B, ws, ws_bytes, o, &need), SSD200_EWORKSPACE,
+          "decode workspace %zu < %zu", ws_bytes, need);
+  Widths wd = widths(d);
+  const bool lp = d->dtype == SSD200_BF16;
+  const int k = d->conv_kernel;
+  // in_proj
+  if (lp) {
+    REQUIRE(hidden_lp, SSD200_EINVAL, "bf16 mode needs the hidden_lp shadow");
+    const bf16 *Win = static_cast<const bf16 *>(w->W_in);
+    if (B <= GEMV_MAX_ROWS) {
+      gemv_nk<float, bf16, bf16, EPI_STORE>
+          <<<dim3(blocks_for(wd.d_in_proj, 32), blocks_for(B, 4)), 256, 0, st>>>(
+              hidden_lp, d->d_model, Win, d->d_model, (float *)o.u, wd.d_in_proj, nullptr, B,
+              (int)wd.d_in_proj, d->d_model);
+      LAUNCH_CHECK("gemv_nk in_proj");
+    } else {
+      TcEpilogue ep{};
+      ep.C = o.u;
+      ep.ldc = wd.d_in_proj;
+      int rc = tc_gemm<TC_EPI_F32>(hidden_lp, d->d_model, Win, d->d_model, B, (int)wd.d_in_proj,
+                                   d->d_model, ep, st);
+      if (rc) return rc;
+    }
+  } else {
+    const T *Win = static_cast<const T *>(w->W_in);
+    if (B <= GEMV_MAX_ROWS) {
+      gemv_kn<T, EPI_STORE><<<dim3(blocks_for(wd.d_in_proj, 32), blocks_for(B, 8)), dim3(32, 8),
+                              0, st>>>(hidden, d->d_model, Win, wd.d_in_proj, o.u, wd.d_in_proj,
+                                       B, (int)wd.d_in_proj, d->d_model);
+    } else {
+      gemm_simt<T, false, EPI_STORE><<<dim3(blocks_for(wd.d_in_proj, 64), blocks_for(B, 64)),
+                                       256, 0, st>>>(hidden, d->d_model, Win, wd.d_in_proj, o.u,
+                                                     wd.d_in_proj, B, (int)wd.d_in_proj,
+                                                     d->d_model);
+    }
+    LAUNCH_CHECK("in_proj (decode)");
+  }
+  // conv window roll + readout
+  REQUIRE(k >= 1 && k <= 16, SSD200_EUNSUPPORTED, "conv_kernel");
+  decode_conv<T, T><<<blocks_for((long)B * wd.conv_dim), 256, 0, st>>>(
+      o.u, wd.d_in_proj, d->d_inner, conv_in, conv_out, static_cast<const T *>(w->conv_w),
+      static_cast<const T *>(w->conv_b), o.act, B, (int)wd.conv_dim, k);
+  LAUNCH_CHECK("decode_conv");
+  // state update + readout + D skip
+  decode_ssm<T, T><<<dim3(d->n_heads, B), 128, 2 * d->d_state * sizeof(T), st>>>(
+      o.u, wd.d_in_proj, (int)(d->d_inner + wd.conv_dim), o.act, d->d_inner,
+      static_cast<const T *>(w->dt_bias), static_cast<const T *>(w->a),
+      static_cast<const T *>(w->D), ssm_in, ssm_out, o.y, d->d_inner, d->n_heads, d->head_dim,
+      d->n_groups, d->d_state, (T)d->dt_min, (T)d->dt_max);
+  LAUNCH_CHECK("decode_ssm");
+  // gated norm + out_proj + residual
+  if (lp) {
+    gated_norm_kernel<float, float, bf16><<<B, 256, 0, st>>>(
+        (const float *)o.y, d->d_inner, (const float *)o.u, wd.d_in_proj,
+        static_cast<const float *>(w->norm_w), o.normed_lp, d->d_inner, d->d_inner,
+        (float)d->norm_eps);
+    LAUNCH_CHECK("gated_norm (decode)");
+    const bf16 *Wout = static_cast<const bf16 *>(w->W_out);
+    if (B <= GEMV_MAX_ROWS) {
+      gemv_nk<float, bf16, bf16, EPI_ADD>
+          <<<dim3(blocks_for(d->d_model, 32), blocks_for(B, 4)), 256, 0, st>>>(
+              o.normed_lp, d->d_inner, Wout, d->d_inner, (float *)hidden, d->d_model, hidden_lp,
+              B, d->d_model, d->d_inner);
+      LAUNCH_CHECK("gemv_nk out_proj");
+    } else {
+      TcEpilogue er{};
+      er.C = hidden;
+      er.ldc = d->d_model;
+      er.C_lp = hidden_lp;
+      int rc = tc_gemm<TC_EPI_RESID>(o.normed_lp, d->d_inner, Wout, d->d_inner, B, d->d_model,
+                                     d->d_inner, er, st);
+      if (rc) return rc;
+    }
+  } else {
+    gated_norm_kernel<T, T, T><<<B, 256, 0, st>>>(o.y, d->d_inner, o.u, wd.d_in_proj,
+                                                  static_cast<const T *>(w->norm_w), o.normed_T,
+                                                  d->d_inner, d->d_inner, (T)d->norm_eps);
+    LAUNCH_CHECK("gated_norm (decode)");
+    const T *Wout = static_cast<const T *>(w->W_out);
+    if (B <= GEMV_MAX_ROWS) {
+      gemv_kn<T, EPI_ADD><<<dim3(blocks_for(d->d_model, 32), blocks_for(B, 8)), dim3(32, 8), 0,
+                            st>>>(o.normed_T, d->d_inner, Wout, d->d_model, hidden, d->d_model,
+                                  B, d->d_model, d->d_inner);
+    } else {
+      gemm_simt<T, false, EPI_ADD><<<dim3(blocks_for(d->d_model, 64), blocks_for(B, 64)), 256, 0,
+                                     st>>>(o.normed_T, d->d_inner, Wout, d->d_model, hidden,
+                                           d->d_model, B, d->d_model, d->d_inner);
+    }
+    LAUNCH_CHECK("out_proj (decode)");
+  }
+  return SSD200_OK;
+}
+
+// ------------------------------------------------------------------- head
+template <typename T>
+int head_simt(const ssd200_dims_t *d, int V, const T *hidden, long hrs, const T *fw, const T *E,
+              T *logits, int64_t *amax, int rows, void *ws, size_t ws_bytes, cudaStream_t st) {
+  Carve cv(ws, ws_bytes);
+  T *normed = cv.take<T>((size_t)rows * d->d_model);
+  T *lg = logits ? logits : cv.take<T>((size_t)rows * V);
+  REQUIRE(cv.ok(), SSD200_EWORKSPACE, "head workspace %zu < %zu", ws_bytes, cv.used);
+  rmsnorm_rows<T, T><<<rows, 256, 0, st>>>(hidden, hrs, fw, normed, d->d_model, d->d_model,
+                                           (T)d->norm_eps);
+  LAUNCH_CHECK("rmsnorm_rows");
+  if (rows <= GEMV_MAX_ROWS) {
+    gemv_nk<T, T, T, EPI_STORE><<<dim3(blocks_for(V, 32), blocks_for(rows, 4)), 256, 0, st>>>(
+        normed, d->d_model, E, d->d_model, lg, V, nullptr, rows, V, d->d_model);
+  } else {
+    gemm_simt<T, true, EPI_STORE><<<dim3(blocks_for(V, 64), blocks_for(rows, 64)), 256, 0, st>>>(
+        normed, d->d_model, E, d->d_model, lg, V, rows, V, d->d_model);
+  }
+  LAUNCH_CHECK("head gemm");
+  if (amax) {
+    argmax_rows<T><<<rows, 256, 0, st>>>(lg, V, V, amax);
+    LAUNCH_CHECK("argmax_rows");
+  }
+  return SSD200_OK;
+}
+
+int head_bf16(const ssd200_dims_t *d, int V, const float *hidden, long hrs, const float *fw,
+              const bf16 *E, float *logits, int64_t *amax, int rows, void *ws, size_t ws_bytes,
+              cudaStream_t st) {
+  Carve cv(ws, ws_bytes);
+  bf16 *normed = cv.take<bf16>((size_t)rows * d->d_model);
+  float *lg = logits ? logits : cv.take<float>((size_t)rows * V);
+  REQUIRE(cv.ok(), SSD200_EWORKSPACE, "head workspace %zu < %zu", ws_bytes, cv.used);
+  rmsnorm_rows<float, bf16><<<rows, 256, 0, st>>>(hidden, hrs, fw, normed, d->d_model,
+                                                  d->d_model, (float)d->norm_eps);
+  LAUNCH_CHECK("rmsnorm_rows");
+  if (rows <= GEMV_MAX_ROWS) {
+    gemv_nk<float, bf16, bf16, EPI_STORE>
+        <<<dim3(blocks_for(V, 32), blocks_for(rows, 4)), 256, 0, st>>>(
+            normed, d->d_model, E, d->d_model, lg, V, nullptr, rows, V, d->d_model);
+    LAUNCH_CHECK("head gemv");
+  } else {
+    TcEpilogue ep{};
+    ep.C = lg;
+    ep.ldc = V;
+    int rc = tc_gemm<TC_EPI_F32>(normed, d->d_model, E, d->d_model, rows, V, d->d_model, ep, st);
+    if (rc) return rc;
+  }
+  if (amax) {
+    argmax_rows<float><<<rows, 256, 0, st>>>(lg, V, V, amax);
+    LAUNCH_CHECK("argmax_rows");
+  }
+  return SSD200_OK;
+}
+
+}  // namespace
+
+// =============================================================== C ABI
+extern "C" {
+
+int ssd200_abi_version(void) { return 1; }
+
+const char *ssd200_last_error(void) { return g_err.c_str(); }
+
+size_t ssd200_chunk_scan_workspace(int dtype, int batch, int seqlen, int heads, int head_dim,
+                                   int d_state, int chunk) {
+  size_t elt = dtype == SSD200_F64 ? 8 : 4;
+  if (batch < 1 || seqlen < 1 || chunk < 1) return 0;
+  return scan_ws_bytes(elt, batch, seqlen, heads, head_dim, d_state, chunk);
+}
+
+int ssd200_chunk_scan(int dtype, const void *X, const void *dt, const void *a, const void *Bmat,
+                      const void *Cmat, const void *D, const void *init_state, void *Y,
+                      void *final_state, int batch, int seqlen, int heads, int head_dim,
+                      int groups, int d_state, int chunk, void *workspace,
+                      size_t workspace_bytes, ssd200_stream_t stream) {
+  REQUIRE(X && dt && a && Bmat && Cmat && Y && final_state, SSD200_EINVAL, "null pointer");
+  REQUIRE(batch >= 1 && seqlen >= 1 && heads >= 1 && head_dim >= 1 && groups >= 1 &&
+              d_state >= 1 && chunk >= 1,
+          SSD200_EINVAL, "need T >= 1 and L >= 1, got T=%d, L=%d", seqlen, chunk);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == SSD200_F32 || dtype == SSD200_F64) {
+    auto fill = [&](auto tag) {
+      using T = decltype(tag);
+      SsdArgs<T, T> s{};
+      s.X = static_cast<const T *>(X);
+      s.x_ts = (long)heads * head_dim;
+      s.dt = static_cast<const T *>(dt);
+      s.dt_ts = heads;
+      s.a = static_cast<const T *>(a);
+      s.Bm = static_cast<const T *>(Bmat);
+      s.Cm = static_cast<const T *>(Cmat);
+      s.bc_ts = (long)groups * d_state;
+      s.D = static_cast<const T *>(D);
+      s.init = static_cast<const T *>(init_state);
+      s.Y = static_cast<T *>(Y);
+      s.y_ts = (long)heads * head_dim;
+      s.final_state = static_cast<T *>(final_state);
+      s.B = batch;
+      s.T_ = seqlen;
+      s.H = heads;
+      s.P = head_dim;
+      s.G = groups;
+      s.N = d_state;
+      s.L = chunk;
+      return run_scan<T, T>(s, workspace, workspace_bytes, st);
+    };
+    return dtype == SSD200_F32 ? fill(float{}) : fill(double{});
+  }
+  set_err("ssd200_chunk_scan: dtype %d not supported (F32/F64)", dtype);
+  return SSD200_EINVAL;
+}
+
+int ssd200_embed(const ssd200_dims_t *d, const int64_t *tokens, int rows, const void *embedding,
+                 void *hidden, void *hidden_lp, ssd200_stream_t stream) {
+  int rc = check_dims(d);
+  if (rc) return rc;
+  REQUIRE(tokens && embedding && hidden && rows >= 1, SSD200_EINVAL, "embed: bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (d->dtype == SSD200_F32)
+    embed_kernel<float, float><<<rows, 256, 0, st>>>(tokens, (const float *)embedding, d->d_model,
+                                                     (float *)hidden, nullptr);
+  else if (d->dtype == SSD200_F64)
+    embed_kernel<double, double><<<rows, 256, 0, st>>>(tokens, (const double *)embedding,
+                                                       d->d_model, (double *)hidden, nullptr);
+  else {
+    REQUIRE(hidden_lp, SSD200_EINVAL, "bf16 mode needs hidden_lp");
+    embed_kernel<float, bf16><<<rows, 256, 0, st>>>(tokens, (const bf16 *)embedding, d->d_model,
+                                                    (float *)hidden, (bf16 *)hidden_lp);
+  }
+  LAUNCH_CHECK("embed_kernel");
+  return SSD200_OK;
+}
+
+size_t ssd200_prefill_layer_workspace(const ssd200_dims_t *d, int batch, int seqlen) {
+  if (check_dims(d) || batch < 1 || seqlen < 1) return 0;
+  size_t need = 0;
+  if (d->dtype == SSD200_F64) {
+    PrefillWs<double> o;
+    carve_prefill<double>(d, batch, seqlen, nullptr, 0, o, &need);
+  } else {
+    PrefillWs<float> o;
+    carve_prefill<float>(d, batch, seqlen, nullptr, 0, o, &need);
+  }
+  return need;
+}
+
+int ssd200_prefill_layer(const ssd200_dims_t *d, const ssd200_layer_t *w, void *hidden,
+                         void *hidden_lp, void *ssm_out, void *conv_out, int batch, int seqlen,
+                         void *workspace, size_t workspace_bytes, ssd200_stream_t stream) {
+  int rc = check_dims(d);
+  if (rc) return rc;
+  REQUIRE(w && hidden && ssm_out && batch >= 1 && seqlen >= 1, SSD200_EINVAL,
+          "prefill_layer: bad arguments");
+  REQUIRE(d->conv_kernel == 1 || conv_out, SSD200_EINVAL, "prefill_layer: conv_out is null");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (d->dtype) {
+    case SSD200_F32:
+      return prefill_layer_simt<float>(d, w, (float *)hidden, (float *)ssm_out, (float *)conv_out,
+                                       batch, seqlen, workspace, workspace_bytes, st);
+    case SSD200_F64:
+      return prefill_layer_simt<double>(d, w, (double *)hidden, (double *)ssm_out,
+                                        (double *)conv_out, batch, seqlen, workspace,
+                                        workspace_bytes, st);
+    default:
+      return prefill_layer_bf16(d, w, (float *)hidden, (bf16 *)hidden_lp, (float *)ssm_out,
+                                (float *)conv_out, batch, seqlen, workspace, workspace_bytes, st);
+  }
+}
+
+size_t ssd200_decode_layer_workspace(const ssd200_dims_t *d, int batch) {
+  if (check_dims(d) || batch < 1) return 0;
+  size_t need = 0;
+  if (d->dtype == SSD200_F64) {
+    DecodeWs<double> o;
+    carve_decode<double>(d, batch, nullptr, 0, o, &need);
+  } else {
+    DecodeWs<float> o;
+    carve_decode<float>(d, batch, nullptr, 0, o, &need);
+  }
+  return need;
+}
+
+int ssd200_decode_layer(const ssd200_dims_t *d, const ssd200_layer_t *w, void *hidden,
+                        void *hidden_lp, const void *ssm_in, void *ssm_out, const void *conv_in,
+                        void *conv_out, int batch, void *workspace, size_t workspace_bytes,
+                        ssd200_stream_t stream) {
+  int rc = check_dims(d);
+  if (rc) return rc;
+  REQUIRE(w && hidden && ssm_in && ssm_out && batch >= 1, SSD200_EINVAL,
+          "decode_layer: bad arguments");
+  REQUIRE(d->conv_kernel == 1 || (conv_in && conv_out), SSD200_EINVAL,
+          "decode_layer: conv state is null");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (d->dtype == SSD200_F64)
+    return decode_layer_impl<double>(d, w, (double *)hidden, nullptr, (const double *)ssm_in,
+                                     (double *)ssm_out, (const double *)conv_in,
+                                     (double *)conv_out, batch, workspace, workspace_bytes, st);
+  return decode_layer_impl<float>(d, w, (float *)hidden, (bf16 *)hidden_lp,
+                                  (const float *)ssm_in, (float *)ssm_out,
+                                  (const float *)conv_in, (float *)conv_out, batch, workspace,
+                                  workspace_bytes, st);
+}
+
+size_t ssd200_head_workspace(const ssd200_dims_t *d, int vocab, int rows) {
+  if (check_dims(d) || rows < 1 || vocab < 1) return 0;
+  size_t elt = d->dtype == SSD200_F64 ? 8 : 4;
+  size_t nel = d->dtype == SSD200_BF16 ? 2 : elt;
+  return align_up((size_t)rows * d->d_model * nel) + align_up((size_t)rows * vocab * elt);
+}
+
+int ssd200_head(const ssd200_dims_t *d, int vocab, const void *hidden, int64_t hidden_row_stride,
+                const void *final_norm_w, const void *embedding, void *logits,
+                int64_t *argmax_out, int rows, void *workspace, size_t workspace_bytes,
+                ssd200_stream_t stream) {
+  int rc = check_dims(d);
+  if (rc) return rc;
+  REQUIRE(hidden && final_norm_w && embedding && rows >= 1 && vocab >= 1, SSD200_EINVAL,
+          "head: bad arguments");
+  REQUIRE(logits || argmax_out, SSD200_EINVAL, "head: nothing to compute");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (d->dtype == SSD200_F32)
+    return head_simt<float>(d, vocab, (const float *)hidden, hidden_row_stride,
+                            (const float *)final_norm_w, (const float *)embedding,
+                            (float *)logits, argmax_out, rows, workspace, workspace_bytes, st);
+  if (d->dtype == SSD200_F64)
+    return head_simt<double>(d, vocab, (const double *)hidden, hidden_row_stride,
+                             (const double *)final_norm_w, (const double *)embedding,
+                             (double *)logits, argmax_out, rows, workspace, workspace_bytes, st);
+  return head_bf16(d, vocab, (const float *)hidden, hidden_row_stride,
+                   (const float *)final_norm_w, (const bf16 *)embedding, (float *)logits,
+                   argmax_out, rows, workspace, workspace_bytes, st);
+}
+
+int ssd200_gemm_bf16(const void *A, const void *B, void *C, int M, int N, int K,
+                     ssd200_stream_t stream) {
+  REQUIRE(A && B && C, SSD200_EINVAL, "gemm: null pointer");
+  TcEpilogue ep{};
+  ep.C = C;
+  ep.ldc = N;
+  return tc_gemm<TC_EPI_F32>((const bf16 *)A, K, (const bf16 *)B, K, M, N, K, ep,
+                             static_cast<cudaStream_t>(stream));
+}
+
+uint64_t ssd200_launch_count(void) { return g_launches; }
+
+int ssd200_set_phase_events(void *const *events, int n_phases) {
+  REQUIRE(n_phases >= 0 && n_phases <= 5, SSD200_EINVAL, "n_phases must be in [0, 5]");
+  g_phase_ev = n_phases ? events : nullptr;
+  g_nphase = events ? n_phases : 0;
+  return SSD200_OK;
+}
+
+}  // extern "C"

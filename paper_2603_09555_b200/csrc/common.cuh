@@ -1,0 +1,72 @@
+// Shared device helpers for the ssd200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+
+namespace ssd200 {
+
+using bf16 = __nv_bfloat16;
+
+// ---------------------------------------------------------------- conversions
+template <typename T> __device__ __forceinline__ T from_f(float v) { return static_cast<T>(v); }
+template <> __device__ __forceinline__ bf16 from_f<bf16>(float v) { return __float2bfloat16_rn(v); }
+
+template <typename T, typename S> __device__ __forceinline__ T cvt(S v) { return static_cast<T>(v); }
+template <> __device__ __forceinline__ float cvt<float, bf16>(bf16 v) { return __bfloat162float(v); }
+template <> __device__ __forceinline__ double cvt<double, bf16>(bf16 v) {
+  return (double)__bfloat162float(v);
+}
+template <> __device__ __forceinline__ bf16 cvt<bf16, float>(float v) { return __float2bfloat16_rn(v); }
+template <> __device__ __forceinline__ bf16 cvt<bf16, double>(double v) {
+  return __float2bfloat16_rn((float)v);
+}
+template <> __device__ __forceinline__ bf16 cvt<bf16, bf16>(bf16 v) { return v; }
+
+// ---------------------------------------------------------------- math (precise, no fast-math)
+__device__ __forceinline__ float exp_(float v) { return expf(v); }
+__device__ __forceinline__ double exp_(double v) { return exp(v); }
+__device__ __forceinline__ float log1p_(float v) { return log1pf(v); }
+__device__ __forceinline__ double log1p_(double v) { return log1p(v); }
+__device__ __forceinline__ float sqrt_(float v) { return sqrtf(v); }
+__device__ __forceinline__ double sqrt_(double v) { return sqrt(v); }
+__device__ __forceinline__ float abs_(float v) { return fabsf(v); }
+__device__ __forceinline__ double abs_(double v) { return fabs(v); }
+
+// numerics.py:56-60 — x above 20 passes through; otherwise log1p(exp(x)).
+template <typename T> __device__ __forceinline__ T softplus(T v) {
+  return v > T(20) ? v : log1p_(exp_(v));
+}
+// numerics.py:63-67 — sign-split logistic.
+template <typename T> __device__ __forceinline__ T sigmoid(T v) {
+  T e = exp_(-abs_(v));
+  return v >= T(0) ? T(1) / (T(1) + e) : e / (T(1) + e);
+}
+template <typename T> __device__ __forceinline__ T silu(T v) { return v * sigmoid(v); }
+
+template <typename T> __device__ __forceinline__ T clamp_(T v, T lo, T hi) {
+  return v < lo ? lo : (v > hi ? hi : v);
+}
+
+template <typename T> __device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// block-wide sum; `red` needs blockDim.x/32 slots.  Returns the total to all.
+template <typename T> __device__ __forceinline__ T block_sum(T v, T *red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  T t = T(0);
+  for (int i = 0; i < nw; ++i) t += red[i];
+  return t;
+}
+
+}  // namespace ssd200

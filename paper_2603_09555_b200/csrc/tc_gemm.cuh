@@ -1,0 +1,254 @@
+// Persistent bf16 tensor-core GEMM for sm_100a:  D (M,N) = A (M,K) . B (N,K)^T
+// with fp32 accumulation in TMEM and fused epilogues for the Mamba-2 block:
+//
+//   EPI_F32    store f32                      (tied head logits, decode u)
+//   EPI_BF16   store bf16
+//   EPI_INPROJ columns [0, n_split) -> bf16 [z | xBC]; columns >= n_split are
+//              dt_raw: dt = clip(softplus(acc + dt_bias)) stored f32
+//              (model.py:141-142 + ssd.py:115-136 fused)
+//   EPI_RESID  hidden_f32 += acc, hidden_bf16 = bf16(hidden)  (model.py:168-173)
+//
+// Structure (one CTA per SM, 6 warps):
+//   warp 0      TMA producer: A/B k-blocks (64 bf16 = 128 B rows, SWIZZLE_128B)
+//               into a STAGES-deep smem ring (full/empty mbarriers)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (128 x BN x 16 per instruction), commits free smem stages
+//   warps 2..5  epilogue: tcgen05.ld 32x32b from TMEM -> registers -> global;
+//               two TMEM accumulators so tile i's epilogue overlaps tile i+1's
+//               mainloop.
+#pragma once
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace ssd200 {
+
+enum { TC_EPI_F32 = 0, TC_EPI_BF16 = 1, TC_EPI_INPROJ = 2, TC_EPI_RESID = 3 };
+
+struct TcEpilogue {
+  void *C;        // F32: float*, BF16/INPROJ: bf16*, RESID: float* (hidden)
+  long ldc;       // elements
+  bf16 *C_lp;     // RESID: bf16 shadow (same ldc)
+  int n_split;    // INPROJ: first dt column
+  float *dt;      // INPROJ: (M, H) f32
+  int H;
+  const float *dt_bias;
+  float dt_lo, dt_hi;
+};
+
+template <int BN> struct TcCfg {
+  static constexpr int BM = 128, BK = 64;
+  static constexpr int STAGES = BN >= 256 ? 4 : 6;
+  static constexpr uint32_t A_BYTES = BM * BK * 2;
+  static constexpr uint32_t B_BYTES = BN * BK * 2;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t *>(&v);
+}
+
+template <int EPI>
+__device__ __forceinline__ void tc_store_chunk(const TcEpilogue &ep, const uint32_t (&r)[32],
+                                               int m, int n0, int N) {
+  const bool full = (n0 + 32 <= N);
+  if (EPI == TC_EPI_F32) {
+    float *dst = reinterpret_cast<float *>(ep.C) + (size_t)m * ep.ldc + n0;
+    if (full && ((ep.ldc & 3) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4 *>(dst + j) =
+            make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                        __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+    } else {
+      for (int j = 0; j < 32 && n0 + j < N; ++j) dst[j] = __uint_as_float(r[j]);
+    }
+  } else if (EPI == TC_EPI_BF16 || EPI == TC_EPI_INPROJ) {
+    const int lim = (EPI == TC_EPI_INPROJ) ? ep.n_split : N;
+    bf16 *dst = reinterpret_cast<bf16 *>(ep.C) + (size_t)m * ep.ldc + n0;
+    if (n0 + 32 <= lim && ((ep.ldc & 7) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        uint4 v;
+        v.x = pack_bf16x2(__uint_as_float(r[j]), __uint_as_float(r[j + 1]));
+        v.y = pack_bf16x2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+        v.z = pack_bf16x2(__uint_as_float(r[j + 4]), __uint_as_float(r[j + 5]));
+        v.w = pack_bf16x2(__uint_as_float(r[j + 6]), __uint_as_float(r[j + 7]));
+        *reinterpret_cast<uint4 *>(dst + j) = v;
+      }
+    } else {
+      for (int j = 0; j < 32 && n0 + j < N; ++j) {
+        const int n = n0 + j;
+        const float acc = __uint_as_float(r[j]);
+        if (n < lim) {
+          dst[j] = __float2bfloat16_rn(acc);
+        } else if (EPI == TC_EPI_INPROJ) {
+          const int h = n - ep.n_split;
+          ep.dt[(size_t)m * ep.H + h] =
+              clamp_(softplus(acc + ep.dt_bias[h]), ep.dt_lo, ep.dt_hi);
+        }
+      }
+    }
+  } else {  // TC_EPI_RESID
+    float *dst = reinterpret_cast<float *>(ep.C) + (size_t)m * ep.ldc + n0;
+    bf16 *lp = ep.C_lp + (size_t)m * ep.ldc + n0;
+    if (full && ((ep.ldc & 7) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        float4 a = *reinterpret_cast<float4 *>(dst + j);
+        float4 b = *reinterpret_cast<float4 *>(dst + j + 4);
+        a.x += __uint_as_float(r[j + 0]);
+        a.y += __uint_as_float(r[j + 1]);
+        a.z += __uint_as_float(r[j + 2]);
+        a.w += __uint_as_float(r[j + 3]);
+        b.x += __uint_as_float(r[j + 4]);
+        b.y += __uint_as_float(r[j + 5]);
+        b.z += __uint_as_float(r[j + 6]);
+        b.w += __uint_as_float(r[j + 7]);
+        *reinterpret_cast<float4 *>(dst + j) = a;
+        *reinterpret_cast<float4 *>(dst + j + 4) = b;
+        uint4 v;
+        v.x = pack_bf16x2(a.x, a.y);
+        v.y = pack_bf16x2(a.z, a.w);
+        v.z = pack_bf16x2(b.x, b.y);
+        v.w = pack_bf16x2(b.z, b.w);
+        *reinterpret_cast<uint4 *>(lp + j) = v;
+      }
+    } else {
+      for (int j = 0; j < 32 && n0 + j < N; ++j) {
+        float v = dst[j] + __uint_as_float(r[j]);
+        dst[j] = v;
+        lp[j] = __float2bfloat16_rn(v);
+      }
+    }
+  }
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(192, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   int M, int N, int K, TcEpilogue ep) {
+  using Cfg = TcCfg<BN>;
+  constexpr int BM = Cfg::BM, BK = Cfg::BK, STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t *sA = smem;
+  uint8_t *sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sB + STAGES * Cfg::B_BYTES);
+  uint64_t *empty = full + STAGES;
+  uint64_t *tfull = empty + STAGES;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_tiles = ((M + BM - 1) / BM) * num_n;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tmA);
+    sm100::tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      sm100::mbar_init(&tfull[s], 1);
+      sm100::mbar_init(&tempty[s], 4);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_blk = tile / num_n, n_blk = tile % num_n;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          sm100::mbar_wait(&empty[s], ph ^ 1);
+          sm100::mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+          sm100::tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * BK, m_blk * BM);
+          sm100::tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, &full[s], kb * BK, n_blk * BN);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = sm100::idesc_bf16(BM, BN, false, false);
+      int s = 0;
+      uint32_t ph = 0;
+      int local = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+        const int as = local & 1;
+        const uint32_t aph = (local >> 1) & 1;
+        sm100::mbar_wait(&tempty[as], aph ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + as * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          sm100::mbar_wait(&full[s], ph);
+          sm100::tc_fence_after();
+          const uint32_t a0 = sm100::smem_u32(sA + s * Cfg::A_BYTES);
+          const uint32_t b0 = sm100::smem_u32(sB + s * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = sm100::sw128_desc(a0 + k * 32, 16, 1024);
+            const uint64_t bd = sm100::sw128_desc(b0 + k * 32, 16, 1024);
+            sm100::mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          sm100::mma_commit(&empty[s]);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        sm100::mma_commit(&tfull[as]);
+      }
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int m_blk = tile / num_n, n_blk = tile % num_n;
+      const int as = local & 1;
+      const uint32_t aph = (local >> 1) & 1;
+      sm100::mbar_wait(&tfull[as], aph);
+      sm100::tc_fence_after();
+      const int m = m_blk * BM + q * 32 + lane;
+      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
+#pragma unroll 1
+      for (int cc = 0; cc < BN; cc += 32) {
+        const int n0 = n_blk * BN + cc;
+        if (n0 >= N) break;  // warp-uniform
+        uint32_t r[32];
+        sm100::tmem_ld32(trow + cc, r);
+        sm100::tmem_ld_wait();
+        if (m < M) tc_store_chunk<EPI>(ep, r, m, n0, N);
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&tempty[as]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+  }
+}
+
+}  // namespace ssd200

@@ -1,0 +1,171 @@
+"""Cached decode over the C-ABI — mirrors ``cache_init``, ``decode_step`` and
+``generate`` (decode.py:49-194).
+
+``decode_step`` is functional like the reference (a new cache is returned;
+the input cache is not mutated).  ``generate`` updates one cache in place and
+replays the whole per-token step (embed -> every layer -> norm -> head ->
+argmax -> token feedback) as ONE CUDA graph, G-1 times, with no host
+synchronisation until the tokens are read back.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _abi
+from .cache import GenerationResult, Mamba2Cache, state_dtype
+from .config import ModelConfig
+from .model import PolicyAudit, _audit, _Runner, check_tokens, prefill
+from .params import ModelParams
+
+
+def cache_init(cfg: ModelConfig, batch: int, device="cuda") -> Mamba2Cache:
+    """decode.py:49-62 — all-zero cache."""
+    if batch < 1:
+        raise ValueError("batch must be >= 1")
+    return Mamba2Cache.empty(cfg, batch, device=device, zero=True)
+
+
+def _step_into(r: _Runner, cfg, tok, cache_in: Mamba2Cache, cache_out: Mamba2Cache,
+               logits=None, argmax=None):
+    B = tok.shape[0]
+    hidden, lp = r.embed(tok)
+    for i in range(cfg.n_layers):
+        r.decode_layer(
+            i, hidden, lp, cache_in.ssm_all[i], cache_out.ssm_all[i],
+            cache_in.conv_all[i], cache_out.conv_all[i], B,
+        )
+    r.head(hidden, cfg.d_model, B, logits=logits, argmax=argmax)
+
+
+def decode_step(params: ModelParams, cache: Mamba2Cache, token, cfg: ModelConfig,
+                audit: PolicyAudit | None = None):
+    """decode.py:77-144 — (B,) ids -> ((B, vocab) logits, new cache)."""
+    dev = params.device
+    tok = check_tokens(token, cfg, 1, dev)
+    if cache.batch != tok.shape[0]:
+        raise ValueError(f"cache batch {cache.batch} != token batch {tok.shape[0]}")
+    r = _Runner(params, cfg)
+    new = Mamba2Cache.empty(cfg, tok.shape[0], device=dev, zero=False)
+    logits = torch.empty((tok.shape[0], cfg.vocab_size), dtype=state_dtype(cfg), device=dev)
+    _step_into(r, cfg, tok, cache, new, logits=logits)
+    for _ in range(cfg.n_layers):
+        _audit(audit, cfg)
+    return logits, new
+
+
+class GreedyDecoder:
+    """In-place greedy decoding loop captured as one CUDA graph per step.
+
+    The graph reads the current token from ``self.tok`` and writes the next
+    greedy token back into it, updates the cache in place, and records the
+    token (and optionally the logits) at the device-side step counter."""
+
+    def __init__(self, params: ModelParams, cfg: ModelConfig, cache: Mamba2Cache, gen_len: int,
+                 keep_logits: bool = False, use_graph: bool = True):
+        self.cfg = cfg
+        self.dev = params.device
+        B = cache.batch
+        self.B = B
+        self.cache = cache
+        self.runner = _Runner(params, cfg)
+        self.tok = torch.zeros((B,), dtype=torch.int64, device=self.dev)
+        self.tokens = torch.zeros((B, gen_len), dtype=torch.int64, device=self.dev)
+        self.logits = torch.empty((B, cfg.vocab_size), dtype=state_dtype(cfg), device=self.dev)
+        self.kept = (
+            torch.empty((B, gen_len, cfg.vocab_size), dtype=state_dtype(cfg), device=self.dev)
+            if keep_logits
+            else None
+        )
+        self.step_idx = torch.zeros((1,), dtype=torch.int64, device=self.dev)
+        self.graph = None
+        self.use_graph = use_graph
+
+    def _body(self):
+        cfg = self.cfg
+        _step_into(self.runner, cfg, self.tok, self.cache, self.cache, logits=self.logits,
+                   argmax=self.tok)
+        # bookkeeping: tokens[:, step] = tok; step += 1
+        self.tokens.index_copy_(1, self.step_idx, self.tok.view(-1, 1))
+        if self.kept is not None:
+            self.kept.index_copy_(1, self.step_idx, self.logits.unsqueeze(1))
+        self.step_idx.add_(1)
+
+    def capture(self):
+        # warm up once on a side stream (workspace allocation, attributes)
+        saved = (self.cache.copy(), self.tok.clone(), self.tokens.clone(), self.step_idx.clone())
+        s = torch.cuda.Stream(device=self.dev)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.runner.stream = _abi.stream_handle(s)
+            self._body()
+        torch.cuda.current_stream().wait_stream(s)
+        # restore the state the warm-up step consumed
+        self.cache.ssm_all.copy_(saved[0].ssm_all)
+        self.cache.conv_all.copy_(saved[0].conv_all)
+        self.tok.copy_(saved[1])
+        self.tokens.copy_(saved[2])
+        self.step_idx.copy_(saved[3])
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.runner.stream = _abi.stream_handle()
+            self._body()
+        self.graph = g
+        self.runner.stream = _abi.stream_handle()
+
+    def step(self):
+        if self.use_graph:
+            if self.graph is None:
+                self.capture()
+            self.graph.replay()
+        else:
+            self.runner.stream = _abi.stream_handle()
+            self._body()
+
+
+def generate(params: ModelParams, prompt, gen_len: int, mode: str = "cached",
+             cfg: ModelConfig | None = None, keep_logits: bool = False,
+             use_graph: bool = True) -> GenerationResult:
+    """decode.py:147-194 — greedy generation of gen_len tokens after (B, P)
+    prompt.  cached: one prefill then gen_len-1 in-place steps (graph
+    replays); non_cached: re-prefill the whole prefix per token (the
+    quadratic baseline).  Ties resolve to the lowest id."""
+    if cfg is None:
+        raise ValueError("cfg is required")
+    if gen_len < 1:
+        raise ValueError("gen_len must be >= 1")
+    if mode not in ("cached", "non_cached"):
+        raise ValueError(f"unknown mode {mode!r}")
+    dev = params.device
+    ptok = check_tokens(prompt, cfg, 2, dev)
+    B = ptok.shape[0]
+
+    if mode == "non_cached":
+        tokens = torch.zeros((B, gen_len), dtype=torch.int64, device=dev)
+        kept = (
+            torch.empty((B, gen_len, cfg.vocab_size), dtype=state_dtype(cfg), device=dev)
+            if keep_logits
+            else None
+        )
+        seq = ptok
+        pick = torch.empty((B,), dtype=torch.int64, device=dev)
+        for g in range(gen_len):
+            last, _ = prefill(params, seq, cfg, logits="last", argmax_out=pick)
+            if kept is not None:
+                kept[:, g] = last
+            tokens[:, g] = pick
+            seq = torch.cat([ptok, tokens[:, : g + 1]], dim=1)
+        return GenerationResult(tokens=tokens, steps=gen_len, per_step_logits=kept)
+
+    pick = torch.empty((B,), dtype=torch.int64, device=dev)
+    last, cache = prefill(params, ptok, cfg, logits="last", argmax_out=pick)
+    dec = GreedyDecoder(params, cfg, cache, gen_len, keep_logits=keep_logits, use_graph=use_graph)
+    dec.tok.copy_(pick)
+    dec.tokens[:, 0] = pick
+    if dec.kept is not None:
+        dec.kept[:, 0] = last
+    dec.step_idx.fill_(1)
+    for _ in range(gen_len - 1):
+        dec.step()
+    return GenerationResult(tokens=dec.tokens, steps=gen_len, per_step_logits=dec.kept)

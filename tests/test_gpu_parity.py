@@ -1,0 +1,264 @@
+"""Parity of the CUDA path against the reference (golden vectors) and the CPU
+oracle.  GPU only; every call goes through libssd200.so."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from conftest import SMALL_MODELS, golden, make_instance, small_config
+
+pytestmark = pytest.mark.gpu
+
+F64_GATE = 1e-10
+F32_RTOL, F32_ATOL = 1e-5, 2e-4  # test_acceptance.py:34-38
+CACHED_FULL_F32 = 1.3e-4
+
+
+def _np(t):
+    return t.detach().cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+
+
+# ----------------------------------------------------------- chunked scan
+
+
+@pytest.mark.parametrize("i", range(8))
+def test_chunk_scan_vs_golden(i):
+    import paper_2603_09555_b200 as m
+
+    z = golden("ssd_cases.npz")
+    g = lambda k: z[f"{i}.{k}"]  # noqa: E731
+    init = g("init") if int(g("has_init")) else None
+    L = int(g("L"))
+    for dt_, tag in ((np.float64, "f64"), (np.float32, "f32")):
+        inp = m.SsdInputs(X=g("X").astype(dt_), dt=g("dt").astype(dt_), a=g("a").astype(dt_),
+                          Bmat=g("B").astype(dt_), Cmat=g("C").astype(dt_))
+        out = m.ssd_forward(inp, L, initial_state=None if init is None else init.astype(dt_))
+        Y, fin = _np(out.Y), _np(out.final_state)
+        ys, hs = z[f"{i}.Y_seq"], z[f"{i}.final_seq"]
+        if tag == "f64":
+            assert np.abs(Y - ys).max() <= F64_GATE
+            assert np.abs(fin - hs).max() <= F64_GATE * max(1.0, np.abs(hs).max())
+        else:
+            assert np.all(np.abs(Y - ys) <= F32_ATOL + F32_RTOL * np.abs(ys))
+            assert np.all(np.abs(fin - hs) <= F32_ATOL + F32_RTOL * np.abs(hs))
+
+
+def test_chunk_scan_acceptance_pool():
+    """Criterion 1 (test_acceptance.py:70-94) on a 60-instance slice of the
+    same distribution, chunk sizes from {1,4,16,64,256}."""
+    import paper_2603_09555_b200 as m
+
+    rng = np.random.default_rng(2024)
+    pick = np.random.default_rng(77)
+    for _ in range(60):
+        heads = int(rng.integers(1, 5))
+        groups = heads if rng.integers(2) else 1
+        inst = make_instance(rng, batch=int(rng.integers(1, 3)), seq=int(rng.integers(1, 513)),
+                             heads=heads, pdim=int(rng.integers(1, 9)),
+                             ndim=int(rng.integers(1, 9)), groups=groups)
+        L = int(pick.choice((1, 4, 16, 64, 256)))
+        ys, hs = orc.sequential_scan(inst["X"], inst["dt"], inst["a"], inst["B"], inst["C"])
+        out = m.ssd_forward(m.SsdInputs(inst["X"], inst["dt"], inst["a"], inst["B"], inst["C"]), L)
+        assert np.abs(_np(out.Y) - ys).max() <= F64_GATE
+        assert np.abs(_np(out.final_state) - hs).max() <= F64_GATE
+        f = {k: v.astype(np.float32) for k, v in inst.items()}
+        out32 = m.ssd_forward(m.SsdInputs(f["X"], f["dt"], f["a"], f["B"], f["C"]), L)
+        assert np.all(np.abs(_np(out32.Y) - ys) <= F32_ATOL + F32_RTOL * np.abs(ys))
+
+
+def test_chunk_invariance_and_masks():
+    """Criterion 2 / 6: results independent of L, masks bitwise identical."""
+    import paper_2603_09555_b200 as m
+
+    rng = np.random.default_rng(5)
+    inst = make_instance(rng, batch=2, seq=300, heads=3, pdim=8, ndim=8)
+    si = m.SsdInputs(inst["X"], inst["dt"], inst["a"], inst["B"], inst["C"])
+    base = m.ssd_forward(si, 1)
+    for L in (4, 16, 64, 256):
+        o = m.ssd_forward(si, L)
+        assert (o.Y - base.Y).abs().max().item() <= F64_GATE
+    s = m.ssd_forward(si, 16, mask_strategy="static")
+    r = m.ssd_forward(si, 16, mask_strategy="rowwise")
+    assert torch.equal(s.Y, r.Y) and torch.equal(s.final_state, r.final_state)
+
+
+def test_chunk_scan_validation():
+    import paper_2603_09555_b200 as m
+
+    rng = np.random.default_rng(3)
+    inst = make_instance(rng)
+    with pytest.raises(ValueError):
+        m.ssd_forward(m.SsdInputs(inst["X"], -inst["dt"], inst["a"], inst["B"], inst["C"]), 4)
+    with pytest.raises(ValueError):
+        m.ssd_forward(m.SsdInputs(inst["X"], inst["dt"], -inst["a"], inst["B"], inst["C"]), 4)
+    with pytest.raises(ValueError):
+        m.ssd_forward(m.SsdInputs(inst["X"], inst["dt"], inst["a"], inst["B"], inst["C"]), 0)
+
+
+# ----------------------------------------------------------- small models
+
+
+@pytest.mark.parametrize("name,ov,seed", SMALL_MODELS)
+@pytest.mark.parametrize("comp", ["f32", "f64"])
+def test_small_model_vs_golden(name, ov, seed, comp):
+    import paper_2603_09555_b200 as m
+
+    z = golden("small_model.npz")
+    cfg = small_config(**ov).with_policy(compute=comp)
+    params = m.random_init(cfg, seed)
+    key = f"{name}.{comp}"
+    tol = 1e-10 if comp == "f64" else 2e-5
+    logits, cache = m.prefill(params, z[f"{key}.tokens"], cfg)
+    ref = z[f"{key}.logits"]
+    assert np.abs(_np(logits) - ref).max() <= tol * max(1.0, np.abs(ref).max())
+    assert np.abs(_np(cache.ssm_all) - z[f"{key}.ssm"]).max() <= tol * max(1.0, np.abs(z[f"{key}.ssm"]).max())
+    assert np.abs(_np(cache.conv_all) - z[f"{key}.conv"]).max() <= tol
+    before = cache.to_bytes()
+    sl, c2 = m.decode_step(params, cache, z[f"{key}.next"], cfg)
+    assert cache.to_bytes() == before  # input cache not mutated (test_decode.py:107-113)
+    ref = z[f"{key}.step_logits"]
+    assert np.abs(_np(sl) - ref).max() <= tol * max(1.0, np.abs(ref).max())
+    assert np.abs(_np(c2.ssm_all) - z[f"{key}.step_ssm"]).max() <= tol * max(1.0, np.abs(z[f"{key}.step_ssm"]).max())
+    assert np.abs(_np(c2.conv_all) - z[f"{key}.step_conv"]).max() <= tol
+    for use_graph in (True, False):
+        res = m.generate(params, z[f"{key}.prompt"], 64, cfg=cfg, use_graph=use_graph)
+        assert np.array_equal(_np(res.tokens), z[f"{key}.gen"])
+
+
+@pytest.mark.parametrize("comp", ["f32", "f64"])
+def test_cached_vs_full(comp):
+    """Criterion 3 (test_acceptance.py:117-140) on the device."""
+    import paper_2603_09555_b200 as m
+
+    gate = CACHED_FULL_F32 if comp == "f32" else 1e-9
+    cfg = small_config(d_model=64, n_layers=4, chunk_size=16).with_policy(compute=comp)
+    params = m.random_init(cfg, 1)
+    rng = np.random.default_rng(101)
+    for prompt_len in (1, 16, 33):
+        for gen in (1, 8, 64):
+            toks = rng.integers(0, cfg.vocab_size, size=(1, prompt_len + gen))
+            full, _ = m.prefill(params, toks, cfg)
+            logits, cache = m.prefill(params, toks[:, :prompt_len], cfg)
+            for g in range(gen):
+                logits, cache = m.decode_step(params, cache, toks[:, prompt_len + g], cfg)
+            assert (logits - full[:, -1]).abs().max().item() <= gate
+
+
+def test_non_cached_matches_cached():
+    import paper_2603_09555_b200 as m
+
+    cfg = small_config(d_model=16, head_dim=4, d_state=4, chunk_size=8)
+    params = m.random_init(cfg, 300)
+    prompt = np.random.default_rng(400).integers(0, cfg.vocab_size, size=(1, 16))
+    a = m.generate(params, prompt, 32, mode="cached", cfg=cfg)
+    b = m.generate(params, prompt, 32, mode="non_cached", cfg=cfg)
+    assert torch.equal(a.tokens, b.tokens)
+
+
+def test_batch_invariance_bitwise():
+    """Rows are independent: a batch-sharded run equals the full run bitwise
+    (analogue of test_model.py:131-140; the basis of the batch sharding)."""
+    import paper_2603_09555_b200 as m
+
+    cfg = small_config(d_model=64, n_layers=2)
+    params = m.random_init(cfg, 9)
+    toks = np.random.default_rng(8).integers(0, cfg.vocab_size, size=(4, 37))
+    full, cache = m.prefill(params, toks, cfg)
+    for lo, hi in ((0, 2), (2, 4), (1, 3)):
+        part, pc = m.prefill(params, toks[lo:hi], cfg)
+        assert torch.equal(part, full[lo:hi])
+        assert torch.equal(pc.ssm_all, cache.ssm_all[:, lo:hi])
+
+
+# ----------------------------------------------------------- config 1 (130M f32)
+
+
+def test_c1_130m_tokens_identical():
+    """Config 1: 130M random_init(0) f32, prompt 512, generate(65): greedy
+    tokens identical to the reference over all 64 decode steps; logits within
+    the Table-5 gates (oracle.py:118)."""
+    import paper_2603_09555_b200 as m
+
+    z = golden("c1_130m.npz")
+    cfg = m.ModelConfig(vocab_size=50288, d_model=768, n_layers=24)
+    params = m.random_init(cfg, 0)
+    res = m.generate(params, z["prompt"], 65, cfg=cfg, keep_logits=True)
+    assert np.array_equal(_np(res.tokens), z["tokens"])
+    lg = _np(res.per_step_logits[0])
+    for got, ref in ((lg[0], z["logits_first"]), (lg[-1], z["logits_last"])):
+        assert np.all(np.abs(got - ref) <= F32_ATOL + F32_RTOL * np.abs(ref))
+    # hidden states after layer 0 within fp32 rounding (rel 1e-4, north_star)
+    hidden0 = params.embedding[torch.as_tensor(z["prompt"]).cuda()]
+    h1, s1, c1 = m.block_forward(params.layers[0], hidden0, cfg)
+    rows = _np(h1[0, [0, 1, 255, 256, 510, 511]])
+    ref = z["layer0_hidden_rows"]
+    assert np.linalg.norm(rows - ref) / np.linalg.norm(ref) <= 1e-4
+    assert np.all(np.abs(rows - ref) <= 1e-4 * np.abs(ref) + 1e-4 * np.abs(ref).max())
+    st = _np(s1[0, 0])
+    assert np.linalg.norm(st - z["layer0_state_head0"]) / np.linalg.norm(z["layer0_state_head0"]) <= 1e-4
+    assert np.array_equal(_np(c1[0]), z["layer0_conv_tail"])
+
+
+# ----------------------------------------------------------- bf16 tensor-core mode
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 500, 1024), (7, 3352, 768), (1000, 1024, 2048), (256, 50288, 256)])
+def test_tc_gemm_matches_torch(M, N, K):
+    from paper_2603_09555_b200 import _abi
+
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    C = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    _abi.check(_abi.lib().ssd200_gemm_bf16(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K,
+                                           _abi.stream_handle()), "gemm")
+    ref = A.float() @ B.float().t()
+    err = (C - ref).abs().max().item()
+    assert err <= 1e-3 * max(1.0, ref.abs().max().item()), err
+
+
+BF16_BOUND = 1e-2  # stated bf16 bound: logits/hidden rel-norm vs f32 ref on bf16-rounded weights
+
+
+def _bf16_cfg(**kw):
+    from paper_2603_09555_b200 import ElemPolicy, ModelConfig
+
+    base = dict(vocab_size=1000, d_model=256, n_layers=2, norm_eps=1e-5)
+    base.update(kw)
+    return ModelConfig(policy=ElemPolicy(compute="bf16"), **base)
+
+
+def test_bf16_prefill_vs_oracle():
+    import paper_2603_09555_b200 as m
+
+    cfg = _bf16_cfg()
+    host = m.random_init_host(cfg, 4)
+    params = m.from_reference(host, cfg)
+    toks = np.random.default_rng(5).integers(0, cfg.vocab_size, size=(2, 300))
+    logits, cache = m.prefill(params, toks, cfg)
+    ref_logits, ref_ssm, _ = orc.prefill(orc.round_weights_bf16(host), toks, cfg.with_policy(compute="f32"))
+    got = _np(logits)
+    rel = np.linalg.norm(got - ref_logits) / np.linalg.norm(ref_logits)
+    assert rel <= BF16_BOUND, rel
+    rs = np.stack(ref_ssm)
+    rel_s = np.linalg.norm(_np(cache.ssm_all) - rs) / np.linalg.norm(rs)
+    assert rel_s <= BF16_BOUND, rel_s
+
+
+def test_bf16_decode_vs_oracle():
+    import paper_2603_09555_b200 as m
+
+    cfg = _bf16_cfg()
+    host = m.random_init_host(cfg, 6)
+    params = m.from_reference(host, cfg)
+    rng = np.random.default_rng(7)
+    for B in (1, 3, 20):
+        toks = rng.integers(0, cfg.vocab_size, size=(B, 40))
+        _, cache = m.prefill(params, toks[:, :39], cfg, logits=None)
+        sl, _ = m.decode_step(params, cache, toks[:, 39], cfg)
+        ref_full = orc.prefill(orc.round_weights_bf16(host), toks, cfg.with_policy(compute="f32"))[0][:, -1]
+        rel = np.linalg.norm(_np(sl) - ref_full) / np.linalg.norm(ref_full)
+        assert rel <= BF16_BOUND, (B, rel)
