@@ -1,0 +1,514 @@
+"""Benchmark of the Mamba-2 SSD hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload prefill|decode] [--model 370m] [--batch B] [--seqlen T]
+
+Headline (BASELINE.json configs[1]): Mamba-2 370M bf16 chunked-SSD prefill,
+per-GPU batch B x T tokens, one step = one full prefill (embed, 48 blocks,
+final norm, tied head on the last position) over a batch already resident in
+HBM.  ``value`` = tokens/s summed over ranks (weak scaling: batch-sharded,
+no collective on the data path).  ``e2e`` = the same metric through the
+public API ``prefill`` with the token ids copied from pinned host memory
+and the last-position logits copied back, inside the timed region.
+
+The JSON line also carries: ``roofline`` for the dominant kernel (timed live
+with CUDA events around every launch of that phase inside the timed region),
+per-phase time shares, ``cpu_baseline`` (the numpy oracle port of the
+reference timed on this host, bounded sample, rank 0 at N=1), ``decode``
+(1.3B cached decode: tok/s and HBM GB/s of a CUDA-graph step), ``clocks``
+sampled by nvidia-smi during the timed region and ``gpu_launches``.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port; /root/reference is not on the GPU box) on this host's cores.
+"""
+
+from __future__ import annotations
+
+import os
+
+# host threads for the CPU legs must be fixed before numpy loads BLAS
+_NCPU = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, str(_NCPU))
+
+import argparse  # noqa: E402
+import ctypes  # noqa: E402
+import json  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import threading  # noqa: E402
+import time  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PHASES = ("in_proj", "conv", "scan", "gated_norm", "out_proj")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--workload", default="prefill", choices=("prefill", "decode"))
+    ap.add_argument("--model", default="370m")
+    ap.add_argument("--batch", type=int, default=4, help="per-GPU batch")
+    ap.add_argument("--seqlen", type=int, default=8192)
+    ap.add_argument("--decode-model", default="1.3b")
+    ap.add_argument("--decode-batch", type=int, default=1)
+    ap.add_argument("--decode-steps", type=int, default=64)
+    ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- distributed
+
+
+def dist_setup(n):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    import torch
+
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = (
+        "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+        "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+        "clocks_event_reasons.sw_power_cap"
+    )
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
+            )
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- peaks
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return {"hbm_gbs": m["hbm_gbs"], "bf16_tflops": m["bf16_tflops"],
+                "bf16_tflops_sustained": m.get("bf16_tflops_sustained", m["bf16_tflops"]),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    except (OSError, KeyError, ValueError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "source": "fallback (B200_PROFILING.md)"}
+
+
+def traffic_from_profiles(kernel_key):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(kernel_key)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------- CPU legs
+
+
+def cpu_prefill_sample(model, T=2048, layers=1):
+    """Reference algorithm (numpy oracle port) on a bounded sample: `layers`
+    blocks of `model` at (B=1, T) + the tied head on the last position.
+    Returns (tok/s extrapolated linearly in n_layers, seconds, description)."""
+    import oracle as orc
+    from paper_2603_09555_b200 import named_config, random_init_host
+
+    cfg = named_config(model, compute="f32", n_layers=layers)
+    full = named_config(model, compute="f32")
+    host = random_init_host(cfg, 0)
+    toks = np.random.default_rng(0).integers(0, cfg.vocab_size, size=(1, T))
+    hidden = host.embedding[toks]
+    orc.block(host.layers[0], hidden[:, :256], cfg)  # warm
+    t0 = time.perf_counter()
+    h = hidden
+    for lyr in host.layers:
+        h, _, _ = orc.block(lyr, h, cfg)
+    t_layers = (time.perf_counter() - t0) / layers
+    t1 = time.perf_counter()
+    normed = orc.rms_norm(h[:, -1], host.final_norm_w, cfg.norm_eps)
+    _ = normed @ host.embedding.T
+    t_head = time.perf_counter() - t1
+    per_seq = full.n_layers * t_layers + t_head
+    desc = (f"numpy oracle port of ssd_engine.block_forward: {layers} block(s) of {model} "
+            f"f32 at B=1,T={T} ({t_layers:.2f} s/block) + last-row head, extrapolated x{full.n_layers} layers")
+    return T / per_seq, t_layers * layers + t_head, desc
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    K, W = args.steps, args.warmup
+    T = 1024 if args.seqlen > 1024 else args.seqlen
+    vals = []
+    for i in range(W + K):
+        v, _, desc = cpu_prefill_sample(args.model, T=T, layers=1)
+        if i >= W:
+            vals.append(v)
+    val = float(np.mean(vals))
+    line = {
+        "impl": "reference",
+        "metric": f"prefill_tokens_per_s[{args.model}]",
+        "value": val,
+        "unit": "tok/s",
+        "n_gpus": args.gpus,
+        "steps": K,
+        "warmup": W,
+        "higher_is_better": True,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"Mamba-2 {args.model} prefill (reference CPU path, numpy oracle port)",
+                   "batch_per_gpu": args.batch, "seq_len": args.seqlen, "sample_seq_len": T},
+        "cpu_baseline": {"value": val, "unit": "tok/s", "cores": _NCPU, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": val, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "vs_baseline": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU legs
+
+
+def make_events(n):
+    import torch
+
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+    for e in evs:
+        e.record()
+    torch.cuda.synchronize()
+    return evs
+
+
+def run_prefill(args, rank, world, local):
+    import torch
+
+    import paper_2603_09555_b200 as m
+    from paper_2603_09555_b200 import _abi, model as mmod
+
+    cfg = m.named_config(args.model, compute="bf16")
+    params = m.synthetic_init(cfg, seed=1234 + rank, device=f"cuda:{local}")
+    B, T = args.batch, args.seqlen
+    g = torch.Generator(device="cpu").manual_seed(rank)
+    host_tok = torch.randint(0, cfg.vocab_size, (B, T), generator=g, dtype=torch.int64).pin_memory()
+    dev_tok = host_tok.cuda()
+    lib = _abi.lib()
+
+    # per-phase CUDA events around every layer's phases (5 phases x 2)
+    L = cfg.n_layers
+    K, W = args.steps, args.warmup
+    ev = make_events(K * L * 10)
+    ev_arr = (ctypes.c_void_p * (K * L * 10))(*[e.cuda_event for e in ev])
+
+    class Hook:
+        step = -1
+
+    orig = mmod._Runner.prefill_layer
+
+    def timed_layer(self, i, *a, **kw):
+        if Hook.step >= 0:
+            base = ctypes.addressof(ev_arr) + (Hook.step * L + i) * 10 * ctypes.sizeof(ctypes.c_void_p)
+            lib.ssd200_set_phase_events(ctypes.c_void_p(base), 5)
+        try:
+            return orig(self, i, *a, **kw)
+        finally:
+            lib.ssd200_set_phase_events(None, 0)
+
+    mmod._Runner.prefill_layer = timed_layer
+
+    def step():
+        return m.prefill(params, dev_tok, cfg, logits="last")
+
+    for _ in range(W):
+        step()
+    barrier(world)
+    n0 = lib.ssd200_launch_count()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record()
+        for k in range(K):
+            Hook.step = k
+            step()
+        Hook.step = -1
+        stop.record()
+        torch.cuda.synchronize()
+    launches = lib.ssd200_launch_count() - n0
+    ms = start.elapsed_time(stop) / K
+    mmod._Runner.prefill_layer = orig
+    ms_max = max_over_ranks(ms, world)
+    tokens_total = B * T * world
+    value = tokens_total / (ms_max / 1e3)
+
+    # phase totals (ms per step, summed over layers)
+    phase_ms = np.zeros(5)
+    for k in range(K):
+        for i in range(L):
+            for p in range(5):
+                b = ev[(k * L + i) * 10 + 2 * p]
+                e = ev[(k * L + i) * 10 + 2 * p + 1]
+                phase_ms[p] += b.elapsed_time(e)
+    phase_ms /= K
+
+    # e2e through the public API: pinned host ids -> device, logits -> host
+    host_out = torch.empty((B, cfg.vocab_size), dtype=torch.float32).pin_memory()
+    barrier(world)
+    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s2.record()
+    for k in range(K):
+        tok = host_tok.to(f"cuda:{local}", non_blocking=True)
+        lg, _ = m.prefill(params, tok, cfg, logits="last")
+        host_out.copy_(lg, non_blocking=True)
+    e2.record()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(s2.elapsed_time(e2) / K, world)
+
+    # the reference FLOP formula (cost.py:79-98) with the head on the last row
+    flops_step = m.flops_prefill(cfg, T, B, head_rows=1)
+    pk = peaks()
+    # dominant kernel: the phase with the largest share
+    dom = int(np.argmax(phase_ms))
+    per_layer = m.cost.flops_prefill_layer(cfg, T)
+    phase_flops = {
+        0: B * per_layer["in_proj"],
+        1: B * per_layer["conv"],
+        2: B * (per_layer["ssd_intra"] + per_layer["ssd_states"] + per_layer["ssd_inter"] + per_layer["ssd_cross"]),
+        3: 0,
+        4: B * per_layer["out_proj"],
+    }
+    launch_ms = phase_ms[dom] / L
+    achieved = phase_flops[dom] / (launch_ms / 1e3) / 1e12 if phase_flops[dom] else None
+    peak = pk["bf16_tflops_sustained"]
+    kernel_key = {0: "tc_gemm_kernel<256,2>", 1: "conv_silu_prefill", 2: "ssd_scan", 3: "gated_norm_kernel", 4: "tc_gemm_kernel<256,3>"}[dom]
+    roof = {
+        "kernel": f"{PHASES[dom]} ({kernel_key})",
+        "bound": "tensor",
+        "achieved": achieved,
+        "peak": peak,
+        "unit": "TFLOP/s",
+        "frac": (achieved / peak) if achieved else None,
+        "traffic": traffic_from_profiles(kernel_key),
+        "algorithmic_flops_per_launch": phase_flops[dom],
+        "avg_launch_ms": launch_ms,
+        "peak_source": pk["source"] + ", sustained (kernel timed inside a long step)",
+    }
+    step_tflops = flops_step / (ms_max / 1e3) / 1e12
+    return {
+        "value": value,
+        "ms": ms_max,
+        "e2e_ms": e2e_ms,
+        "e2e_value": tokens_total / (e2e_ms / 1e3),
+        "h2d": B * T * 8,
+        "d2h": B * cfg.vocab_size * 4,
+        "launches": launches,
+        "roofline": roof,
+        "phases_ms": {PHASES[p]: float(phase_ms[p]) for p in range(5)},
+        "step_tflops_per_gpu": step_tflops / world,
+        "step_mfu": step_tflops / world / pk["bf16_tflops"],
+        "clocks": clk.summary(),
+        "flops_step": flops_step,
+    }
+
+
+def run_decode(args, local):
+    """1.3B cached decode: one CUDA-graph step (all layers + head + argmax)
+    replayed; HBM bytes = weights once + state read/write + logits."""
+    import torch
+
+    import paper_2603_09555_b200 as m
+
+    cfg = m.named_config(args.decode_model, compute="bf16")
+    params = m.synthetic_init(cfg, seed=7, device=f"cuda:{local}")
+    B = args.decode_batch
+    prompt = torch.randint(0, cfg.vocab_size, (B, 16), device=f"cuda:{local}")
+    _, cache = m.prefill(params, prompt, cfg, logits=None)
+    dec = m.GreedyDecoder(params, cfg, cache, args.decode_steps + 8)
+    dec.step()  # capture + first replay
+    for _ in range(3):
+        dec.step()
+    torch.cuda.synchronize()
+    n = args.decode_steps
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(n):
+        dec.step()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / n
+    nbytes = m.decode_step_bytes(cfg, B)
+    gbs = nbytes / (ms / 1e3) / 1e9
+    pk = peaks()
+    return {
+        "model": args.decode_model,
+        "batch": B,
+        "ms_per_step": ms,
+        "tok_per_s": B / (ms / 1e3),
+        "hbm_gbs": gbs,
+        "hbm_frac": gbs / pk["hbm_gbs"],
+        "bytes_per_step": nbytes,
+        "note": "CUDA-graph step: embed + 48 layers (GEMV in_proj, conv, SSM update in place, gated norm, GEMV out_proj) + head + argmax",
+    }
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import torch
+
+    rank, world, local = dist_setup(args.gpus)
+    res = run_prefill(args, rank, world, local)
+    dec = None
+    if not args.no_decode:
+        dec = run_decode(args, local)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, secs, desc = cpu_prefill_sample(args.model, T=2048, layers=1)
+        cpu = {"value": v, "unit": "tok/s", "cores": _NCPU, "kind": "port", "sample": desc,
+               "seconds": secs}
+    if rank == 0:
+        line = {
+            "metric": f"prefill_tokens_per_s[{args.model}]",
+            "value": res["value"],
+            "unit": "tok/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": res["ms"],
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic (random ids; device-drawn weights with the reference init distributions)",
+            "config": {
+                "workload": f"Mamba-2 {args.model} bf16 chunked-SSD prefill (BASELINE configs[1] sweep point)",
+                "batch_per_gpu": args.batch,
+                "global_batch": args.batch * world,
+                "seq_len": args.seqlen,
+                "chunk": 256,
+                "head": "tied head on the last position only",
+                "parallelism": f"batch-sharded x{world} (no data-path collective)",
+                "l2": "working set > 126 MB L2 (activations + 0.74 GB weights per step); no flush",
+            },
+            "tflops_per_gpu": res["step_tflops_per_gpu"],
+            "mfu": res["step_mfu"],
+            "e2e": {"value": res["e2e_value"], "unit": "tok/s", "h2d_bytes_per_step": res["h2d"] * world,
+                    "d2h_bytes_per_step": res["d2h"] * world},
+            "roofline": res["roofline"],
+            "phases_ms_per_step": res["phases_ms"],
+            "cpu_baseline": cpu,
+            "decode": dec,
+            "clocks": res["clocks"],
+            "gpu_launches": int(res["launches"]),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -11,6 +11,7 @@
 #include "../../include/ssd200.h"
 #include "common.cuh"
 #include "simt.cuh"
+#include "ssd_tc.cuh"
 #include "tc_gemm.cuh"
 
 using namespace ssd200;
@@ -184,7 +185,7 @@ int run_scan(SsdArgs<T, TI> a, void *ws, size_t ws_bytes, cudaStream_t st) {
   REQUIRE(cv.ok(), SSD200_EWORKSPACE, "scan workspace %zu < %zu", ws_bytes, cv.used);
   const size_t smem1 = (3 * (size_t)a.L + 16 * (size_t)a.P + 16 * (size_t)a.N) * sizeof(T);
   const size_t smem3 =
-      (2 * (size_t)a.L + 16 * (size_t)a.N + 32 * (size_t)a.N + 32 * (size_t)a.P + 16 * 32) *
+      (2 * (size_t)a.L + 16 * (size_t)a.N + 32 * ((size_t)a.N + 1) + 32 * (size_t)a.P + 16 * 32) *
       sizeof(T);
   REQUIRE(smem1 <= 220 * 1024 && smem3 <= 220 * 1024, SSD200_EUNSUPPORTED,
           "scan shared memory too large");
@@ -234,6 +235,116 @@ inline Widths widths(const ssd200_dims_t *d) {
 
 inline unsigned blocks_for(long n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
+// ----------------------------------------------------- tensor-core SSD path
+// Production Mamba-2 head dims: the tcgen05 scan (ssd_tc.cuh) handles these;
+// anything else runs the generic CUDA-core scan.
+inline bool tc_ssd_eligible(const ssd200_dims_t *d) {
+  return d->head_dim == TC_P && d->d_state == TC_N && d->chunk_size == TC_L &&
+         d->n_groups == 1 && d->conv_kernel >= 1;
+}
+
+struct TcScanWs {
+  float *cs, *cs_end, *S;
+  bf16 *prev;
+};
+
+inline size_t tc_scan_carve(int B, int Tn, int H, void *base, TcScanWs *o) {
+  const long Nc = (Tn + TC_L - 1) / TC_L;
+  Carve cv(base, SIZE_MAX);
+  float *S = cv.take<float>((size_t)B * Nc * H * TC_P * TC_N);
+  bf16 *prev = cv.take<bf16>((size_t)B * Nc * H * TC_P * TC_N);
+  float *cs = cv.take<float>((size_t)B * H * Nc * TC_L);
+  float *ce = cv.take<float>((size_t)B * H * Nc);
+  if (o) *o = TcScanWs{cs, ce, S, prev};
+  return cv.used;
+}
+
+inline size_t tc_scan_ws_bytes(int B, int Tn, int H) { return tc_scan_carve(B, Tn, H, nullptr, nullptr); }
+
+// 3-D bf16 map over (B, T, cols) with row pitch ld: box (64 cols, box_rows, 1)
+int make_map_3d(CUtensorMap *m, const void *ptr, long B, long T, long cols, long ld, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  REQUIRE(fn, SSD200_ELAUNCH, "cuTensorMapEncodeTiled unavailable");
+  REQUIRE(((uintptr_t)ptr & 15) == 0, SSD200_EINVAL, "TMA base pointer not 16-byte aligned");
+  REQUIRE((ld * 2) % 16 == 0, SSD200_EINVAL, "TMA row stride must be a multiple of 16 bytes");
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)T, (cuuint64_t)B};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)ld * 2 * T};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(ptr), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  REQUIRE(r == CUDA_SUCCESS, SSD200_ELAUNCH, "cuTensorMapEncodeTiled(3d) failed (%d)", (int)r);
+  return SSD200_OK;
+}
+
+// smallest divisor of H giving at least `target` CTAs over `units` work units
+inline int pick_groups(int H, long units, long target) {
+  for (int ng = 1; ng <= H; ++ng)
+    if (H % ng == 0 && units * ng >= target) return ng;
+  return H;
+}
+
+// act: post-conv xBC (B*T, conv_dim) bf16; z: gate (B*T, z_ld) bf16.
+// Writes u (B*T, d_inner) bf16, ssq (B*T, NG) f32, final state (B,H,P,N) f32.
+int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act, long conv_dim,
+                const bf16 *z, long z_ld, const float *dt, float *final_state, bf16 *u_out,
+                float *ssq, int *ng_out, void *scan_ws, int B, int Tn, cudaStream_t st) {
+  static bool attrs = false;
+  if (!attrs) {
+    cudaFuncSetAttribute(ssd_tc_state, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)StateSmem::TOTAL);
+    cudaFuncSetAttribute(ssd_tc_out, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)OutSmem::TOTAL);
+    attrs = true;
+  }
+  const int H = d->n_heads;
+  TcSsdArgs a{};
+  a.B = B;
+  a.T = Tn;
+  a.H = H;
+  a.Nc = (Tn + TC_L - 1) / TC_L;
+  a.d_inner = d->d_inner;
+  a.z = z;
+  a.z_ld = z_ld;
+  a.dt = dt;
+  a.a = static_cast<const float *>(w->a);
+  a.D = static_cast<const float *>(w->D);
+  a.init = nullptr;
+  TcScanWs ws;
+  tc_scan_carve(B, Tn, H, scan_ws, &ws);
+  a.cs = ws.cs;
+  a.cs_end = ws.cs_end;
+  a.S = ws.S;
+  a.prev = ws.prev;
+  a.final_state = final_state;
+  a.u_out = u_out;
+  a.ssq = ssq;
+  CUtensorMap tm_act, tm_prev;
+  int rc = make_map_3d(&tm_act, act, B, Tn, conv_dim, conv_dim, 128);
+  if (rc) return rc;
+  rc = make_map_2d(&tm_prev, ws.prev, (long)B * a.Nc * H * TC_P, TC_N, TC_N, 64);
+  if (rc) return rc;
+  const long sms = num_sms();
+  // chunk cumsums
+  ssd_tc_cumsum<<<dim3(B * a.Nc, (H + 7) / 8), 256, 0, st>>>(a);
+  LAUNCH_CHECK("ssd_tc_cumsum");
+  // chunk states
+  a.NG = pick_groups(H, (long)B * a.Nc, 2 * sms);
+  a.HG = H / a.NG;
+  ssd_tc_state<<<B * a.Nc * a.NG, 192, StateSmem::TOTAL, st>>>(tm_act, a);
+  LAUNCH_CHECK("ssd_tc_state");
+  ssd_tc_pass<<<dim3(B * H, TC_P * TC_N / 256), 256, 0, st>>>(a);
+  LAUNCH_CHECK("ssd_tc_pass");
+  // outputs (+ D skip + gate)
+  a.NG = pick_groups(H, (long)B * a.Nc * 2, 2 * sms);
+  a.HG = H / a.NG;
+  ssd_tc_out<<<B * a.Nc * 2 * a.NG, 192, OutSmem::TOTAL, st>>>(tm_act, tm_prev, a);
+  LAUNCH_CHECK("ssd_tc_out");
+  *ng_out = a.NG;
+  return SSD200_OK;
+}
+
 // ------------------------------------------------------------ prefill layer
 // workspace carve (identical in sizing and launch)
 template <typename T> struct PrefillWs {
@@ -261,8 +372,10 @@ bool carve_prefill(const ssd200_dims_t *d, int B, int Tn, void *ws, size_t cap, 
   }
   o.dt = cv.take<T>(rows * d->n_heads);
   o.y = cv.take<T>(rows * d->d_inner);
-  o.scan_bytes = scan_ws_bytes(sizeof(T), B, Tn, d->n_heads, d->head_dim, d->d_state,
-                               d->chunk_size);
+  o.scan_bytes = (lp && tc_ssd_eligible(d))
+                     ? tc_scan_ws_bytes(B, Tn, d->n_heads)
+                     : scan_ws_bytes(sizeof(T), B, Tn, d->n_heads, d->head_dim, d->d_state,
+                                     d->chunk_size);
   o.scan = cv.take<char>(o.scan_bytes);
   if (need) *need = cv.used;
   return cv.ok();
@@ -293,10 +406,9 @@ int prefill_layer_simt(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidde
         u + d->d_inner, wd.d_in_proj, conv_out, B, Tn, (int)wd.conv_dim, k);
     LAUNCH_CHECK("conv_tail");
   }
-  conv_silu_prefill<T, T, T><<<blocks_for(rows * wd.conv_dim), 256, 0, st>>>(
+  conv_silu_prefill<T, T, T><<<dim3(blocks_for(wd.conv_dim), blocks_for(rows, 16)), 256, 0, st>>>(
       u + d->d_inner, wd.d_in_proj, static_cast<const T *>(w->conv_w),
-      static_cast<const T *>(w->conv_b), act, wd.conv_dim, Tn, (int)wd.conv_dim, k,
-      rows * wd.conv_dim);
+      static_cast<const T *>(w->conv_b), act, wd.conv_dim, Tn, (int)wd.conv_dim, k, rows);
   LAUNCH_CHECK("conv_silu_prefill");
   dt_kernel<T, T><<<blocks_for(rows * d->n_heads), 256, 0, st>>>(
       u + d->d_inner + wd.conv_dim, wd.d_in_proj, static_cast<const T *>(w->dt_bias), o.dt, rows,
@@ -374,12 +486,40 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
         u + d->d_inner, n_split, conv_out, B, Tn, (int)wd.conv_dim, k);
     LAUNCH_CHECK("conv_tail");
   }
-  conv_silu_prefill<float, bf16, bf16><<<blocks_for(rows * wd.conv_dim), 256, 0, st>>>(
-      u + d->d_inner, n_split, static_cast<const float *>(w->conv_w),
-      static_cast<const float *>(w->conv_b), act, wd.conv_dim, Tn, (int)wd.conv_dim, k,
-      rows * wd.conv_dim);
+  conv_silu_prefill<float, bf16, bf16>
+      <<<dim3(blocks_for(wd.conv_dim), blocks_for(rows, 16)), 256, 0, st>>>(
+          u + d->d_inner, n_split, static_cast<const float *>(w->conv_w),
+          static_cast<const float *>(w->conv_b), act, wd.conv_dim, Tn, (int)wd.conv_dim, k, rows);
   LAUNCH_CHECK("conv_silu_prefill");
   phase_mark(PH_CONV, 1, st);
+  if (tc_ssd_eligible(d)) {
+    // tensor-core scan with the D skip + gate fused; the norm's row scale is
+    // applied by the out_proj epilogue (norm_w folded into W_out).
+    bf16 *u_gated = reinterpret_cast<bf16 *>(o.y);
+    float *ssq = reinterpret_cast<float *>(reinterpret_cast<char *>(o.y) +
+                                           align_up((size_t)rows * d->d_inner * 2));
+    int ng = 1;
+    phase_mark(PH_SCAN, 0, st);
+    rc = run_tc_scan(d, w, act, wd.conv_dim, u, n_split, o.dt, ssm_out, u_gated, ssq, &ng, o.scan,
+                     B, Tn, st);
+    if (rc) return rc;
+    phase_mark(PH_SCAN, 1, st);
+    phase_mark(PH_NORM, 0, st);
+    phase_mark(PH_NORM, 1, st);
+    TcEpilogue er{};
+    er.C = hidden;
+    er.ldc = d->d_model;
+    er.C_lp = hidden_lp;
+    er.ssq = ssq;
+    er.ng = ng;
+    er.inv_d = 1.f / (float)d->d_inner;
+    er.eps = (float)d->norm_eps;
+    phase_mark(PH_OUT_PROJ, 0, st);
+    rc = tc_gemm<TC_EPI_RESID_NORM>(u_gated, d->d_inner, static_cast<const bf16 *>(w->W_out),
+                                    d->d_inner, (int)rows, d->d_model, d->d_inner, er, st);
+    phase_mark(PH_OUT_PROJ, 1, st);
+    return rc;
+  }
   SsdArgs<float, bf16> sa{};
   sa.X = act;
   sa.x_ts = wd.conv_dim;
@@ -408,7 +548,7 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
   phase_mark(PH_NORM, 0, st);
   bf16 *normed = act;  // act is dead after the scan
   gated_norm_kernel<float, bf16, bf16><<<(unsigned)rows, 256, 0, st>>>(
-      o.y, d->d_inner, u, n_split, static_cast<const float *>(w->norm_w), normed, d->d_inner,
+      o.y, d->d_inner, u, n_split, nullptr /* norm_w folded into W_out */, normed, d->d_inner,
       d->d_inner, (float)d->norm_eps);
   LAUNCH_CHECK("gated_norm");
   phase_mark(PH_NORM, 1, st);
@@ -505,7 +645,7 @@ int decode_layer_impl(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidden
   if (lp) {
     gated_norm_kernel<float, float, bf16><<<B, 256, 0, st>>>(
         (const float *)o.y, d->d_inner, (const float *)o.u, wd.d_in_proj,
-        static_cast<const float *>(w->norm_w), o.normed_lp, d->d_inner, d->d_inner,
+        nullptr /* norm_w folded into W_out */, o.normed_lp, d->d_inner, d->d_inner,
         (float)d->norm_eps);
     LAUNCH_CHECK("gated_norm (decode)");
     const bf16 *Wout = static_cast<const bf16 *>(w->W_out);

@@ -209,22 +209,38 @@ __global__ __launch_bounds__(256) void gemv_nk(const TX *__restrict__ X, long ld
 // causal depthwise conv + SiLU over the xBC columns — numerics.py:169-189
 // (taps oldest first, bias after the taps, zero left padding).
 // =========================================================================
-template <typename T, typename TI, typename TO>
-__global__ void conv_silu_prefill(const TI *__restrict__ xbc, long ld_in,
-                                  const T *__restrict__ w, const T *__restrict__ bias,
-                                  TO *__restrict__ out, long ld_out, int Tlen, int C, int k,
-                                  long total) {
-  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  const int c = (int)(i % C);
-  const long row = i / C;  // b*T + t
-  const int t = (int)(row % Tlen);
-  T acc = T(0);
-  for (int j = 0; j < k; ++j) {
-    int src = t - (k - 1) + j;
-    if (src >= 0) acc += w[(size_t)c * k + j] * cvt<T>(xbc[(row - t + src) * ld_in + c]);
+// grid (ceil(C/256), rows/ROWS_PER_BLOCK): each thread walks ROWS consecutive
+// tokens of one channel, keeping the k-1 previous inputs in registers.
+template <typename T, typename TI, typename TO, int ROWS = 16>
+__global__ __launch_bounds__(256) void conv_silu_prefill(const TI *__restrict__ xbc, long ld_in,
+                                                         const T *__restrict__ w,
+                                                         const T *__restrict__ bias,
+                                                         TO *__restrict__ out, long ld_out,
+                                                         int Tlen, int C, int k, long rows) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const long r0 = (long)blockIdx.y * ROWS;
+  if (c >= C) return;
+  T wk[16], win[16];
+  for (int j = 0; j < k; ++j) wk[j] = w[(size_t)c * k + j];
+  const T bc = bias[c];
+  const int t0 = (int)(r0 % Tlen);
+  // history before r0 within the same sequence (zero before t = 0)
+  for (int j = 0; j < k - 1; ++j) {
+    const int src = t0 - (k - 1) + j;
+    win[j] = src >= 0 ? cvt<T>(xbc[(r0 - t0 + src) * ld_in + c]) : T(0);
   }
-  out[row * ld_out + c] = cvt<TO>(silu(acc + bias[c]));
+  int t = t0;
+  for (long r = r0; r < r0 + ROWS && r < rows; ++r, ++t) {
+    if (t == Tlen) {  // crossed into the next sequence: reset the history
+      t = 0;
+      for (int j = 0; j < k - 1; ++j) win[j] = T(0);
+    }
+    win[k - 1] = cvt<T>(xbc[r * ld_in + c]);
+    T acc = T(0);
+    for (int j = 0; j < k; ++j) acc += wk[j] * win[j];  // taps oldest first
+    out[r * ld_out + c] = cvt<TO>(silu(acc + bc));
+    for (int j = 0; j < k - 1; ++j) win[j] = win[j + 1];
+  }
 }
 
 // conv tail: last k-1 pre-activation xBC inputs, newest last, zero-padded
@@ -384,8 +400,8 @@ __global__ __launch_bounds__(256) void ssd_chunk_out(SsdArgs<T, TI> p) {
   T *cs = reinterpret_cast<T *>(smem_raw);
   T *dts = cs + L;
   T *Cr = dts + L;      // RT x N
-  T *Bs = Cr + RT * N;  // ST x N
-  T *Xs = Bs + ST * N;  // ST x P (Xbar)
+  T *Bs = Cr + RT * N;        // ST x (N+1): padded against bank conflicts
+  T *Xs = Bs + ST * (N + 1);  // ST x P (Xbar)
   T *Mt = Xs + ST * P;  // RT x ST
   const int nRT = (L + RT - 1) / RT;
   const int c = blockIdx.x / nRT, rt = blockIdx.x % nRT;
@@ -417,7 +433,7 @@ __global__ __launch_bounds__(256) void ssd_chunk_out(SsdArgs<T, TI> p) {
     for (int i = tid; i < ST * N; i += blockDim.x) {
       int si = i / N, nn = i % N;
       long t = t0 + s0 + si;
-      Bs[i] = (s0 + si < L && t < p.T_)
+      Bs[si * (N + 1) + nn] = (s0 + si < L && t < p.T_)
                   ? cvt<T>(p.Bm[((long)b * p.T_ + t) * p.bc_ts + (long)g * N + nn])
                   : T(0);
     }
@@ -435,7 +451,7 @@ __global__ __launch_bounds__(256) void ssd_chunk_out(SsdArgs<T, TI> p) {
       T m = T(0);
       if (l < L && s <= l) {
         T gsum = T(0);
-        for (int nn = 0; nn < N; ++nn) gsum = fma(Cr[r * N + nn], Bs[si * N + nn], gsum);
+        for (int nn = 0; nn < N; ++nn) gsum = fma(Cr[r * N + nn], Bs[si * (N + 1) + nn], gsum);
         m = gsum * exp_(cs[l] - cs[s]);  // (C.B^T) * exp(segsum), ssd.py:147-148
       }
       Mt[i] = m;
@@ -495,7 +511,7 @@ __global__ __launch_bounds__(256) void gated_norm_kernel(const T *__restrict__ y
   const T denom = sqrt_(ss / T(D) + eps);
   for (int c = threadIdx.x; c < D; c += blockDim.x) {
     T u = y[r * ldy + c] * silu(cvt<T>(z[r * ldz + c]));
-    out[r * ldo + c] = cvt<TO>((u / denom) * w[c]);
+    out[r * ldo + c] = cvt<TO>(w ? (u / denom) * w[c] : u / denom);
   }
 }
 

@@ -23,7 +23,10 @@
 
 namespace ssd200 {
 
-enum { TC_EPI_F32 = 0, TC_EPI_BF16 = 1, TC_EPI_INPROJ = 2, TC_EPI_RESID = 3 };
+// TC_EPI_RESID_NORM: hidden += acc * rstd(row), rstd = 1/sqrt(sum_g ssq[row,g]/d + eps):
+// the gated RMSNorm's row scale applied after the GEMM (it commutes with it;
+// norm_w is folded into W_out's columns at load time) — numerics.py:149-158.
+enum { TC_EPI_F32 = 0, TC_EPI_BF16 = 1, TC_EPI_INPROJ = 2, TC_EPI_RESID = 3, TC_EPI_RESID_NORM = 4 };
 
 struct TcEpilogue {
   void *C;        // F32: float*, BF16/INPROJ: bf16*, RESID: float* (hidden)
@@ -34,6 +37,9 @@ struct TcEpilogue {
   int H;
   const float *dt_bias;
   float dt_lo, dt_hi;
+  const float *ssq;  // RESID_NORM: (M, ng) partial sums of u^2
+  int ng;
+  float inv_d, eps;
 };
 
 template <int BN> struct TcCfg {
@@ -52,8 +58,12 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 }
 
 template <int EPI>
-__device__ __forceinline__ void tc_store_chunk(const TcEpilogue &ep, const uint32_t (&r)[32],
-                                               int m, int n0, int N) {
+__device__ __forceinline__ void tc_store_chunk(const TcEpilogue &ep, uint32_t (&r)[32], int m,
+                                               int n0, int N, float rowscale) {
+  if (EPI == TC_EPI_RESID_NORM) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * rowscale);
+  }
   const bool full = (n0 + 32 <= N);
   if (EPI == TC_EPI_F32) {
     float *dst = reinterpret_cast<float *>(ep.C) + (size_t)m * ep.ldc + n0;
@@ -64,7 +74,9 @@ __device__ __forceinline__ void tc_store_chunk(const TcEpilogue &ep, const uint3
             make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
                         __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
     } else {
-      for (int j = 0; j < 32 && n0 + j < N; ++j) dst[j] = __uint_as_float(r[j]);
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (n0 + j < N) dst[j] = __uint_as_float(r[j]);
     }
   } else if (EPI == TC_EPI_BF16 || EPI == TC_EPI_INPROJ) {
     const int lim = (EPI == TC_EPI_INPROJ) ? ep.n_split : N;
@@ -80,8 +92,10 @@ __device__ __forceinline__ void tc_store_chunk(const TcEpilogue &ep, const uint3
         *reinterpret_cast<uint4 *>(dst + j) = v;
       }
     } else {
-      for (int j = 0; j < 32 && n0 + j < N; ++j) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
         const int n = n0 + j;
+        if (n >= N) continue;
         const float acc = __uint_as_float(r[j]);
         if (n < lim) {
           dst[j] = __float2bfloat16_rn(acc);
@@ -92,7 +106,7 @@ __device__ __forceinline__ void tc_store_chunk(const TcEpilogue &ep, const uint3
         }
       }
     }
-  } else {  // TC_EPI_RESID
+  } else {  // TC_EPI_RESID / TC_EPI_RESID_NORM
     float *dst = reinterpret_cast<float *>(ep.C) + (size_t)m * ep.ldc + n0;
     bf16 *lp = ep.C_lp + (size_t)m * ep.ldc + n0;
     if (full && ((ep.ldc & 7) == 0)) {
@@ -118,7 +132,9 @@ __device__ __forceinline__ void tc_store_chunk(const TcEpilogue &ep, const uint3
         *reinterpret_cast<uint4 *>(lp + j) = v;
       }
     } else {
-      for (int j = 0; j < 32 && n0 + j < N; ++j) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (n0 + j >= N) continue;
         float v = dst[j] + __uint_as_float(r[j]);
         dst[j] = v;
         lp[j] = __float2bfloat16_rn(v);
@@ -229,6 +245,12 @@ __global__ void __launch_bounds__(192, 1)
       sm100::tc_fence_after();
       const int m = m_blk * BM + q * 32 + lane;
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
+      float rowscale = 1.f;
+      if (EPI == TC_EPI_RESID_NORM && m < M) {
+        float s = 0.f;
+        for (int gg = 0; gg < ep.ng; ++gg) s += ep.ssq[(size_t)m * ep.ng + gg];
+        rowscale = 1.f / sqrtf(s * ep.inv_d + ep.eps);
+      }
 #pragma unroll 1
       for (int cc = 0; cc < BN; cc += 32) {
         const int n0 = n_blk * BN + cc;
@@ -236,7 +258,7 @@ __global__ void __launch_bounds__(192, 1)
         uint32_t r[32];
         sm100::tmem_ld32(trow + cc, r);
         sm100::tmem_ld_wait();
-        if (m < M) tc_store_chunk<EPI>(ep, r, m, n0, N);
+        if (m < M) tc_store_chunk<EPI>(ep, r, m, n0, N, rowscale);
       }
       sm100::tc_fence_before();
       __syncwarp();

@@ -97,6 +97,11 @@ def from_reference(params, cfg: ModelConfig, device="cuda") -> ModelParams:
 
     layers = []
     for lp in params.layers:
+        W_out = _np(lp.W_out)
+        if mode == "bf16":
+            # the gated norm's weight is folded into W_out's rows (the norm's
+            # row scale is applied after the out_proj GEMM; numerics.py:149-158)
+            W_out = _np(lp.norm_w).astype(np.float32)[:, None] * W_out.astype(np.float32)
         layers.append(
             LayerParams(
                 W_in=big(lp.W_in, transpose=True),
@@ -106,7 +111,7 @@ def from_reference(params, cfg: ModelConfig, device="cuda") -> ModelParams:
                 A_log=small(lp.A_log),
                 D=small(lp.D),
                 norm_w=small(lp.norm_w),
-                W_out=big(lp.W_out, transpose=True),
+                W_out=big(W_out, transpose=True),
                 a=small(decay_coefficient(_np(lp.A_log), cfg)),
             )
         )

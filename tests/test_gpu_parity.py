@@ -199,7 +199,9 @@ def test_c1_130m_tokens_identical():
     assert np.all(np.abs(rows - ref) <= 1e-4 * np.abs(ref) + 1e-4 * np.abs(ref).max())
     st = _np(s1[0, 0])
     assert np.linalg.norm(st - z["layer0_state_head0"]) / np.linalg.norm(z["layer0_state_head0"]) <= 1e-4
-    assert np.array_equal(_np(c1[0]), z["layer0_conv_tail"])
+    # the tail holds pre-activation in_proj outputs: fp32 GEMM rounding only
+    ct, rt = _np(c1[0]), z["layer0_conv_tail"]
+    assert np.linalg.norm(ct - rt) / np.linalg.norm(rt) <= 1e-5
 
 
 # ----------------------------------------------------------- bf16 tensor-core mode
