@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include "../../include/ssd200.h"
 #include "common.cuh"
@@ -235,6 +236,29 @@ inline Widths widths(const ssd200_dims_t *d) {
 
 inline unsigned blocks_for(long n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
+template <typename T, typename TI, typename TO>
+void launch_conv(const TI *in, long ld_in, const T *w, const T *bias, TO *out, long ld_out, int Tn,
+                 int C, int k, long rows, cudaStream_t st) {
+  if constexpr (std::is_same<TI, bf16>::value && std::is_same<TO, bf16>::value &&
+                std::is_same<T, float>::value) {
+    if (k == 4 && C % 8 == 0 && ld_in % 8 == 0 && ld_out % 8 == 0 &&
+        ((uintptr_t)in & 15) == 0 && ((uintptr_t)out & 15) == 0) {
+      constexpr int ROWS = 8;
+      const dim3 g8(blocks_for(C, 256), blocks_for(rows, 8 * ROWS));
+      conv_silu_bf16x8<4, ROWS><<<g8, dim3(32, 8), 0, st>>>(in, ld_in, w, bias, out, ld_out, Tn,
+                                                          C, rows);
+      return;
+    }
+  }
+  const dim3 grid(blocks_for(C), blocks_for(rows, 16));
+  if (k == 4)
+    conv_silu_prefill<T, TI, TO, 4><<<grid, 256, 0, st>>>(in, ld_in, w, bias, out, ld_out, Tn, C,
+                                                          k, rows);
+  else
+    conv_silu_prefill<T, TI, TO, 0><<<grid, 256, 0, st>>>(in, ld_in, w, bias, out, ld_out, Tn, C,
+                                                          k, rows);
+}
+
 // ----------------------------------------------------- tensor-core SSD path
 // Production Mamba-2 head dims: the tcgen05 scan (ssd_tc.cuh) handles these;
 // anything else runs the generic CUDA-core scan.
@@ -244,7 +268,7 @@ inline bool tc_ssd_eligible(const ssd200_dims_t *d) {
 }
 
 struct TcScanWs {
-  float *cs, *cs_end, *S;
+  float *cs, *cs_end, *S, *dtT;
   bf16 *prev;
 };
 
@@ -254,8 +278,9 @@ inline size_t tc_scan_carve(int B, int Tn, int H, void *base, TcScanWs *o) {
   float *S = cv.take<float>((size_t)B * Nc * H * TC_P * TC_N);
   bf16 *prev = cv.take<bf16>((size_t)B * Nc * H * TC_P * TC_N);
   float *cs = cv.take<float>((size_t)B * H * Nc * TC_L);
+  float *dtT = cv.take<float>((size_t)B * H * Nc * TC_L);
   float *ce = cv.take<float>((size_t)B * H * Nc);
-  if (o) *o = TcScanWs{cs, ce, S, prev};
+  if (o) *o = TcScanWs{cs, ce, S, dtT, prev};
   return cv.used;
 }
 
@@ -314,6 +339,7 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
   TcScanWs ws;
   tc_scan_carve(B, Tn, H, scan_ws, &ws);
   a.cs = ws.cs;
+  a.dtT = ws.dtT;
   a.cs_end = ws.cs_end;
   a.S = ws.S;
   a.prev = ws.prev;
@@ -339,7 +365,8 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
   // outputs (+ D skip + gate)
   a.NG = pick_groups(H, (long)B * a.Nc * 2, 2 * sms);
   a.HG = H / a.NG;
-  ssd_tc_out<<<B * a.Nc * 2 * a.NG, 192, OutSmem::TOTAL, st>>>(tm_act, tm_prev, a);
+  ssd_tc_out<<<B * a.Nc * 2 * a.NG, OUT_THREADS, OutSmem::TOTAL, st>>>(tm_act, tm_prev, a, act,
+                                                                        conv_dim);
   LAUNCH_CHECK("ssd_tc_out");
   *ng_out = a.NG;
   return SSD200_OK;
@@ -406,9 +433,9 @@ int prefill_layer_simt(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidde
         u + d->d_inner, wd.d_in_proj, conv_out, B, Tn, (int)wd.conv_dim, k);
     LAUNCH_CHECK("conv_tail");
   }
-  conv_silu_prefill<T, T, T><<<dim3(blocks_for(wd.conv_dim), blocks_for(rows, 16)), 256, 0, st>>>(
-      u + d->d_inner, wd.d_in_proj, static_cast<const T *>(w->conv_w),
-      static_cast<const T *>(w->conv_b), act, wd.conv_dim, Tn, (int)wd.conv_dim, k, rows);
+  launch_conv<T, T, T>(u + d->d_inner, wd.d_in_proj, static_cast<const T *>(w->conv_w),
+                       static_cast<const T *>(w->conv_b), act, wd.conv_dim, Tn, (int)wd.conv_dim,
+                       k, rows, st);
   LAUNCH_CHECK("conv_silu_prefill");
   dt_kernel<T, T><<<blocks_for(rows * d->n_heads), 256, 0, st>>>(
       u + d->d_inner + wd.conv_dim, wd.d_in_proj, static_cast<const T *>(w->dt_bias), o.dt, rows,
@@ -486,10 +513,9 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
         u + d->d_inner, n_split, conv_out, B, Tn, (int)wd.conv_dim, k);
     LAUNCH_CHECK("conv_tail");
   }
-  conv_silu_prefill<float, bf16, bf16>
-      <<<dim3(blocks_for(wd.conv_dim), blocks_for(rows, 16)), 256, 0, st>>>(
-          u + d->d_inner, n_split, static_cast<const float *>(w->conv_w),
-          static_cast<const float *>(w->conv_b), act, wd.conv_dim, Tn, (int)wd.conv_dim, k, rows);
+  launch_conv<float, bf16, bf16>(u + d->d_inner, n_split, static_cast<const float *>(w->conv_w),
+                                 static_cast<const float *>(w->conv_b), act, wd.conv_dim, Tn,
+                                 (int)wd.conv_dim, k, rows, st);
   LAUNCH_CHECK("conv_silu_prefill");
   phase_mark(PH_CONV, 1, st);
   if (tc_ssd_eligible(d)) {

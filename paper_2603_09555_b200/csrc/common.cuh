@@ -47,6 +47,17 @@ template <typename T> __device__ __forceinline__ T sigmoid(T v) {
 }
 template <typename T> __device__ __forceinline__ T silu(T v) { return v * sigmoid(v); }
 
+// MUFU-based fast paths for the bf16 mode (inputs/outputs are bf16 there)
+constexpr float kLog2e = 1.4426950408889634f;
+__device__ __forceinline__ float ex2(float v) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ float silu_fast(float x) {
+  return __fdividef(x, 1.f + ex2(-x * kLog2e));
+}
+
 template <typename T> __device__ __forceinline__ T clamp_(T v, T lo, T hi) {
   return v < lo ? lo : (v > hi ? hi : v);
 }

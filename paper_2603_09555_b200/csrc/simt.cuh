@@ -211,35 +211,130 @@ __global__ __launch_bounds__(256) void gemv_nk(const TX *__restrict__ X, long ld
 // =========================================================================
 // grid (ceil(C/256), rows/ROWS_PER_BLOCK): each thread walks ROWS consecutive
 // tokens of one channel, keeping the k-1 previous inputs in registers.
-template <typename T, typename TI, typename TO, int ROWS = 16>
+// KC > 0: compile-time kernel width (the production k = 4, fully in
+// registers); KC == 0: runtime k <= 16.
+template <typename T, typename TI, typename TO, int KC = 0, int ROWS = 16>
 __global__ __launch_bounds__(256) void conv_silu_prefill(const TI *__restrict__ xbc, long ld_in,
                                                          const T *__restrict__ w,
                                                          const T *__restrict__ bias,
                                                          TO *__restrict__ out, long ld_out,
-                                                         int Tlen, int C, int k, long rows) {
+                                                         int Tlen, int C, int k_rt, long rows) {
+  const int k = KC > 0 ? KC : k_rt;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const long r0 = (long)blockIdx.y * ROWS;
   if (c >= C) return;
-  T wk[16], win[16];
+  T wk[KC > 0 ? KC : 16], win[KC > 0 ? KC : 16];
+#pragma unroll
   for (int j = 0; j < k; ++j) wk[j] = w[(size_t)c * k + j];
   const T bc = bias[c];
   const int t0 = (int)(r0 % Tlen);
   // history before r0 within the same sequence (zero before t = 0)
+#pragma unroll
   for (int j = 0; j < k - 1; ++j) {
     const int src = t0 - (k - 1) + j;
     win[j] = src >= 0 ? cvt<T>(xbc[(r0 - t0 + src) * ld_in + c]) : T(0);
   }
+  T xin[ROWS];  // all loads in flight before the dependent taps
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i) {
+    const long r = r0 + i;
+    xin[i] = r < rows ? cvt<T>(xbc[r * ld_in + c]) : T(0);
+  }
   int t = t0;
-  for (long r = r0; r < r0 + ROWS && r < rows; ++r, ++t) {
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i, ++t) {
+    const long r = r0 + i;
+    if (r >= rows) break;
     if (t == Tlen) {  // crossed into the next sequence: reset the history
       t = 0;
+#pragma unroll
       for (int j = 0; j < k - 1; ++j) win[j] = T(0);
     }
-    win[k - 1] = cvt<T>(xbc[r * ld_in + c]);
+    win[k - 1] = xin[i];
     T acc = T(0);
+#pragma unroll
     for (int j = 0; j < k; ++j) acc += wk[j] * win[j];  // taps oldest first
     out[r * ld_out + c] = cvt<TO>(silu(acc + bc));
+#pragma unroll
     for (int j = 0; j < k - 1; ++j) win[j] = win[j + 1];
+  }
+}
+
+// bf16 path, k = KC: a thread owns 8 consecutive channels (one 16-byte load
+// per token) for ROWS consecutive tokens; block (32, 8) covers 256 channels x
+// 8*ROWS tokens.  Needs C % 8 == 0 and 16-byte aligned rows.
+template <int KC, int ROWS>
+__global__ __launch_bounds__(256, 2) void conv_silu_bf16x8(const bf16 *__restrict__ xbc, long ld_in,
+                                                        const float *__restrict__ w,
+                                                        const float *__restrict__ bias,
+                                                        bf16 *__restrict__ out, long ld_out,
+                                                        int Tlen, int C, long rows) {
+  const int c0 = (blockIdx.x * 32 + threadIdx.x) * 8;
+  const long r0 = ((long)blockIdx.y * 8 + threadIdx.y) * ROWS;
+  if (c0 >= C || r0 >= rows) return;
+  float wk[8][KC], bc[8], win[8][KC];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+#pragma unroll
+    for (int j = 0; j < KC; ++j) wk[e][j] = w[(size_t)(c0 + e) * KC + j];
+    bc[e] = bias[c0 + e];
+  }
+  const int t0 = (int)(r0 % Tlen);
+#pragma unroll
+  for (int j = 0; j < KC - 1; ++j) {
+    const int src = t0 - (KC - 1) + j;
+    uint4 v = src >= 0 ? *reinterpret_cast<const uint4 *>(xbc + (r0 - t0 + src) * ld_in + c0)
+                       : make_uint4(0, 0, 0, 0);
+    const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 f = __bfloat1622float2(h[e]);
+      win[2 * e][j] = f.x;
+      win[2 * e + 1][j] = f.y;
+    }
+  }
+  uint4 xin[ROWS];
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i) {
+    const long r = r0 + i;
+    xin[i] = r < rows ? *reinterpret_cast<const uint4 *>(xbc + r * ld_in + c0) : make_uint4(0, 0, 0, 0);
+  }
+  int t = t0;
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i, ++t) {
+    const long r = r0 + i;
+    if (r >= rows) break;
+    if (t == Tlen) {
+      t = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+#pragma unroll
+        for (int j = 0; j < KC - 1; ++j) win[e][j] = 0.f;
+    }
+    const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&xin[i]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 f = __bfloat1622float2(h[e]);
+      win[2 * e][KC - 1] = f.x;
+      win[2 * e + 1][KC - 1] = f.y;
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+      for (int j = 0; j < KC; ++j) {  // taps oldest first (numerics.py:187-188)
+        a0 += wk[e][j] * win[e][j];
+        a1 += wk[e + 1][j] * win[e + 1][j];
+      }
+      __nv_bfloat162 v = __floats2bfloat162_rn(silu_fast(a0 + bc[e]), silu_fast(a1 + bc[e + 1]));
+      o[e >> 1] = *reinterpret_cast<uint32_t *>(&v);
+    }
+    *reinterpret_cast<uint4 *>(out + r * ld_out + c0) = make_uint4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+#pragma unroll
+      for (int j = 0; j < KC - 1; ++j) win[e][j] = win[e][j + 1];
   }
 }
 

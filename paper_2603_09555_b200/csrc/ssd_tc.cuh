@@ -33,6 +33,7 @@ struct TcSsdArgs {
   const float *D;     // (H)
   const float *init;  // (B, H, P, N) or null
   float *cs;          // (B, H, Nc*L)
+  float *dtT;         // (B, H, Nc*L) dt transposed (0 past T)
   float *cs_end;      // (B, H, Nc)
   float *S;           // (B, Nc, H, P, N) f32: each chunk's own end state
   bf16 *prev;         // (B, Nc, H, P, N) bf16: state entering each chunk
@@ -40,14 +41,6 @@ struct TcSsdArgs {
   bf16 *u_out;        // (rows, d_inner)
   float *ssq;         // (rows, NG) partial sum of u^2
 };
-
-constexpr float kLog2e = 1.4426950408889634f;
-
-__device__ __forceinline__ float ex2(float v) {
-  float r;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
-  return r;
-}
 
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -66,14 +59,18 @@ __global__ __launch_bounds__(256) void ssd_tc_cumsum(TcSsdArgs p) {
   const int h = blockIdx.y * 8 + warp;
   if (h >= p.H) return;
   const float ah = p.a[h];
-  float v[8], run = 0.f;
+  float v[8], dv[8], run = 0.f;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const int t = c * TC_L + lane * 8 + j;
     const float d = t < p.T ? p.dt[((long)b * p.T + t) * p.H + h] : 0.f;
+    dv[j] = d;
     run += ah * d;
     v[j] = run;
   }
+  float *dtd = p.dtT + ((long)b * p.H + h) * ((long)p.Nc * TC_L) + (long)c * TC_L + lane * 8;
+  *reinterpret_cast<float4 *>(dtd) = make_float4(dv[0], dv[1], dv[2], dv[3]);
+  *reinterpret_cast<float4 *>(dtd + 4) = make_float4(dv[4], dv[5], dv[6], dv[7]);
   float tot = run;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -186,7 +183,8 @@ __global__ void __launch_bounds__(192, 1)
       for (int rr = 0; rr < 2; ++rr) {
         const int l = tid + rr * 128;
         const int t = c * TC_L + l;
-        const float w = t < p.T ? p.dt[((long)b * p.T + t) * p.H + h] * ex2((cend - cs[l]) * kLog2e) : 0.f;
+        const float *dtr = p.dtT + ((long)b * p.H + h) * csb + (long)c * TC_L;
+        const float w = t < p.T ? dtr[l] * ex2((cend - cs[l]) * kLog2e) : 0.f;
         uint4 *row = reinterpret_cast<uint4 *>(xb + l * 128);
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch) {
@@ -263,235 +261,6 @@ __global__ __launch_bounds__(256) void ssd_tc_pass(TcSsdArgs p) {
   p.final_state[(long)bh * PN + e] = s;
 }
 
-// ------------------------------------------------------------------ outputs
-struct OutSmem {
-  static constexpr uint32_t CR = 0;                  // C rows of the tile: 2 x [128 l][64 n]
-  static constexpr uint32_t BM = 32768;              // B rows (G operand), then M: 64 KB
-  static constexpr uint32_t X0 = BM + 65536;         // 2 x [256 s][64 p]
-  static constexpr uint32_t P0 = X0 + 2 * 32768;     // 2 x (2 x [64 p][64 n])
-  static constexpr uint32_t CS = P0 + 2 * 16384;     // 2 x 256 f32 (cs * log2e)
-  static constexpr uint32_t DT = CS + 2 * 1024;      // 2 x 256 f32
-  static constexpr uint32_t BAR = DT + 2 * 1024;
-  static constexpr uint32_t TOTAL = BAR + 256 + 1024;
-};
-
-// grid (B*Nc*2*NG), 192 threads: warp0 TMA, warp1 MMA, warps 2-5 math (one
-// TMEM lane = one output row each).
-__global__ void __launch_bounds__(192, 1)
-    ssd_tc_out(const __grid_constant__ CUtensorMap tm_act, const __grid_constant__ CUtensorMap tm_prev,
-               TcSsdArgs p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                            ~(uintptr_t)1023);
-  uint64_t *bar_cb = reinterpret_cast<uint64_t *>(sm + OutSmem::BAR);
-  uint64_t *bar_g = bar_cb + 1;
-  uint64_t *bar_xp = bar_cb + 2;  // [2]
-  uint64_t *xpfree = bar_cb + 4;  // [2]
-  uint64_t *bar_m = bar_cb + 6;
-  uint64_t *bar_y = bar_cb + 7;
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bar_cb + 8);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int idx = blockIdx.x;
-  const int g = idx % p.NG;
-  idx /= p.NG;
-  const int R = idx & 1;
-  idx >>= 1;
-  const int b = idx / p.Nc, c = idx % p.Nc;
-  const int h0 = g * p.HG;
-  const int NS = 128 * (R + 1);  // columns s of this row tile
-  const uint32_t TM_G = 0, TM_YD = 256, TM_YO = 320;
-
-  if (warp == 0 && lane == 0) {
-    sm100::tma_prefetch(&tm_act);
-    sm100::tma_prefetch(&tm_prev);
-    sm100::mbar_init(bar_cb, 1);
-    sm100::mbar_init(bar_g, 1);
-    for (int i = 0; i < 2; ++i) {
-      sm100::mbar_init(&bar_xp[i], 1);
-      sm100::mbar_init(&xpfree[i], 128);
-    }
-    sm100::mbar_init(bar_m, 128);
-    sm100::mbar_init(bar_y, 1);
-    sm100::fence_barrier_init();
-  }
-  if (warp == 1) sm100::tmem_alloc<512>(tslot);
-  sm100::tc_fence_before();
-  __syncthreads();
-  sm100::tc_fence_after();
-  const uint32_t tmem = *tslot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      sm100::mbar_arrive_expect_tx(bar_cb, 32768 + 2 * NS * 128);
-      for (int nb = 0; nb < 2; ++nb) {
-        sm100::tma_load_3d(sm + OutSmem::CR + nb * 16384, &tm_act, bar_cb,
-                           p.d_inner + TC_N + nb * 64, c * TC_L + R * 128, b);
-        for (int q = 0; q <= R; ++q)
-          sm100::tma_load_3d(sm + OutSmem::BM + nb * NS * 128 + q * 16384, &tm_act, bar_cb,
-                             p.d_inner + nb * 64, c * TC_L + q * 128, b);
-      }
-      for (int i = 0; i < p.HG; ++i) {
-        const int buf = i & 1, h = h0 + i;
-        sm100::mbar_wait(&xpfree[buf], ((i >> 1) & 1) ^ 1);
-        sm100::mbar_arrive_expect_tx(&bar_xp[buf], NS * 128 + 16384);
-        for (int q = 0; q <= R; ++q)
-          sm100::tma_load_3d(sm + OutSmem::X0 + buf * 32768 + q * 16384, &tm_act, &bar_xp[buf],
-                             h * TC_P, c * TC_L + q * 128, b);
-        const int prow = (((b * p.Nc + c) * p.H + h) * TC_P);
-        for (int nb = 0; nb < 2; ++nb)
-          sm100::tma_load_2d(sm + OutSmem::P0 + buf * 16384 + nb * 8192, &tm_prev, &bar_xp[buf],
-                             nb * 64, prow);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t cr = sm100::smem_u32(sm + OutSmem::CR);
-      const uint32_t bm = sm100::smem_u32(sm + OutSmem::BM);
-      sm100::mbar_wait(bar_cb, 0);
-      sm100::tc_fence_after();
-      const uint32_t idg = sm100::idesc_bf16(128, NS, false, false);
-#pragma unroll
-      for (int k = 0; k < TC_N / 16; ++k) {
-        const uint64_t ad = sm100::sw128_desc(cr + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
-        const uint64_t bd = sm100::sw128_desc(bm + (k >> 2) * NS * 128 + (k & 3) * 32, 16, 1024);
-        sm100::mma_bf16(tmem + TM_G, ad, bd, idg, k > 0);
-      }
-      sm100::mma_commit(bar_g);
-      constexpr uint32_t idy = sm100::idesc_bf16(128, TC_P, false, true);
-      constexpr uint32_t ido = sm100::idesc_bf16(128, TC_P, false, false);
-      for (int i = 0; i < p.HG; ++i) {
-        const int buf = i & 1;
-        sm100::mbar_wait(bar_m, i & 1);
-        sm100::mbar_wait(&bar_xp[buf], (i >> 1) & 1);
-        sm100::tc_fence_after();
-        const uint32_t xb = sm100::smem_u32(sm + OutSmem::X0 + buf * 32768);
-        const uint32_t pb = sm100::smem_u32(sm + OutSmem::P0 + buf * 16384);
-        for (int k = 0; k < NS / 16; ++k) {  // Ydiag = M . X
-          const uint64_t ad = sm100::sw128_desc(bm + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = sm100::sw128_desc(xb + k * 2048, 8192, 1024);
-          sm100::mma_bf16(tmem + TM_YD, ad, bd, idy, k > 0);
-        }
-#pragma unroll
-        for (int k = 0; k < TC_N / 16; ++k) {  // Yoff = C_R . prev^T
-          const uint64_t ad = sm100::sw128_desc(cr + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = sm100::sw128_desc(pb + (k >> 2) * 8192 + (k & 3) * 32, 16, 1024);
-          sm100::mma_bf16(tmem + TM_YO, ad, bd, ido, k > 0);
-        }
-        sm100::mma_commit(bar_y);
-      }
-    }
-  } else {
-    const int q = warp & 3;
-    const int tid = threadIdx.x - 64;  // 0..127 == TMEM lane == tile row
-    const int l = R * 128 + tid;
-    const int t = c * TC_L + l;
-    const bool valid = t < p.T;
-    const int lmax_warp = R * 128 + q * 32 + 31;
-    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const long csb = (long)p.Nc * TC_L;
-    float ssq = 0.f;
-    float *cs_s = reinterpret_cast<float *>(sm + OutSmem::CS);
-    float *dt_s = reinterpret_cast<float *>(sm + OutSmem::DT);
-    uint8_t *mbuf = sm + OutSmem::BM;
-    for (int i = 0; i < p.HG; ++i) {
-      const int buf = i & 1, h = h0 + i;
-      float *csh = cs_s + buf * 256;
-      float *dth = dt_s + buf * 256;
-      const float *csg = p.cs + ((long)b * p.H + h) * csb + (long)c * TC_L;
-      for (int s = tid; s < NS; s += 128) {
-        const int ts = c * TC_L + s;
-        csh[s] = csg[s] * kLog2e;
-        dth[s] = ts < p.T ? p.dt[((long)b * p.T + ts) * p.H + h] : 0.f;
-      }
-      named_bar(1, 128);
-      if (i == 0) {
-        sm100::mbar_wait(bar_g, 0);
-        sm100::tc_fence_after();
-      }
-      // ---- M = G * exp(cs_l - cs_s) * dt_s  (s <= l), bf16, K-major SW128
-      const float csl = csh[l];
-      for (int s0 = 0; s0 < NS; s0 += 32) {
-        uint32_t pk[16];
-        if (s0 > lmax_warp) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) pk[j] = 0u;
-        } else {
-          uint32_t r[32];
-          sm100::tmem_ld32(tmem + lane_off + TM_G + s0, r);
-          sm100::tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const int s = s0 + j;
-            const float m0 = s <= l ? __uint_as_float(r[j]) * ex2(csl - csh[s]) * dth[s] : 0.f;
-            const float m1 = s + 1 <= l ? __uint_as_float(r[j + 1]) * ex2(csl - csh[s + 1]) * dth[s + 1] : 0.f;
-            __nv_bfloat162 v = __floats2bfloat162_rn(m0, m1);
-            pk[j >> 1] = *reinterpret_cast<uint32_t *>(&v);
-          }
-        }
-        uint8_t *blk = mbuf + (s0 >> 6) * 16384;
-        const int ch0 = (s0 & 63) >> 3;
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
-          *reinterpret_cast<uint4 *>(blk + sw128_off(tid, ch0 + cc)) =
-              make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
-      }
-      sm100::fence_proxy_async();
-      sm100::tc_fence_before();
-      sm100::mbar_arrive(bar_m);
-      // ---- epilogue: y = Ydiag + e^{cs_l} Yoff + D x ; u = y silu(z)
-      sm100::mbar_wait(bar_y, i & 1);
-      sm100::tc_fence_after();
-      sm100::mbar_wait(&bar_xp[buf], (i >> 1) & 1);
-      const float el = ex2(csl);
-      const float Dh = p.D[h];
-      const uint8_t *xrow = sm + OutSmem::X0 + buf * 32768;
-      const bf16 *zrow = p.z + ((long)b * p.T + t) * p.z_ld + h * TC_P;
-      bf16 *urow = p.u_out + ((long)b * p.T + t) * p.d_inner + h * TC_P;
-#pragma unroll
-      for (int pc = 0; pc < TC_P; pc += 32) {
-        uint32_t yd[32], yo[32];
-        sm100::tmem_ld32(tmem + lane_off + TM_YD + pc, yd);
-        sm100::tmem_ld32(tmem + lane_off + TM_YO + pc, yo);
-        sm100::tmem_ld_wait();
-        uint4 xv[4], zv[4];
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          xv[cc] = *reinterpret_cast<const uint4 *>(xrow + sw128_off(l, (pc >> 3) + cc));
-          zv[cc] = valid ? *reinterpret_cast<const uint4 *>(zrow + pc + cc * 8) : make_uint4(0, 0, 0, 0);
-        }
-        const __nv_bfloat162 *xe = reinterpret_cast<const __nv_bfloat162 *>(xv);
-        const __nv_bfloat162 *ze = reinterpret_cast<const __nv_bfloat162 *>(zv);
-        uint32_t out[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float2 xf = __bfloat1622float2(xe[j]);
-          const float2 zf = __bfloat1622float2(ze[j]);
-          const float y0 = __uint_as_float(yd[2 * j]) + el * __uint_as_float(yo[2 * j]) + Dh * xf.x;
-          const float y1 = __uint_as_float(yd[2 * j + 1]) + el * __uint_as_float(yo[2 * j + 1]) + Dh * xf.y;
-          const float u0 = y0 * silu(zf.x), u1 = y1 * silu(zf.y);
-          ssq += u0 * u0 + u1 * u1;
-          __nv_bfloat162 v = __floats2bfloat162_rn(u0, u1);
-          out[j] = *reinterpret_cast<uint32_t *>(&v);
-        }
-        if (valid) {
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc)
-            *reinterpret_cast<uint4 *>(urow + pc + cc * 8) =
-                make_uint4(out[4 * cc], out[4 * cc + 1], out[4 * cc + 2], out[4 * cc + 3]);
-        }
-      }
-      sm100::tc_fence_before();
-      sm100::mbar_arrive(&xpfree[buf]);
-    }
-    if (valid) p.ssq[((long)b * p.T + t) * p.NG + g] = ssq;
-  }
-  __syncthreads();
-  if (warp == 1) {
-    __syncwarp();
-    sm100::tc_fence_after();
-    sm100::tmem_dealloc<512>(tmem);
-  }
-}
-
 }  // namespace ssd200
+
+#include "ssd_tc_out.cuh"
