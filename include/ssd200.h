@@ -105,6 +105,23 @@ int ssd200_head(const ssd200_dims_t *d, int vocab, const void *hidden, int64_t h
                 int64_t *argmax_out, int rows, void *workspace, size_t workspace_bytes,
                 ssd200_stream_t stream);
 
+/* ---- one whole decode_step in a single persistent kernel (bf16 mode) ----
+ * decode.py:77-144 for batch <= 8: embed tokens, every layer (in_proj,
+ * conv/SSM update in place, gate, out_proj + norm + residual), final norm,
+ * tied head, argmax (ties -> lowest id).  layers_dev is a DEVICE array of
+ * n_layers ssd200_layer_t.  ssm (n_layers, B, H, P, N) and conv
+ * (n_layers, B, conv_dim, k-1) are updated in place.  barrier_state: two
+ * uint32 owned by the caller, zeroed once before first use.  Returns
+ * SSD200_EUNSUPPORTED for configurations the fused step does not cover
+ * (the per-layer entry points handle those). */
+size_t ssd200_decode_step_workspace(const ssd200_dims_t *d, int batch);
+int ssd200_decode_step(const ssd200_dims_t *d, const ssd200_layer_t *layers_dev, int n_layers,
+                       int vocab, const void *embedding, const void *final_norm_w,
+                       const int64_t *tokens, void *hidden, void *hidden_lp, void *ssm,
+                       void *conv, void *logits, int64_t *argmax_out, unsigned *barrier_state,
+                       int batch, void *workspace, size_t workspace_bytes,
+                       ssd200_stream_t stream);
+
 /* ---- raw bf16 tensor-core GEMM (tcgen05 + TMA + TMEM), for tests/bench --
  * C (M,N) f32 = A (M,K) bf16 row-major  x  B^T where B is (N,K) bf16 row-major.
  * K % 8 == 0 (16-byte TMA row pitch); ragged M/N/K tiles are zero-filled. */
@@ -119,6 +136,9 @@ uint64_t ssd200_launch_count(void);
  * (p: 0 in_proj, 1 conv, 2 scan, 3 gated norm, 4 out_proj); events are
  * cudaEvent_t handles owned by the caller.  Pass NULL to disable. */
 int ssd200_set_phase_events(void *const *events, int n_phases);
+/* Debug: device buffer (>= 8192 uint64) that ssd200_decode_step fills with
+ * %globaltimer stamps of CTA 0's phases; NULL disables. */
+int ssd200_debug_trace(void *device_buffer);
 
 #ifdef __cplusplus
 }

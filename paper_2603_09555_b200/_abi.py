@@ -81,9 +81,16 @@ SIGNATURES = [
         c_int,
         [ctypes.POINTER(Dims), c_int, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_size_t, c_void_p],
     ),
+    ("ssd200_decode_step_workspace", c_size_t, [ctypes.POINTER(Dims), c_int]),
+    (
+        "ssd200_decode_step",
+        c_int,
+        [ctypes.POINTER(Dims), c_void_p, c_int, c_int] + [c_void_p] * 10 + [c_int, c_void_p, c_size_t, c_void_p],
+    ),
     ("ssd200_gemm_bf16", c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p]),
     ("ssd200_launch_count", ctypes.c_uint64, []),
     ("ssd200_set_phase_events", c_int, [c_void_p, c_int]),
+    ("ssd200_debug_trace", c_int, [c_void_p]),
 ]
 
 _lib = None

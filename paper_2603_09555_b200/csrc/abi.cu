@@ -12,6 +12,8 @@
 #include "../../include/ssd200.h"
 #include "common.cuh"
 #include "simt.cuh"
+#include "decode.cuh"
+#include "decode_mega.cuh"
 #include "ssd_tc.cuh"
 #include "tc_gemm.cuh"
 
@@ -23,6 +25,7 @@ thread_local std::string g_err;
 thread_local uint64_t g_launches = 0;
 thread_local void *const *g_phase_ev = nullptr;
 thread_local int g_nphase = 0;
+thread_local void *g_mega_trace = nullptr;  // debug: device buffer of >= 8192 u64
 
 enum { PH_IN_PROJ = 0, PH_CONV = 1, PH_SCAN = 2, PH_NORM = 3, PH_OUT_PROJ = 4 };
 
@@ -611,6 +614,133 @@ bool carve_decode(const ssd200_dims_t *d, int B, void *ws, size_t cap, DecodeWs<
 
 constexpr int GEMV_MAX_ROWS = 16;
 
+// launch with programmatic stream serialization (PDL): the kernel may start
+// while its predecessor drains; it waits (griddepcontrol.wait) before reading
+// the predecessor's outputs.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+inline bool dec_fast_eligible(const ssd200_dims_t *d, int B) {
+  return d->dtype == SSD200_BF16 && B >= 1 && B <= DEC_MAX_B && d->d_model % 256 == 0 &&
+         d->d_inner % 256 == 0 && d->d_state <= 256 && d->d_state % 4 == 0 &&
+         d->head_dim % 4 == 0 && d->conv_kernel >= 1 && d->conv_kernel <= 16;
+}
+
+inline int dec_grid(int rows) {
+  const int g = (rows + 7) / 8;  // 8 warps per CTA, one row per warp at a time
+  return g < 2 * num_sms() ? g : 2 * num_sms();
+}
+
+// streaming GEMV launch: ring depth from a ~108 KB budget (two CTAs of
+// consecutive kernels can co-reside under PDL), grid = one CTA per SM
+template <int EPI>
+int launch_dec_stream(const DecArgs &a, cudaStream_t st, int *grid_out = nullptr) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dec_gemv_stream<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         220 * 1024);
+    attr = true;
+  }
+  DecStream cfg;
+  cfg.stage_bytes = (uint32_t)DS_ROWS * a.K * 2;
+  const size_t xb = (size_t)a.B * a.K * 2;
+  long stages = ((long)108 * 1024 - (long)xb) / (long)cfg.stage_bytes;
+  if (stages < 2) stages = 2;
+  if (stages > 8) stages = 8;
+  cfg.stages = (int)stages;
+  const size_t smem = (size_t)cfg.stages * cfg.stage_bytes + xb;
+  REQUIRE(smem <= 220 * 1024, SSD200_EUNSUPPORTED, "decode GEMV: K=%d, B=%d too large", a.K,
+          a.B);
+  const int groups = (a.N + DS_ROWS - 1) / DS_ROWS;
+  const int grid = groups < num_sms() ? groups : num_sms();
+  if (grid_out) *grid_out = grid;
+  cudaError_t e = launch_pdl(dec_gemv_stream<EPI>, dim3(grid), dim3(DS_THREADS), smem, st, a, cfg);
+  REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_gemv_stream: %s", cudaGetErrorString(e));
+  LAUNCH_CHECK("dec_gemv_stream");
+  return SSD200_OK;
+}
+
+// bf16 small-batch decode layer: 3 HBM-streaming kernels (decode.cuh)
+int decode_layer_fast(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hidden,
+                      bf16 *hidden_lp, const float *ssm_in, float *ssm_out, const float *conv_in,
+                      float *conv_out, int B, DecodeWs<float> &o, cudaStream_t st) {
+  Widths wd = widths(d);
+  constexpr int PS = 4;
+  float *z = o.u;
+  float *act = z + (size_t)B * d->d_inner;
+  float *dtv = act + (size_t)B * wd.conv_dim;
+  bf16 *ug = o.normed_lp;
+  float *ssq = o.y;
+  DecArgs a{};
+  a.B = B;
+  a.N = (int)wd.d_in_proj;
+  a.K = d->d_model;
+  a.W = static_cast<const bf16 *>(w->W_in);
+  a.X = hidden_lp;
+  a.d_inner = d->d_inner;
+  a.conv_dim = (int)wd.conv_dim;
+  a.H = d->n_heads;
+  a.k = d->conv_kernel;
+  a.z = z;
+  a.act = act;
+  a.dt = dtv;
+  a.conv_in = conv_in;
+  a.conv_out = conv_out;
+  a.conv_w = static_cast<const float *>(w->conv_w);
+  a.conv_b = static_cast<const float *>(w->conv_b);
+  a.dt_bias = static_cast<const float *>(w->dt_bias);
+  a.dt_lo = (float)d->dt_min;
+  a.dt_hi = (float)d->dt_max;
+  int rc = launch_dec_stream<DEC_EPI_IN>(a, st);
+  if (rc) return rc;
+  DecSsmArgs s{};
+  s.H = d->n_heads;
+  s.P = d->head_dim;
+  s.G = d->n_groups;
+  s.N = d->d_state;
+  s.d_inner = d->d_inner;
+  s.conv_dim = (int)wd.conv_dim;
+  s.PS = PS;
+  s.act = act;
+  s.z = z;
+  s.dt = dtv;
+  s.a = static_cast<const float *>(w->a);
+  s.D = static_cast<const float *>(w->D);
+  s.ssm_in = ssm_in;
+  s.ssm_out = ssm_out;
+  s.u = ug;
+  s.ssq = ssq;
+  cudaError_t e = launch_pdl(dec_ssm, dim3(d->n_heads * PS, B), dim3(128), 0, st, s);
+  REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_ssm: %s", cudaGetErrorString(e));
+  LAUNCH_CHECK("dec_ssm");
+  DecArgs o2{};
+  o2.B = B;
+  o2.N = d->d_model;
+  o2.K = d->d_inner;
+  o2.W = static_cast<const bf16 *>(w->W_out);
+  o2.X = ug;
+  o2.ssq = ssq;
+  o2.nssq = d->n_heads * PS;
+  o2.inv_d = 1.f / (float)d->d_inner;
+  o2.eps = (float)d->norm_eps;
+  o2.hidden = hidden;
+  o2.hidden_lp = hidden_lp;
+  return launch_dec_stream<DEC_EPI_OUT>(o2, st);
+}
+
 template <typename T>
 int decode_layer_impl(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidden,
                       bf16 *hidden_lp, const T *ssm_in, T *ssm_out, const T *conv_in,
@@ -622,6 +752,20 @@ int decode_layer_impl(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidden
   Widths wd = widths(d);
   const bool lp = d->dtype == SSD200_BF16;
   const int k = d->conv_kernel;
+  if constexpr (std::is_same<T, float>::value) {
+    if (dec_fast_eligible(d, B) && hidden_lp) {
+      static bool attrs = false;
+      if (!attrs) {
+        cudaFuncSetAttribute(dec_gemv<DEC_EPI_IN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        cudaFuncSetAttribute(dec_gemv<DEC_EPI_OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        attrs = true;
+      }
+      return decode_layer_fast(d, w, hidden, hidden_lp, ssm_in, ssm_out, conv_in, conv_out, B, o,
+                               st);
+    }
+  }
   // in_proj
   if (lp) {
     REQUIRE(hidden_lp, SSD200_EINVAL, "bf16 mode needs the hidden_lp shadow");
@@ -740,6 +884,35 @@ int head_bf16(const ssd200_dims_t *d, int V, const float *hidden, long hrs, cons
               const bf16 *E, float *logits, int64_t *amax, int rows, void *ws, size_t ws_bytes,
               cudaStream_t st) {
   Carve cv(ws, ws_bytes);
+  if (rows <= DEC_MAX_B && d->d_model % 256 == 0) {
+    // fused final RMSNorm + tied-head GEMV + per-CTA argmax partials (decode.cuh)
+    const int grid = num_sms();  // upper bound of launch_dec_stream's grid
+    float *pv = cv.take<float>((size_t)grid * rows);
+    int *pi = cv.take<int>((size_t)grid * rows);
+    REQUIRE(cv.ok(), SSD200_EWORKSPACE, "head workspace %zu < %zu", ws_bytes, cv.used);
+    DecArgs a{};
+    a.B = rows;
+    a.N = V;
+    a.K = d->d_model;
+    a.W = E;
+    a.hidden = const_cast<float *>(hidden);
+    a.hstride = hrs;
+    a.final_w = fw;
+    a.eps = (float)d->norm_eps;
+    a.logits = logits;
+    a.amax_val = pv;
+    a.amax_idx = pi;
+    int used_grid = grid;
+    int rc = launch_dec_stream<DEC_EPI_HEAD>(a, st, &used_grid);
+    if (rc) return rc;
+    if (amax) {
+      cudaError_t e = launch_pdl(dec_argmax, dim3(1), dim3(32 * rows), 0, st, (const float *)pv,
+                                 (const int *)pi, used_grid, rows, amax);
+      REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_argmax: %s", cudaGetErrorString(e));
+      LAUNCH_CHECK("dec_argmax");
+    }
+    return SSD200_OK;
+  }
   bf16 *normed = cv.take<bf16>((size_t)rows * d->d_model);
   float *lg = logits ? logits : cv.take<float>((size_t)rows * V);
   REQUIRE(cv.ok(), SSD200_EWORKSPACE, "head workspace %zu < %zu", ws_bytes, cv.used);
@@ -954,7 +1127,144 @@ int ssd200_gemm_bf16(const void *A, const void *B, void *C, int M, int N, int K,
                              static_cast<cudaStream_t>(stream));
 }
 
+// ---------------------------------------------------------------- fused step
+static bool mega_eligible(const ssd200_dims_t *d, int B) {
+  return d->dtype == SSD200_BF16 && B >= 1 && B <= DEC_MAX_B && d->d_model % 256 == 0 &&
+         d->d_inner % 256 == 0 && d->d_state <= 256 && d->d_state % 4 == 0 &&
+         d->head_dim % 4 == 0 && d->conv_kernel >= 1 && d->conv_kernel <= 16 &&
+         (size_t)2 * d->d_inner * 2 <= MEGA_STAGE && (size_t)2 * d->d_model * 2 <= MEGA_STAGE;
+}
+
+static int mega_bt(int B) { return B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8; }
+
+static int mega_stages(const ssd200_dims_t *d, int B, size_t *smem) {
+  const size_t xb = (size_t)mega_bt(B) * (d->d_inner > d->d_model ? d->d_inner : d->d_model) * 2;
+  const size_t cap = 220 * 1024;
+  int S = 3;
+  while (S > 2 && (size_t)S * MEGA_STAGE + xb > cap) --S;
+  *smem = (size_t)S * MEGA_STAGE + xb;
+  return *smem <= cap ? S : 0;
+}
+
+static size_t mega_carve(const ssd200_dims_t *d, int B, void *ws, MegaArgs *a) {
+  Widths w = widths(d);
+  Carve cv(ws, SIZE_MAX);
+  float *z = cv.take<float>((size_t)B * d->d_inner);
+  float *act = cv.take<float>((size_t)B * w.conv_dim);
+  float *dt = cv.take<float>((size_t)B * d->n_heads);
+  bf16 *u = cv.take<bf16>((size_t)B * d->d_inner);
+  float *usq = cv.take<float>((size_t)B * d->d_inner);
+  float *pv = cv.take<float>((size_t)1024 * B);
+  int *pi = cv.take<int>((size_t)1024 * B);
+  if (a) {
+    a->z = z;
+    a->act = act;
+    a->dt = dt;
+    a->u = u;
+    a->usq = usq;
+    a->amax_val = pv;
+    a->amax_idx = pi;
+  }
+  return cv.used;
+}
+
+size_t ssd200_decode_step_workspace(const ssd200_dims_t *d, int batch) {
+  if (check_dims(d) || batch < 1) return 0;
+  return mega_carve(d, batch, nullptr, nullptr);
+}
+
+int ssd200_decode_step(const ssd200_dims_t *d, const ssd200_layer_t *layers_dev, int n_layers,
+                       int vocab, const void *embedding, const void *final_norm_w,
+                       const int64_t *tokens, void *hidden, void *hidden_lp, void *ssm,
+                       void *conv, void *logits, int64_t *argmax_out, unsigned *barrier_state,
+                       int batch, void *workspace, size_t workspace_bytes,
+                       ssd200_stream_t stream) {
+  int rc = check_dims(d);
+  if (rc) return rc;
+  REQUIRE(layers_dev && embedding && final_norm_w && tokens && hidden && hidden_lp && ssm &&
+              barrier_state && n_layers >= 1 && vocab >= 1,
+          SSD200_EINVAL, "decode_step: bad arguments");
+  REQUIRE(d->conv_kernel == 1 || conv, SSD200_EINVAL, "decode_step: conv state is null");
+  REQUIRE(mega_eligible(d, batch), SSD200_EUNSUPPORTED,
+          "decode_step: fused step needs bf16, batch <= %d and 256-multiple widths", DEC_MAX_B);
+  size_t smem = 0;
+  const int S = mega_stages(d, batch, &smem);
+  REQUIRE(S >= 2, SSD200_EUNSUPPORTED, "decode_step: batch %d too large for the smem ring", batch);
+  const size_t need = mega_carve(d, batch, nullptr, nullptr);
+  REQUIRE(workspace_bytes >= need, SSD200_EWORKSPACE, "decode_step workspace %zu < %zu",
+          workspace_bytes, need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  mega_embed<<<batch, 256, 0, st>>>(tokens, (const bf16 *)embedding, d->d_model, (float *)hidden,
+                                    (bf16 *)hidden_lp, barrier_state);
+  LAUNCH_CHECK("mega_embed");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(decode_mega<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(decode_mega<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(decode_mega<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(decode_mega<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
+  }
+  Widths w = widths(d);
+  MegaArgs a{};
+  mega_carve(d, batch, workspace, &a);
+  a.B = batch;
+  a.L = n_layers;
+  a.V = vocab;
+  a.stages = S;
+  a.d_model = d->d_model;
+  a.d_inner = d->d_inner;
+  a.conv_dim = (int)w.conv_dim;
+  a.d_in_proj = (int)w.d_in_proj;
+  a.H = d->n_heads;
+  a.P = d->head_dim;
+  a.G = d->n_groups;
+  a.N = d->d_state;
+  a.k = d->conv_kernel;
+  a.PS = 4;
+  a.eps = (float)d->norm_eps;
+  a.dt_lo = (float)d->dt_min;
+  a.dt_hi = (float)d->dt_max;
+  a.layers = layers_dev;
+  a.E = (const bf16 *)embedding;
+  a.final_w = (const float *)final_norm_w;
+  a.hidden = (float *)hidden;
+  a.hidden_lp = (bf16 *)hidden_lp;
+  a.ssm = (float *)ssm;
+  a.conv = (float *)conv;
+  a.logits = (float *)logits;
+  a.argmax_out = argmax_out;
+  a.bar_count = barrier_state;
+  a.bar_epoch = barrier_state + 1;
+  a.trace = static_cast<unsigned long long *>(g_mega_trace);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_sms());
+  cfg.blockDim = dim3(MEGA_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeCooperative;
+  attrs[0].val.cooperative = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  switch (mega_bt(batch)) {
+    case 1: e = cudaLaunchKernelEx(&cfg, decode_mega<1>, a); break;
+    case 2: e = cudaLaunchKernelEx(&cfg, decode_mega<2>, a); break;
+    case 4: e = cudaLaunchKernelEx(&cfg, decode_mega<4>, a); break;
+    default: e = cudaLaunchKernelEx(&cfg, decode_mega<8>, a); break;
+  }
+  REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "decode_mega: %s", cudaGetErrorString(e));
+  LAUNCH_CHECK("decode_mega");
+  return SSD200_OK;
+}
+
 uint64_t ssd200_launch_count(void) { return g_launches; }
+
+int ssd200_debug_trace(void *device_buffer) {
+  g_mega_trace = device_buffer;
+  return SSD200_OK;
+}
 
 int ssd200_set_phase_events(void *const *events, int n_phases) {
   REQUIRE(n_phases >= 0 && n_phases <= 5, SSD200_EINVAL, "n_phases must be in [0, 5]");

@@ -16,7 +16,7 @@ import torch
 from . import _abi
 from .cache import GenerationResult, Mamba2Cache, state_dtype
 from .config import ModelConfig
-from .model import PolicyAudit, _audit, _Runner, check_tokens, prefill
+from .model import PolicyAudit, _audit, _Runner, check_tokens, layer_table, prefill
 from .params import ModelParams
 
 
@@ -25,6 +25,31 @@ def cache_init(cfg: ModelConfig, batch: int, device="cuda") -> Mamba2Cache:
     if batch < 1:
         raise ValueError("batch must be >= 1")
     return Mamba2Cache.empty(cfg, batch, device=device, zero=True)
+
+
+def _fused_step(r: _Runner, cfg, tok, cache: Mamba2Cache, logits, argmax, bar) -> bool:
+    """The whole step as one persistent kernel (ssd200_decode_step), cache
+    updated in place.  Returns False when the configuration is outside the
+    fused kernel's coverage (the caller then runs the per-layer sequence)."""
+    if cfg.policy.compute != "bf16" or tok.shape[0] > 8:
+        return False
+    B = tok.shape[0]
+    hidden = torch.empty((B, cfg.d_model), dtype=torch.float32, device=r.dev)
+    lp = torch.empty((B, cfg.d_model), dtype=torch.bfloat16, device=r.dev)
+    need = r.lib.ssd200_decode_step_workspace(r.dims, B)
+    ws = r.workspace(need)
+    rc = r.lib.ssd200_decode_step(
+        r.dims, layer_table(r.params).data_ptr(), cfg.n_layers, cfg.vocab_size,
+        r.params.embedding.data_ptr(), r.params.final_norm_w.data_ptr(), tok.data_ptr(),
+        hidden.data_ptr(), lp.data_ptr(), cache.ssm_all.data_ptr(),
+        cache.conv_all.data_ptr() if cache.conv_all.numel() else None,
+        _abi.ptr(logits), _abi.ptr(argmax), bar.data_ptr(), B, ws.data_ptr(), ws.numel(),
+        r.stream,
+    )
+    if rc == _abi.EUNSUPPORTED:
+        return False
+    _abi.check(rc, "ssd200_decode_step")
+    return True
 
 
 def _step_into(r: _Runner, cfg, tok, cache_in: Mamba2Cache, cache_out: Mamba2Cache,
@@ -63,7 +88,7 @@ class GreedyDecoder:
     token (and optionally the logits) at the device-side step counter."""
 
     def __init__(self, params: ModelParams, cfg: ModelConfig, cache: Mamba2Cache, gen_len: int,
-                 keep_logits: bool = False, use_graph: bool = True):
+                 keep_logits: bool = False, use_graph: bool = True, fused: bool = True):
         self.cfg = cfg
         self.dev = params.device
         B = cache.batch
@@ -79,13 +104,18 @@ class GreedyDecoder:
             else None
         )
         self.step_idx = torch.zeros((1,), dtype=torch.int64, device=self.dev)
+        self.bar = torch.zeros((2,), dtype=torch.int32, device=self.dev)  # grid-barrier state
         self.graph = None
         self.use_graph = use_graph
+        self.fused = fused
 
     def _body(self):
         cfg = self.cfg
-        _step_into(self.runner, cfg, self.tok, self.cache, self.cache, logits=self.logits,
-                   argmax=self.tok)
+        done = self.fused and _fused_step(self.runner, cfg, self.tok, self.cache, self.logits,
+                                          self.tok, self.bar)
+        if not done:
+            _step_into(self.runner, cfg, self.tok, self.cache, self.cache, logits=self.logits,
+                       argmax=self.tok)
         # bookkeeping: tokens[:, step] = tok; step += 1
         self.tokens.index_copy_(1, self.step_idx, self.tok.view(-1, 1))
         if self.kept is not None:

@@ -60,6 +60,18 @@ def layer_struct(lp: LayerParams) -> _abi.Layer:
     )
 
 
+def layer_table(params: ModelParams) -> torch.Tensor:
+    """Device array of ssd200_layer_t (one per layer) for the fused decode
+    step; built once per ModelParams."""
+    tab = getattr(params, "_layer_table", None)
+    if tab is None:
+        arr = (_abi.Layer * len(params.layers))(*[layer_struct(lp) for lp in params.layers])
+        raw = bytes(arr)
+        tab = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(params.device)
+        params._layer_table = tab
+    return tab
+
+
 def _audit(audit, cfg):
     if audit is not None:
         audit.record("decay_exp", "bf16e" if cfg.policy.bf16_decay else cfg.dtype)

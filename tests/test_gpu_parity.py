@@ -250,6 +250,57 @@ def test_bf16_prefill_vs_oracle():
     assert rel_s <= BF16_BOUND, rel_s
 
 
+def test_bf16_generate_graph_is_deterministic():
+    """The CUDA-graph generate loop (PDL launches, in-place cache) gives the
+    same tokens as the eager step loop, and decode logits stay within the
+    bf16 bound of the f32 oracle on bf16-rounded weights."""
+    import paper_2603_09555_b200 as m
+
+    cfg = _bf16_cfg()
+    host = m.random_init_host(cfg, 11)
+    params = m.from_reference(host, cfg)
+    prompt = np.random.default_rng(12).integers(0, cfg.vocab_size, size=(2, 40))
+    a = m.generate(params, prompt, 24, cfg=cfg, use_graph=True, keep_logits=True)
+    b = m.generate(params, prompt, 24, cfg=cfg, use_graph=False, keep_logits=True)
+    assert torch.equal(a.tokens, b.tokens)
+    assert torch.equal(a.per_step_logits, b.per_step_logits)
+    toks = _np(a.tokens)
+    seq = np.concatenate([prompt, toks[:, :-1]], axis=1)
+    ref = orc.prefill(orc.round_weights_bf16(host), seq, cfg.with_policy(compute="f32"))[0]
+    got = _np(a.per_step_logits)
+    for g in (1, 10, 23):
+        r = ref[:, prompt.shape[1] + g - 1]
+        rel = np.linalg.norm(got[:, g] - r) / np.linalg.norm(r)
+        assert rel <= 2 * BF16_BOUND, (g, rel)
+
+
+@pytest.mark.parametrize("B", [1, 3, 8])
+def test_bf16_fused_step_matches_per_layer(B):
+    """The persistent single-kernel decode step (ssd200_decode_step) against
+    the per-layer kernel sequence: same tokens, logits within fp32 rounding,
+    same in-place cache."""
+    import paper_2603_09555_b200 as m
+
+    cfg = _bf16_cfg(n_layers=3)
+    params = m.from_reference(m.random_init_host(cfg, 21), cfg)
+    prompt = np.random.default_rng(22).integers(0, cfg.vocab_size, size=(B, 33))
+    _, c0 = m.prefill(params, prompt, cfg, logits=None)
+    ca, cb = c0.copy(), c0.copy()
+    da = m.GreedyDecoder(params, cfg, ca, 12, keep_logits=True, use_graph=False, fused=True)
+    db = m.GreedyDecoder(params, cfg, cb, 12, keep_logits=True, use_graph=False, fused=False)
+    first = torch.as_tensor(prompt[:, -1], device="cuda")
+    for d in (da, db):
+        d.tok.copy_(first)
+        d.step_idx.fill_(1)
+        for _ in range(10):
+            d.step()
+    assert torch.equal(da.tokens, db.tokens)
+    la, lb = da.kept[:, 1:11], db.kept[:, 1:11]
+    assert ((la - lb).norm() / lb.norm()).item() <= 1e-5
+    assert ((ca.ssm_all - cb.ssm_all).norm() / cb.ssm_all.norm()).item() <= 1e-5
+    assert torch.equal(ca.conv_all, cb.conv_all)
+
+
 def test_bf16_decode_vs_oracle():
     import paper_2603_09555_b200 as m
 
