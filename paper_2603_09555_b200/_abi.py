@@ -91,6 +91,7 @@ SIGNATURES = [
     ("ssd200_launch_count", ctypes.c_uint64, []),
     ("ssd200_set_phase_events", c_int, [c_void_p, c_int]),
     ("ssd200_debug_trace", c_int, [c_void_p]),
+    ("ssd200_set_option", c_int, [c_int, c_int]),
 ]
 
 _lib = None

@@ -26,6 +26,8 @@ thread_local uint64_t g_launches = 0;
 thread_local void *const *g_phase_ev = nullptr;
 thread_local int g_nphase = 0;
 thread_local void *g_mega_trace = nullptr;  // debug: device buffer of >= 8192 u64
+thread_local bool g_force_fused_conv = false;  // tests: exercise the fused-conv in_proj
+thread_local bool g_force_chunkscan = false;   // tests: exercise the fused state+pass scan
 
 enum { PH_IN_PROJ = 0, PH_CONV = 1, PH_SCAN = 2, PH_NORM = 3, PH_OUT_PROJ = 4 };
 
@@ -131,6 +133,24 @@ int make_map_2d(CUtensorMap *m, const void *ptr, long rows, long cols, long ld, 
   return SSD200_OK;
 }
 
+// 2-D bf16 map without swizzle, box (box_cols, box_rows)
+int make_map_2d_plain(CUtensorMap *m, const void *ptr, long rows, long cols, long ld, int box_cols,
+                      int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  REQUIRE(fn, SSD200_ELAUNCH, "cuTensorMapEncodeTiled unavailable");
+  REQUIRE(((uintptr_t)ptr & 15) == 0, SSD200_EINVAL, "TMA base pointer not 16-byte aligned");
+  REQUIRE((ld * 2) % 16 == 0, SSD200_EINVAL, "TMA row stride must be a multiple of 16 bytes");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  REQUIRE(r == CUDA_SUCCESS, SSD200_ELAUNCH, "cuTensorMapEncodeTiled(plain) failed (%d)", (int)r);
+  return SSD200_OK;
+}
+
 template <int BN, int EPI>
 int launch_tc_gemm_bn(const bf16 *A, long lda, const bf16 *B, long ldb, int M, int N, int K,
                       const TcEpilogue &ep, cudaStream_t st) {
@@ -148,7 +168,7 @@ int launch_tc_gemm_bn(const bf16 *A, long lda, const bf16 *B, long ldb, int M, i
   }
   const int tiles = ((M + Cfg::BM - 1) / Cfg::BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  tc_gemm_kernel<BN, EPI><<<grid, 192, Cfg::SMEM, st>>>(ta, tb, M, N, K, ep);
+  tc_gemm_kernel<BN, EPI><<<grid, 320, Cfg::SMEM, st>>>(ta, tb, M, N, K, ep);
   LAUNCH_CHECK("tc_gemm_kernel");
   return SSD200_OK;
 }
@@ -324,6 +344,8 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
                          (int)StateSmem::TOTAL);
     cudaFuncSetAttribute(ssd_tc_out, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)OutSmem::TOTAL);
+    cudaFuncSetAttribute(ssd_tc_chunkscan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)ScanSmem::TOTAL);
     attrs = true;
   }
   const int H = d->n_heads;
@@ -358,13 +380,19 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
   // chunk cumsums
   ssd_tc_cumsum<<<dim3(B * a.Nc, (H + 7) / 8), 256, 0, st>>>(a);
   LAUNCH_CHECK("ssd_tc_cumsum");
-  // chunk states
-  a.NG = pick_groups(H, (long)B * a.Nc, 2 * sms);
-  a.HG = H / a.NG;
-  ssd_tc_state<<<B * a.Nc * a.NG, 192, StateSmem::TOTAL, st>>>(tm_act, a);
-  LAUNCH_CHECK("ssd_tc_state");
-  ssd_tc_pass<<<dim3(B * H, TC_P * TC_N / 256), 256, 0, st>>>(a);
-  LAUNCH_CHECK("ssd_tc_pass");
+  if ((long)B * H >= (sms * 3) / 4 || g_force_chunkscan) {
+    // chunk states + inter-chunk pass fused: one CTA per (b, h), chunks in order
+    ssd_tc_chunkscan<<<B * H, 192, ScanSmem::TOTAL, st>>>(tm_act, a);
+    LAUNCH_CHECK("ssd_tc_chunkscan");
+  } else {
+    // few (b, h) pairs: parallel chunk states, then the O(Nc) pass
+    a.NG = pick_groups(H, (long)B * a.Nc, 2 * sms);
+    a.HG = H / a.NG;
+    ssd_tc_state<<<B * a.Nc * a.NG, 192, StateSmem::TOTAL, st>>>(tm_act, a);
+    LAUNCH_CHECK("ssd_tc_state");
+    ssd_tc_pass<<<dim3(B * H, TC_P * TC_N / 256), 256, 0, st>>>(a);
+    LAUNCH_CHECK("ssd_tc_pass");
+  }
   // outputs (+ D skip + gate)
   a.NG = pick_groups(H, (long)B * a.Nc * 2, 2 * sms);
   a.HG = H / a.NG;
@@ -505,21 +533,62 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
   ep.dt_bias = static_cast<const float *>(w->dt_bias);
   ep.dt_lo = (float)d->dt_min;
   ep.dt_hi = (float)d->dt_max;
+  // conv fused into the in_proj epilogue only when the K loop (d_model) is
+  // long enough to hide the extra epilogue work; otherwise the standalone
+  // streaming conv kernel is faster (measured: 370M d_model 1024 -> separate).
+  const bool fuse_conv = tc_ssd_eligible(d) && k == 4 && (d->d_model >= 2048 || g_force_fused_conv);
   phase_mark(PH_IN_PROJ, 0, st);
-  int rc = tc_gemm<TC_EPI_INPROJ>(hidden_lp, d->d_model, static_cast<const bf16 *>(w->W_in),
-                                  d->d_model, (int)rows, (int)wd.d_in_proj, d->d_model, ep, st);
-  if (rc) return rc;
-  phase_mark(PH_IN_PROJ, 1, st);
-  phase_mark(PH_CONV, 0, st);
-  if (k > 1) {
-    conv_tail_kernel<float, bf16><<<blocks_for((long)B * wd.conv_dim * (k - 1)), 256, 0, st>>>(
-        u + d->d_inner, n_split, conv_out, B, Tn, (int)wd.conv_dim, k);
-    LAUNCH_CHECK("conv_tail");
+  int rc;
+  if (fuse_conv) {
+    // conv1d + SiLU fused into the in_proj epilogue (3-row halo tiles)
+    if (Tn < k - 1) {
+      cudaError_t e = cudaMemsetAsync(conv_out, 0, sizeof(float) * B * wd.conv_dim * (k - 1), st);
+      REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "memset conv tail: %s", cudaGetErrorString(e));
+    }
+    ep.act = act;
+    ep.d_inner = d->d_inner;
+    ep.conv_dim = (int)wd.conv_dim;
+    ep.T = Tn;
+    ep.conv_w = static_cast<const float *>(w->conv_w);
+    ep.conv_b = static_cast<const float *>(w->conv_b);
+    ep.conv_tail = conv_out;
+    rc = tc_gemm<TC_EPI_INPROJ_CONV>(hidden_lp, d->d_model, static_cast<const bf16 *>(w->W_in),
+                                     d->d_model, (int)rows, (int)wd.d_in_proj, d->d_model, ep, st);
+    if (rc) return rc;
+    phase_mark(PH_IN_PROJ, 1, st);
+    phase_mark(PH_CONV, 0, st);
+  } else {
+    rc = tc_gemm<TC_EPI_INPROJ>(hidden_lp, d->d_model, static_cast<const bf16 *>(w->W_in),
+                                d->d_model, (int)rows, (int)wd.d_in_proj, d->d_model, ep, st);
+    if (rc) return rc;
+    phase_mark(PH_IN_PROJ, 1, st);
+    phase_mark(PH_CONV, 0, st);
   }
-  launch_conv<float, bf16, bf16>(u + d->d_inner, n_split, static_cast<const float *>(w->conv_w),
-                                 static_cast<const float *>(w->conv_b), act, wd.conv_dim, Tn,
-                                 (int)wd.conv_dim, k, rows, st);
-  LAUNCH_CHECK("conv_silu_prefill");
+  if (!fuse_conv) {
+    if (k > 1) {
+      conv_tail_kernel<float, bf16><<<blocks_for((long)B * wd.conv_dim * (k - 1)), 256, 0, st>>>(
+          u + d->d_inner, n_split, conv_out, B, Tn, (int)wd.conv_dim, k);
+      LAUNCH_CHECK("conv_tail");
+    }
+    if (k == 4 && n_split % 8 == 0 && d->d_inner % 8 == 0) {
+      // TMA-tiled streaming conv (ssd_tc.cuh)
+      CUtensorMap tmx;
+      rc = make_map_2d_plain(&tmx, u + d->d_inner, rows, wd.conv_dim, n_split, CONV_COLS,
+                             CONV_ROWS + 3);
+      if (rc) return rc;
+      conv_silu_tma<<<dim3(blocks_for(wd.conv_dim, CONV_COLS), blocks_for(rows, CONV_ROWS)), 256,
+                      0, st>>>(tmx, static_cast<const float *>(w->conv_w),
+                               static_cast<const float *>(w->conv_b), act, wd.conv_dim, Tn,
+                               (int)wd.conv_dim, rows);
+      LAUNCH_CHECK("conv_silu_tma");
+    } else {
+      launch_conv<float, bf16, bf16>(u + d->d_inner, n_split,
+                                     static_cast<const float *>(w->conv_w),
+                                     static_cast<const float *>(w->conv_b), act, wd.conv_dim, Tn,
+                                     (int)wd.conv_dim, k, rows, st);
+      LAUNCH_CHECK("conv_silu_prefill");
+    }
+  }
   phase_mark(PH_CONV, 1, st);
   if (tc_ssd_eligible(d)) {
     // tensor-core scan with the D skip + gate fused; the norm's row scale is
@@ -639,10 +708,6 @@ inline bool dec_fast_eligible(const ssd200_dims_t *d, int B) {
          d->head_dim % 4 == 0 && d->conv_kernel >= 1 && d->conv_kernel <= 16;
 }
 
-inline int dec_grid(int rows) {
-  const int g = (rows + 7) / 8;  // 8 warps per CTA, one row per warp at a time
-  return g < 2 * num_sms() ? g : 2 * num_sms();
-}
 
 // streaming GEMV launch: ring depth from a ~108 KB budget (two CTAs of
 // consecutive kernels can co-reside under PDL), grid = one CTA per SM
@@ -1264,6 +1329,20 @@ uint64_t ssd200_launch_count(void) { return g_launches; }
 int ssd200_debug_trace(void *device_buffer) {
   g_mega_trace = device_buffer;
   return SSD200_OK;
+}
+
+int ssd200_set_option(int option, int value) {
+  switch (option) {
+    case 1:  // force the conv1d fused into the in_proj epilogue (else size-based)
+      g_force_fused_conv = value != 0;
+      return SSD200_OK;
+    case 2:  // force the fused chunk-state + pass scan kernel (else size-based)
+      g_force_chunkscan = value != 0;
+      return SSD200_OK;
+    default:
+      set_err("unknown option %d", option);
+      return SSD200_EINVAL;
+  }
 }
 
 int ssd200_set_phase_events(void *const *events, int n_phases) {

@@ -90,7 +90,7 @@ struct DecArgs {
 // one warp per weight row; rows strided over the grid
 template <int EPI>
 __global__ __launch_bounds__(256) void dec_gemv(DecArgs a) {
-  extern __shared__ __align__(16) uint8_t dsm[];
+  extern __shared__ __align__(128) uint8_t dsm[];
   bf16 *xs = reinterpret_cast<bf16 *>(dsm);  // (B, K)
   __shared__ float s_scale[DEC_MAX_B];
   __shared__ float s_best[8][DEC_MAX_B];

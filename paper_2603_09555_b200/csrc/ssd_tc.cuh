@@ -51,6 +51,74 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int ch) {
   return (uint32_t)r * 128u + (uint32_t)((ch ^ (r & 7)) << 4);
 }
 
+// ------------------------------------------------------------------ conv1d
+// Causal depthwise conv (k = 4) + SiLU over the xBC columns, numerics.py:169-189.
+// One CTA = 256 channels x 64 tokens: one TMA load brings the [64+3, 256]
+// bf16 tile (3-row history halo; rows before the buffer start are zero-filled)
+// into smem; thread (pair p, half h) slides the window down channels
+// (2p, 2p+1) over rows [32h, 32h+32), restarting it at sequence starts.
+constexpr int CONV_ROWS = 64, CONV_COLS = 256;
+
+__global__ void __launch_bounds__(256) conv_silu_tma(const __grid_constant__ CUtensorMap tm_xbc,
+                                                     const float *__restrict__ w,
+                                                     const float *__restrict__ bias,
+                                                     bf16 *__restrict__ out, long ld_out, int T,
+                                                     int C, long rows) {
+  __shared__ __align__(128) bf16 tile[CONV_ROWS + 3][CONV_COLS];
+  __shared__ __align__(8) uint64_t bar;
+  const int c0 = blockIdx.x * CONV_COLS;
+  const long r0 = (long)blockIdx.y * CONV_ROWS;
+  if (threadIdx.x == 0) {
+    sm100::mbar_init(&bar, 1);
+    sm100::fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sm100::mbar_arrive_expect_tx(&bar, (CONV_ROWS + 3) * CONV_COLS * 2);
+    sm100::tma_load_2d(&tile[0][0], &tm_xbc, &bar, c0, (int)(r0 - 3));
+  }
+  const int pair = threadIdx.x & 127, half = threadIdx.x >> 7;
+  const int c = c0 + 2 * pair;
+  float w0[4], w1[4], b0 = 0.f, b1 = 0.f;
+  if (c + 1 < C) {
+    const float4 a = reinterpret_cast<const float4 *>(w)[c];
+    const float4 bb = reinterpret_cast<const float4 *>(w)[c + 1];
+    w0[0] = a.x; w0[1] = a.y; w0[2] = a.z; w0[3] = a.w;
+    w1[0] = bb.x; w1[1] = bb.y; w1[2] = bb.z; w1[3] = bb.w;
+    b0 = bias[c];
+    b1 = bias[c + 1];
+  }
+  sm100::mbar_wait(&bar, 0);
+  if (c + 1 >= C) return;
+  const int i0 = half * 32;  // first output row of this thread (tile row i0 + 3)
+  long r = r0 + i0;
+  int t = (int)(r % T);
+  // window: x[t-3], x[t-2], x[t-1] from the tile rows i0, i0+1, i0+2 (masked at sequence start)
+  float2 h3 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&tile[i0][2 * pair]));
+  float2 h2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&tile[i0 + 1][2 * pair]));
+  float2 h1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&tile[i0 + 2][2 * pair]));
+  if (t < 3) h3 = make_float2(0.f, 0.f);
+  if (t < 2) h2 = make_float2(0.f, 0.f);
+  if (t < 1) h1 = make_float2(0.f, 0.f);
+#pragma unroll 4
+  for (int i = 0; i < 32; ++i, ++r, ++t) {
+    if (r >= rows) break;
+    if (t == T) {  // next sequence: zero history
+      t = 0;
+      h1 = h2 = h3 = make_float2(0.f, 0.f);
+    }
+    const float2 x = __bfloat1622float2(
+        *reinterpret_cast<const __nv_bfloat162 *>(&tile[i0 + i + 3][2 * pair]));
+    const float a0 = w0[0] * h3.x + w0[1] * h2.x + w0[2] * h1.x + w0[3] * x.x + b0;
+    const float a1 = w1[0] * h3.y + w1[1] * h2.y + w1[2] * h1.y + w1[3] * x.y + b1;
+    *reinterpret_cast<__nv_bfloat162 *>(out + r * ld_out + c) =
+        __floats2bfloat162_rn(silu_fast(a0), silu_fast(a1));
+    h3 = h2;
+    h2 = h1;
+    h1 = x;
+  }
+}
+
 // ------------------------------------------------------------------ cumsum
 // grid (B*Nc, ceil(H/8)), 256 threads: one warp per (b, chunk, head).
 __global__ __launch_bounds__(256) void ssd_tc_cumsum(TcSsdArgs p) {
@@ -259,6 +327,162 @@ __global__ __launch_bounds__(256) void ssd_tc_pass(TcSsdArgs p) {
     }
   }
   p.final_state[(long)bh * PN + e] = s;
+}
+
+// ------------------------------------------------------------------ fused states + pass
+// One CTA per (b, h) walks the chunks in order (ssd.py:152-184 fused):
+//   S_c^T = B_c^T . (X_c * dt * e^{cs_end - cs})   (UMMA 128 x 64 x 256, TMEM)
+//   prev_c = s ;  s = e^{cs_end,c} s + S_c          (running state in registers:
+//                                                    thread n holds s[:, n])
+// Two smem stages (B^T 64 KB + X 32 KB) and two TMEM accumulators pipeline
+// chunk c+1's load/scale/MMA under chunk c's state update.
+struct ScanSmem {
+  static constexpr uint32_t STG = 98304;  // Bt [2 n-blocks][256 l][64 n] + X [256 l][64 p]
+  static constexpr uint32_t XO = 65536;
+  static constexpr uint32_t BAR = 2 * STG;
+  static constexpr uint32_t TOTAL = BAR + 256 + 1024;
+};
+
+__global__ void __launch_bounds__(192, 1)
+    ssd_tc_chunkscan(const __grid_constant__ CUtensorMap tm_act, TcSsdArgs p) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t *sm = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t *full = reinterpret_cast<uint64_t *>(sm + ScanSmem::BAR);  // [2] TMA landed
+  uint64_t *xsd = full + 2;    // [2] X scaled
+  uint64_t *sfull = full + 4;  // [2] accumulator ready
+  uint64_t *stfree = full + 6; // [2] stage consumed by the MMA
+  uint64_t *tfree = full + 8;  // [2] accumulator drained
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(full + 10);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x / p.H, h = blockIdx.x % p.H;
+  const int Nc = p.Nc;
+  const long csb = (long)Nc * TC_L;
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tm_act);
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&full[i], 1);
+      sm100::mbar_init(&xsd[i], 128);
+      sm100::mbar_init(&sfull[i], 1);
+      sm100::mbar_init(&stfree[i], 1);
+      sm100::mbar_init(&tfree[i], 128);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<128>(tslot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int c = 0; c < Nc; ++c) {
+        const int st = c & 1;
+        uint8_t *stg = sm + st * ScanSmem::STG;
+        sm100::mbar_wait(&stfree[st], ((c >> 1) & 1) ^ 1);
+        sm100::mbar_arrive_expect_tx(&full[st], ScanSmem::STG);
+        for (int j = 0; j < 2; ++j)
+          for (int q = 0; q < 2; ++q)
+            sm100::tma_load_3d(stg + j * 32768 + q * 16384, &tm_act, &full[st],
+                               p.d_inner + j * 64, c * TC_L + q * 128, b);
+        for (int q = 0; q < 2; ++q)
+          sm100::tma_load_3d(stg + ScanSmem::XO + q * 16384, &tm_act, &full[st], h * TC_P,
+                             c * TC_L + q * 128, b);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = sm100::idesc_bf16(128, TC_P, true, true);
+      for (int c = 0; c < Nc; ++c) {
+        const int st = c & 1;
+        const uint32_t par = (c >> 1) & 1;
+        sm100::mbar_wait(&xsd[st], par);
+        sm100::mbar_wait(&tfree[st], par ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t a0 = sm100::smem_u32(sm + st * ScanSmem::STG);
+        const uint32_t x0 = a0 + ScanSmem::XO;
+#pragma unroll
+        for (int k = 0; k < TC_L / 16; ++k) {
+          const uint64_t ad = sm100::sw128_desc(a0 + k * 2048, 32768, 1024);
+          const uint64_t bd = sm100::sw128_desc(x0 + k * 2048, 32768, 1024);
+          sm100::mma_bf16(tmem + st * TC_P, ad, bd, idesc, k > 0);
+        }
+        sm100::mma_commit(&sfull[st]);
+        sm100::mma_commit(&stfree[st]);
+      }
+    }
+  } else {
+    const int tid = threadIdx.x - 64;  // 0..127: X rows in the scale step, state row n later
+    const int q = warp & 3;
+    const int n = q * 32 + lane;
+    const float *csg = p.cs + ((long)b * p.H + h) * csb;
+    const float *dtg = p.dtT + ((long)b * p.H + h) * csb;
+    const float *ceg = p.cs_end + ((long)b * p.H + h) * Nc;
+    auto scale = [&](int c) {
+      const int st = c & 1;
+      sm100::mbar_wait(&full[st], (c >> 1) & 1);
+      const float cend = ceg[c];
+      uint8_t *xb = sm + st * ScanSmem::STG + ScanSmem::XO;
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        const int l = tid + rr * 128;
+        const long t = (long)c * TC_L + l;
+        const float w = t < p.T ? dtg[t] * ex2((cend - csg[t]) * kLog2e) : 0.f;
+        uint4 *row = reinterpret_cast<uint4 *>(xb + l * 128);
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          uint4 v = row[ch];
+          __nv_bfloat162 *e = reinterpret_cast<__nv_bfloat162 *>(&v);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 f = __bfloat1622float2(e[j]);
+            e[j] = __floats2bfloat162_rn(f.x * w, f.y * w);
+          }
+          row[ch] = v;
+        }
+      }
+      sm100::fence_proxy_async();
+      sm100::mbar_arrive(&xsd[st]);
+    };
+    float s[TC_P];
+    const long sbase = ((long)b * p.H + h) * TC_P * TC_N + n;
+#pragma unroll
+    for (int pp = 0; pp < TC_P; ++pp) s[pp] = p.init ? p.init[sbase + (long)pp * TC_N] : 0.f;
+    scale(0);
+    for (int c = 0; c < Nc; ++c) {
+      if (c + 1 < Nc) scale(c + 1);
+      const int st = c & 1;
+      sm100::mbar_wait(&sfull[st], (c >> 1) & 1);
+      sm100::tc_fence_after();
+      uint32_t r0[32], r1[32];
+      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + st * TC_P;
+      sm100::tmem_ld32(ta, r0);
+      sm100::tmem_ld32(ta + 32, r1);
+      sm100::tmem_ld_wait();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&tfree[st]);
+      const float decay = expf(ceg[c]);
+      bf16 *pv = p.prev + (((long)b * Nc + c) * p.H + h) * TC_P * TC_N + n;
+#pragma unroll
+      for (int pp = 0; pp < 32; ++pp) {
+        pv[(long)pp * TC_N] = __float2bfloat16_rn(s[pp]);  // state entering chunk c
+        s[pp] = decay * s[pp] + __uint_as_float(r0[pp]);
+      }
+#pragma unroll
+      for (int pp = 0; pp < 32; ++pp) {
+        pv[(long)(pp + 32) * TC_N] = __float2bfloat16_rn(s[pp + 32]);
+        s[pp + 32] = decay * s[pp + 32] + __uint_as_float(r1[pp]);
+      }
+    }
+#pragma unroll
+    for (int pp = 0; pp < TC_P; ++pp) p.final_state[sbase + (long)pp * TC_N] = s[pp];
+  }
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<128>(tmem);
+  }
 }
 
 }  // namespace ssd200

@@ -8,12 +8,14 @@
 //              (model.py:141-142 + ssd.py:115-136 fused)
 //   EPI_RESID  hidden_f32 += acc, hidden_bf16 = bf16(hidden)  (model.py:168-173)
 //
-// Structure (one CTA per SM, 6 warps):
+// Structure (one CTA per SM, 10 warps):
 //   warp 0      TMA producer: A/B k-blocks (64 bf16 = 128 B rows, SWIZZLE_128B)
 //               into a STAGES-deep smem ring (full/empty mbarriers)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
 //               (128 x BN x 16 per instruction), commits free smem stages
-//   warps 2..5  epilogue: tcgen05.ld 32x32b from TMEM -> registers -> global;
+//   warps 2..9  epilogue (two per TMEM lane quarter, alternating 32-column
+//               chunks; residual loads prefetched one chunk ahead):
+//               tcgen05.ld 32x32b from TMEM -> registers -> global;
 //               two TMEM accumulators so tile i's epilogue overlaps tile i+1's
 //               mainloop.
 #pragma once
@@ -26,7 +28,19 @@ namespace ssd200 {
 // TC_EPI_RESID_NORM: hidden += acc * rstd(row), rstd = 1/sqrt(sum_g ssq[row,g]/d + eps):
 // the gated RMSNorm's row scale applied after the GEMM (it commutes with it;
 // norm_w is folded into W_out's columns at load time) — numerics.py:149-158.
-enum { TC_EPI_F32 = 0, TC_EPI_BF16 = 1, TC_EPI_INPROJ = 2, TC_EPI_RESID = 3, TC_EPI_RESID_NORM = 4 };
+// TC_EPI_INPROJ_CONV: in_proj with the causal depthwise conv (k = 4) + SiLU of
+// the xBC columns fused (numerics.py:169-189): M tiles overlap by a 3-row halo
+// (row stride 125), the taps' history rows come from neighbouring TMEM lanes
+// (warp shuffles, plus a small smem exchange across warps); writes z (bf16),
+// post-conv xBC (bf16), dt (f32) and the pre-activation conv tail (f32).
+enum {
+  TC_EPI_F32 = 0,
+  TC_EPI_BF16 = 1,
+  TC_EPI_INPROJ = 2,
+  TC_EPI_RESID = 3,
+  TC_EPI_RESID_NORM = 4,
+  TC_EPI_INPROJ_CONV = 5
+};
 
 struct TcEpilogue {
   void *C;        // F32: float*, BF16/INPROJ: bf16*, RESID: float* (hidden)
@@ -40,6 +54,17 @@ struct TcEpilogue {
   const float *ssq;  // RESID_NORM: (M, ng) partial sums of u^2
   int ng;
   float inv_d, eps;
+  // INPROJ_CONV
+  bf16 *act;            // (M, conv_dim) post-conv xBC
+  int d_inner, conv_dim, T;
+  const float *conv_w;  // (conv_dim, 4)
+  const float *conv_b;  // (conv_dim)
+  float *conv_tail;     // (M / T, conv_dim, 3)
+};
+
+template <int EPI> struct TcRows {
+  static constexpr int STRIDE = EPI == TC_EPI_INPROJ_CONV ? 125 : 128;  // output rows per tile
+  static constexpr int HALO = 128 - STRIDE;
 };
 
 template <int BN> struct TcCfg {
@@ -144,7 +169,7 @@ __device__ __forceinline__ void tc_store_chunk(const TcEpilogue &ep, uint32_t (&
 }
 
 template <int BN, int EPI>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int M, int N, int K, TcEpilogue ep) {
   using Cfg = TcCfg<BN>;
@@ -161,9 +186,11 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int RSTRIDE = TcRows<EPI>::STRIDE, HALO = TcRows<EPI>::HALO;
   const int num_n = (N + BN - 1) / BN;
-  const int num_tiles = ((M + BM - 1) / BM) * num_n;
+  const int num_tiles = ((M + RSTRIDE - 1) / RSTRIDE) * num_n;
   const int num_kb = (K + BK - 1) / BK;
+  __shared__ float xch[2][2][4][3][32];  // INPROJ_CONV: [half][buf][quarter][row][col]
 
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tmA);
@@ -174,7 +201,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&tfull[s], 1);
-      sm100::mbar_init(&tempty[s], 4);
+      sm100::mbar_init(&tempty[s], 8);
     }
     sm100::fence_barrier_init();
   }
@@ -193,7 +220,8 @@ __global__ void __launch_bounds__(192, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           sm100::mbar_wait(&empty[s], ph ^ 1);
           sm100::mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
-          sm100::tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * BK, m_blk * BM);
+          sm100::tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * BK,
+                             m_blk * RSTRIDE - HALO);
           sm100::tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, &full[s], kb * BK, n_blk * BN);
           if (++s == STAGES) {
             s = 0;
@@ -235,31 +263,136 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
+    // 8 epilogue warps: two per TMEM lane quarter, alternating 32-column chunks
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;
+    constexpr bool RESID = (EPI == TC_EPI_RESID || EPI == TC_EPI_RESID_NORM);
+    const bool vec_ok = (ep.ldc & 7) == 0;
     int local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const int m_blk = tile / num_n, n_blk = tile % num_n;
       const int as = local & 1;
       const uint32_t aph = (local >> 1) & 1;
-      sm100::mbar_wait(&tfull[as], aph);
-      sm100::tc_fence_after();
-      const int m = m_blk * BM + q * 32 + lane;
-      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
+      const int i_row = q * 32 + lane;                 // tile row == TMEM lane
+      const int m = m_blk * RSTRIDE - HALO + i_row;    // global row (HALO = 0: m_blk*128+i)
+      const bool out_row = i_row >= HALO && m < M;
+      // row-only inputs before the wait: the norm scale and the first residual chunk
       float rowscale = 1.f;
       if (EPI == TC_EPI_RESID_NORM && m < M) {
         float s = 0.f;
         for (int gg = 0; gg < ep.ng; ++gg) s += ep.ssq[(size_t)m * ep.ng + gg];
         rowscale = 1.f / sqrtf(s * ep.inv_d + ep.eps);
       }
+      float4 hv[8];
+      auto fetch = [&](int cc, float4(&dst)[8]) {
+        const int n0 = n_blk * BN + cc;
+        if (RESID && m < M && vec_ok && n0 + 32 <= N && cc < BN) {
+          const float4 *src =
+              reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(ep.C) +
+                                               (size_t)m * ep.ldc + n0);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) dst[j] = src[j];
+        }
+      };
+      fetch(half * 32, hv);
+      sm100::mbar_wait(&tfull[as], aph);
+      sm100::tc_fence_after();
+      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
 #pragma unroll 1
-      for (int cc = 0; cc < BN; cc += 32) {
+      for (int cc = half * 32; cc < BN; cc += 64) {
         const int n0 = n_blk * BN + cc;
         if (n0 >= N) break;  // warp-uniform
+        float4 hn[8];
+        fetch(cc + 64, hn);  // next residual chunk in flight during this one
         uint32_t r[32];
         sm100::tmem_ld32(trow + cc, r);
         sm100::tmem_ld_wait();
-        if (m < M) tc_store_chunk<EPI>(ep, r, m, n0, N, rowscale);
+        if constexpr (EPI == TC_EPI_INPROJ_CONV) {
+          if (n0 >= ep.d_inner && n0 < ep.d_inner + ep.conv_dim) {
+            // ---- xBC chunk: causal k=4 conv + SiLU across rows (lanes)
+            const int xb = (cc >> 6) & 1;
+            if (lane >= 29) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) xch[half][xb][q][lane - 29][j] = __uint_as_float(r[j]);
+            }
+            asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
+            const int t = out_row ? m % ep.T : 0;
+            const int c0 = n0 - ep.d_inner;
+            uint32_t pk[16];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float v = __uint_as_float(r[j]);
+              float h1 = __shfl_up_sync(0xffffffffu, v, 1);
+              float h2 = __shfl_up_sync(0xffffffffu, v, 2);
+              float h3 = __shfl_up_sync(0xffffffffu, v, 3);
+              if (lane < 3 && q > 0) {
+                const float p0 = xch[half][xb][q - 1][0][j];  // previous warp's lane 29
+                const float p1 = xch[half][xb][q - 1][1][j];  // lane 30
+                const float p2 = xch[half][xb][q - 1][2][j];  // lane 31
+                if (lane == 0) {
+                  h1 = p2;
+                  h2 = p1;
+                  h3 = p0;
+                } else if (lane == 1) {
+                  h2 = p2;
+                  h3 = p1;
+                } else {
+                  h3 = p2;
+                }
+              }
+              if (t < 1) h1 = 0.f;  // zero history before the sequence start
+              if (t < 2) h2 = 0.f;
+              if (t < 3) h3 = 0.f;
+              const float4 wc = reinterpret_cast<const float4 *>(ep.conv_w)[c0 + j];
+              const float a = wc.x * h3 + wc.y * h2 + wc.z * h1 + wc.w * v + ep.conv_b[c0 + j];
+              const float o = silu_fast(a);
+              if (j & 1)
+                pk[j >> 1] |= (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(o)) << 16;
+              else
+                pk[j >> 1] = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(o));
+            }
+            if (out_row) {
+              uint4 *dst = reinterpret_cast<uint4 *>(ep.act + (size_t)m * ep.conv_dim + c0);
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+              if (t >= ep.T - 3) {  // pre-activation conv tail, newest last (model.py:144-147)
+                float *tail = ep.conv_tail + ((size_t)(m / ep.T) * ep.conv_dim + c0) * 3 +
+                              (t - (ep.T - 3));
+#pragma unroll
+                for (int j = 0; j < 32; ++j) tail[j * 3] = __uint_as_float(r[j]);
+              }
+            }
+          } else if (out_row) {
+            // z columns (bf16) or dt columns (f32 softplus), like TC_EPI_INPROJ
+            tc_store_chunk<TC_EPI_INPROJ>(ep, r, m, n0, N, 1.f);
+          }
+        } else if (m < M) {
+          if (RESID && vec_ok && n0 + 32 <= N) {
+            float *dst = reinterpret_cast<float *>(ep.C) + (size_t)m * ep.ldc + n0;
+            bf16 *lp = ep.C_lp + (size_t)m * ep.ldc + n0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4 o = hv[j];
+              o.x += __uint_as_float(r[4 * j + 0]) * rowscale;
+              o.y += __uint_as_float(r[4 * j + 1]) * rowscale;
+              o.z += __uint_as_float(r[4 * j + 2]) * rowscale;
+              o.w += __uint_as_float(r[4 * j + 3]) * rowscale;
+              reinterpret_cast<float4 *>(dst)[j] = o;
+              uint2 pk;
+              pk.x = pack_bf16x2(o.x, o.y);
+              pk.y = pack_bf16x2(o.z, o.w);
+              reinterpret_cast<uint2 *>(lp)[j] = pk;
+            }
+          } else {
+            tc_store_chunk<EPI>(ep, r, m, n0, N, rowscale);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) hv[j] = hn[j];
       }
+      if constexpr (EPI == TC_EPI_INPROJ_CONV)  // exchange buffers free for the next tile
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[as]);

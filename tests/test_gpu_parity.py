@@ -233,14 +233,23 @@ def _bf16_cfg(**kw):
     return ModelConfig(policy=ElemPolicy(compute="bf16"), **base)
 
 
-def test_bf16_prefill_vs_oracle():
+@pytest.mark.parametrize("chunkscan", [False, True])
+def test_bf16_prefill_vs_oracle(chunkscan):
+    """bf16 prefill (tensor-core GEMMs + SSD) vs the f32 oracle on the same
+    bf16-rounded weights; both scan variants (parallel states + pass, and
+    the fused per-(b, h) chunk walk)."""
     import paper_2603_09555_b200 as m
+    from paper_2603_09555_b200 import _abi
 
     cfg = _bf16_cfg()
     host = m.random_init_host(cfg, 4)
     params = m.from_reference(host, cfg)
     toks = np.random.default_rng(5).integers(0, cfg.vocab_size, size=(2, 300))
-    logits, cache = m.prefill(params, toks, cfg)
+    _abi.lib().ssd200_set_option(2, int(chunkscan))
+    try:
+        logits, cache = m.prefill(params, toks, cfg)
+    finally:
+        _abi.lib().ssd200_set_option(2, 0)
     ref_logits, ref_ssm, _ = orc.prefill(orc.round_weights_bf16(host), toks, cfg.with_policy(compute="f32"))
     got = _np(logits)
     rel = np.linalg.norm(got - ref_logits) / np.linalg.norm(ref_logits)
@@ -299,6 +308,34 @@ def test_bf16_fused_step_matches_per_layer(B):
     assert ((la - lb).norm() / lb.norm()).item() <= 1e-5
     assert ((ca.ssm_all - cb.ssm_all).norm() / cb.ssm_all.norm()).item() <= 1e-5
     assert torch.equal(ca.conv_all, cb.conv_all)
+
+
+@pytest.mark.parametrize("B,T", [(1, 1), (2, 2), (3, 5), (2, 125), (1, 253), (2, 600)])
+def test_bf16_fused_conv_edges(B, T):
+    """in_proj with the conv fused into its epilogue (125-row tiles, 3-row
+    halo): sequence starts inside tiles, T < k-1 zero-padded tails, ragged
+    tiles — checked against the oracle on bf16-rounded weights."""
+    import paper_2603_09555_b200 as m
+    from paper_2603_09555_b200 import _abi
+
+    cfg = _bf16_cfg(n_layers=1)
+    host = m.random_init_host(cfg, 31)
+    params = m.from_reference(host, cfg)
+    toks = np.random.default_rng(32 + T).integers(0, cfg.vocab_size, size=(B, T))
+    _abi.lib().ssd200_set_option(1, 1)
+    try:
+        logits, cache = m.prefill(params, toks, cfg)
+    finally:
+        _abi.lib().ssd200_set_option(1, 0)
+    ref_logits, ref_ssm, ref_conv = orc.prefill(orc.round_weights_bf16(host), toks,
+                                                cfg.with_policy(compute="f32"))
+    got = _np(logits)
+    assert np.linalg.norm(got - ref_logits) / np.linalg.norm(ref_logits) <= BF16_BOUND
+    rc = np.stack(ref_conv)
+    gc = _np(cache.conv_all)
+    assert np.linalg.norm(gc - rc) / max(np.linalg.norm(rc), 1e-30) <= BF16_BOUND
+    if T < 3:
+        assert np.all(gc[..., : 3 - T] == 0)
 
 
 def test_bf16_decode_vs_oracle():
