@@ -327,9 +327,12 @@ int make_map_3d(CUtensorMap *m, const void *ptr, long B, long T, long cols, long
 }
 
 // smallest divisor of H giving at least `target` CTAs over `units` work units
-inline int pick_groups(int H, long units, long target) {
+// (and at most max_hg heads per group)
+inline int pick_groups(int H, long units, long target, int max_hg = 1 << 30) {
   for (int ng = 1; ng <= H; ++ng)
-    if (H % ng == 0 && units * ng >= target) return ng;
+    if (H % ng == 0 && H / ng <= max_hg && units * ng >= target) return ng;
+  for (int ng = 1; ng <= H; ++ng)
+    if (H % ng == 0 && H / ng <= max_hg) return ng;
   return H;
 }
 
@@ -371,6 +374,7 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
   a.final_state = final_state;
   a.u_out = u_out;
   a.ssq = ssq;
+  a.trace = static_cast<unsigned long long *>(g_mega_trace);
   CUtensorMap tm_act, tm_prev;
   int rc = make_map_3d(&tm_act, act, B, Tn, conv_dim, conv_dim, 128);
   if (rc) return rc;
@@ -394,7 +398,7 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
     LAUNCH_CHECK("ssd_tc_pass");
   }
   // outputs (+ D skip + gate)
-  a.NG = pick_groups(H, (long)B * a.Nc * 2, 2 * sms);
+  a.NG = pick_groups(H, (long)B * a.Nc * 2, 2 * sms, OutSmem::MAX_HG);
   a.HG = H / a.NG;
   ssd_tc_out<<<B * a.Nc * 2 * a.NG, OUT_THREADS, OutSmem::TOTAL, st>>>(tm_act, tm_prev, a, act,
                                                                         conv_dim);

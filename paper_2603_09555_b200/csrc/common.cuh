@@ -57,6 +57,13 @@ __device__ __forceinline__ float ex2(float v) {
 __device__ __forceinline__ float silu_fast(float x) {
   return __fdividef(x, 1.f + ex2(-x * kLog2e));
 }
+// silu(x) = x/2 (1 + tanh(x/2)): one MUFU op instead of two (|rel err| < 2^-10)
+__device__ __forceinline__ float silu_tanh(float x) {
+  float t;
+  const float h = 0.5f * x;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
+  return fmaf(h, t, h);
+}
 
 template <typename T> __device__ __forceinline__ T clamp_(T v, T lo, T hi) {
   return v < lo ? lo : (v > hi ? hi : v);

@@ -40,7 +40,14 @@ struct TcSsdArgs {
   float *final_state; // (B, H, P, N)
   bf16 *u_out;        // (rows, d_inner)
   float *ssq;         // (rows, NG) partial sum of u^2
+  unsigned long long *trace;  // debug: clock stamps of CTA 0 (or null)
 };
+
+__device__ __forceinline__ unsigned long long clk64() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %clock64;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");

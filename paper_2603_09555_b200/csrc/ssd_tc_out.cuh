@@ -3,42 +3,65 @@
 // One CTA per (batch b, chunk c, 128-row tile R of the chunk, head group g):
 //   G = C_R . B^T   (128 x 128(R+1) x 128 UMMA, once; shared by every head, G = 1)
 //   per head h:
-//     M[l,s] = G[l,s] * e^{cs_l - cs_s} * dt_s  (s <= l)  -> bf16, K-major SW128 smem
+//     M[l,s] = G[l,s] * e^{cs_l - cs_s} * dt_s  (s <= l)  -> bf16, written to TMEM
 //       the decay is factorised per 32-column chunk J (r = last index of J):
 //         e^{cs_l - cs_s} = e^{cs_l - cs_r} * e^{cs_r - cs_s},   both factors <= 1
 //       so each (row, chunk) needs one ex2 and each column one ex2 per head;
 //       only the diagonal chunk (s, l in the same 32-block) exponentiates
 //       per element (ssd.py:147-148 / numerics.py:134-146 restated)
-//     Ydiag = M . X_h        (K = 128(R+1))                        ssd.py:149
-//     Yoff  = C_R . prev_h^T (K = N = 128)                          ssd.py:196
-//     y = Ydiag + e^{cs_l} Yoff + D_h x;  u = y * silu(z);  sum u^2  model.py:166-167
-// Pipeline: X / prev tiles and the two TMEM accumulator sets are double
-// buffered, so head h's epilogue runs while the tensor core computes head
-// h+1 and TMA fetches head h+2; per-head column constants are prefetched one
-// head ahead into warp-private smem (no block barriers in the head loop).
-// Warp roles (320 threads): warp 0 TMA, warp 1 MMA + TMEM owner, warps 2..9
-// math — two warps per TMEM lane quarter, splitting the columns.
+//     Ydiag = M . X_h        (K = 128(R+1)), A operand read from TMEM   ssd.py:149
+//     Yoff  = C_R . prev_h^T (K = N = 128)                               ssd.py:196
+//     y = Ydiag + e^{cs_l} Yoff + D_h x;  u = y * silu(z);  sum u^2       model.py:166-167
+//
+// M lives in TMEM (tcgen05.st by the math warps, consumed as the A operand of
+// tcgen05.mma), double buffered: the math warps build M_{h+1} while the tensor
+// core multiplies M_h, with no shared-memory round trip and no proxy fence.
+// G itself is kept as bf16 in shared memory (the B-row staging area, free once
+// G is computed) so TMEM holds only the two M buffers and two accumulator sets:
+//   TMEM cols [0,128) M buffer 0, [128,256) M buffer 1 (bf16 pairs per column),
+//             [256+128k, +64) Ydiag set k, [320+128k, +64) Yoff set k.
+// X / prev tiles are double buffered as well, so head h's epilogue runs while
+// the tensor core computes head h+1 and TMA fetches head h+2.
+// Warp roles: warp 0 TMA, warp 1 MMA + TMEM owner, then OUT_KW math warps per
+// TMEM lane quarter: warp k of a quarter builds columns [CW k, CW (k+1)) of
+// every 32-column chunk of M, CW = 32 / OUT_KW (so the expensive diagonal chunk
+// is shared evenly) and runs the epilogue on head columns [EW k, EW (k+1)),
+// EW = 64 / OUT_KW.
 // Block order: the heavier R = 1 tiles first, then R = 0.
 #pragma once
+
+#include <type_traits>
 
 #include "common.cuh"
 #include "sm100.cuh"
 
 namespace ssd200 {
 
-struct OutSmem {
-  static constexpr uint32_t CR = 0;                  // C rows of the tile: 2 x [128 l][64 n]
-  static constexpr uint32_t BM = 32768;              // B rows (G operand), then M: 64 KB
-  static constexpr uint32_t X0 = BM + 65536;         // 2 x [256 s][64 p]
-  static constexpr uint32_t P0 = X0 + 2 * 32768;     // 2 x (2 x [64 p][64 n])
-  static constexpr uint32_t WC = P0 + 2 * 16384;     // 8 warps x 3 x 256 f32 (cs2, cf, dt)
-  static constexpr uint32_t SQ = WC + 8 * 3 * 1024;  // 128 f32: ssq of the second half
-  static constexpr uint32_t BAR = SQ + 512;
-  static constexpr uint32_t TOTAL = BAR + 256 + 1024;
-};
+#ifndef SSD200_OUT_KW
+#define SSD200_OUT_KW 2
+#endif
+constexpr int OUT_KW = SSD200_OUT_KW;  // math warps per TMEM lane quarter (2 or 4)
+constexpr int OUT_CW = 32 / OUT_KW;    // columns of every 32-column M chunk per warp
+constexpr int OUT_MW = 4 * OUT_KW;     // math warps
+constexpr int OUT_EW = TC_P / OUT_KW;  // epilogue head columns per warp
+constexpr int OUT_MATH = OUT_MW * 32;  // math threads
+constexpr int OUT_THREADS = OUT_MATH + 64;
+#ifndef SSD200_OUT_TRACE
+#define SSD200_OUT_TRACE 0  // 1: clock64 stamps of CTA 0 into TcSsdArgs::trace (scripts/trace_ssd_out.py)
+#endif
 
-constexpr int OUT_THREADS = 320;
-constexpr int OUT_MATH = 256;
+struct OutSmem {
+  static constexpr uint32_t CR = 0;           // C rows of the tile: 2 x [128 l][64 n] (SW128)
+  static constexpr uint32_t GB = 32768;       // B rows 2 x [NS s][64 n]; then G bf16 [128 l][NS s]
+  static constexpr uint32_t X0 = GB + 65536;  // 2 x [256 s][64 p]
+  static constexpr uint32_t P0 = X0 + 2 * 32768;  // 2 x (2 x [64 p][64 n])
+  static constexpr uint32_t WC = P0 + 2 * 16384;  // per warp 4 x 8 OUT_CW f32 (cs2, cf, dt, cr)
+  static constexpr uint32_t SQ = WC + OUT_MW * 4 * 8 * OUT_CW * 4;  // ssq of slices 1..
+  static constexpr uint32_t DH = SQ + (OUT_KW - 1) * 512;  // D of the group's heads (<= 128)
+  static constexpr uint32_t BAR = DH + 512;
+  static constexpr uint32_t TOTAL = BAR + 256 + 1024;
+  static constexpr int MAX_HG = 128;  // heads per CTA (DH table)
+};
 
 // 1024-byte aligned view of dynamic smem that keeps the shared address space
 // visible to the compiler (STS/LDS instead of generic accesses)
@@ -54,14 +77,14 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
   uint8_t *sm = smem_align1k(smem_raw);
   uint64_t *bar_cb = reinterpret_cast<uint64_t *>(sm + OutSmem::BAR);
   uint64_t *bar_g = bar_cb + 1;
-  uint64_t *bar_x = bar_cb + 2;   // [2]
-  uint64_t *xfree = bar_cb + 4;   // [2]
-  uint64_t *bar_p = bar_cb + 6;   // [2]
-  uint64_t *pfree = bar_cb + 8;   // [2]
-  uint64_t *bar_m = bar_cb + 10;
-  uint64_t *bar_y = bar_cb + 11;  // [2]
-  uint64_t *yfree = bar_cb + 13;  // [2]
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bar_cb + 15);
+  uint64_t *bar_x = bar_cb + 2;   // [2] X tile landed
+  uint64_t *xfree = bar_cb + 4;   // [2] X tile consumed
+  uint64_t *bar_p = bar_cb + 6;   // [2] prev tile landed
+  uint64_t *pfree = bar_cb + 8;   // [2] prev tile consumed
+  uint64_t *bar_y = bar_cb + 10;  // [2] accumulator set ready
+  uint64_t *yfree = bar_cb + 12;  // [2] accumulator set read out
+  uint64_t *mrdy = bar_cb + 14;   // [2] M buffer written (one arrival per math warp)
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bar_cb + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half_grid = gridDim.x >> 1;
@@ -72,8 +95,7 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
   const int b = idx / p.Nc, c = idx % p.Nc;
   const int h0 = g * p.HG;
   const int NS = 128 * (R + 1);  // columns s of this row tile
-  // TMEM: G [0,256), accumulator set k: Ydiag [256+128k, +64), Yoff [320+128k, +64)
-  const uint32_t TM_G = 0, TM_Y = 256;
+  const uint32_t TM_M = 0, TM_Y = 256;
 
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tm_act);
@@ -87,8 +109,8 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
       sm100::mbar_init(&pfree[i], 1);
       sm100::mbar_init(&bar_y[i], 1);
       sm100::mbar_init(&yfree[i], OUT_MATH);
+      sm100::mbar_init(&mrdy[i], OUT_MW);
     }
-    sm100::mbar_init(bar_m, OUT_MATH);
     sm100::fence_barrier_init();
   }
   if (warp == 1) sm100::tmem_alloc<512>(tslot);
@@ -105,7 +127,7 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
         sm100::tma_load_3d(sm + OutSmem::CR + nb * 16384, &tm_act, bar_cb,
                            p.d_inner + TC_N + nb * 64, c * TC_L + R * 128, b);
         for (int q = 0; q <= R; ++q)
-          sm100::tma_load_3d(sm + OutSmem::BM + nb * NS * 128 + q * 16384, &tm_act, bar_cb,
+          sm100::tma_load_3d(sm + OutSmem::GB + nb * NS * 128 + q * 16384, &tm_act, bar_cb,
                              p.d_inner + nb * 64, c * TC_L + q * 128, b);
       }
       for (int i = 0; i < p.HG; ++i) {
@@ -128,15 +150,15 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t cr = sm100::smem_u32(sm + OutSmem::CR);
-      const uint32_t bm = sm100::smem_u32(sm + OutSmem::BM);
+      const uint32_t gb = sm100::smem_u32(sm + OutSmem::GB);
       sm100::mbar_wait(bar_cb, 0);
       sm100::tc_fence_after();
       const uint32_t idg = sm100::idesc_bf16(128, NS, false, false);
 #pragma unroll
-      for (int k = 0; k < TC_N / 16; ++k) {
+      for (int k = 0; k < TC_N / 16; ++k) {  // G into TMEM cols [0, NS) (before any M)
         const uint64_t ad = sm100::sw128_desc(cr + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
-        const uint64_t bd = sm100::sw128_desc(bm + (k >> 2) * NS * 128 + (k & 3) * 32, 16, 1024);
-        sm100::mma_bf16(tmem + TM_G, ad, bd, idg, k > 0);
+        const uint64_t bd = sm100::sw128_desc(gb + (k >> 2) * NS * 128 + (k & 3) * 32, 16, 1024);
+        sm100::mma_bf16(tmem + TM_M, ad, bd, idg, k > 0);
       }
       sm100::mma_commit(bar_g);
       constexpr uint32_t idy = sm100::idesc_bf16(128, TC_P, false, true);
@@ -145,209 +167,344 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
         const int buf = i & 1;
         const uint32_t par = (i >> 1) & 1;
         const uint32_t yd = tmem + TM_Y + buf * 128, yo = yd + 64;
+#if SSD200_OUT_TRACE
+        unsigned long long *tr =
+            (p.trace && blockIdx.x == 0 && i < 64) ? p.trace + i * 8 : nullptr;
+#endif
+#if SSD200_OUT_TRACE
+        if (tr) tr[0] = clk64();
+#endif
         sm100::mbar_wait(&yfree[buf], par ^ 1);
+#if SSD200_OUT_TRACE
+        if (tr) tr[1] = clk64();
+#endif
         sm100::mbar_wait(&bar_p[buf], par);
-        sm100::mbar_wait(bar_m, i & 1);
+#if SSD200_OUT_TRACE
+        if (tr) tr[2] = clk64();
+#endif
         sm100::tc_fence_after();
         const uint32_t pb = sm100::smem_u32(sm + OutSmem::P0 + buf * 16384);
 #pragma unroll
-        for (int k = 0; k < TC_N / 16; ++k) {  // Yoff = C_R . prev^T
+        for (int k = 0; k < TC_N / 16; ++k) {  // Yoff = C_R . prev^T (independent of M)
           const uint64_t ad = sm100::sw128_desc(cr + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
           const uint64_t bd = sm100::sw128_desc(pb + (k >> 2) * 8192 + (k & 3) * 32, 16, 1024);
           sm100::mma_bf16(yo, ad, bd, ido, k > 0);
         }
         sm100::mma_commit(&pfree[buf]);
         sm100::mbar_wait(&bar_x[buf], par);
+        sm100::mbar_wait(&mrdy[buf], par);
+#if SSD200_OUT_TRACE
+        if (tr) tr[3] = clk64();
+#endif
         sm100::tc_fence_after();
         const uint32_t xb = sm100::smem_u32(sm + OutSmem::X0 + buf * 32768);
-        for (int k = 0; k < NS / 16; ++k) {  // Ydiag = M . X
-          const uint64_t ad = sm100::sw128_desc(bm + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
+        const uint32_t am = tmem + TM_M + buf * 128;
+        for (int k = 0; k < NS / 16; ++k) {  // Ydiag = M . X, M from TMEM
           const uint64_t bd = sm100::sw128_desc(xb + k * 2048, 8192, 1024);
-          sm100::mma_bf16(yd, ad, bd, idy, k > 0);
+          sm100::mma_bf16_ts(yd, am + k * 8, bd, idy, k > 0);
         }
-        sm100::mma_commit(&bar_y[buf]);  // accumulators ready; M buffer free
-        sm100::mma_commit(&xfree[buf]);  // X buffer free
+#if SSD200_OUT_TRACE
+        if (tr) tr[7] = clk64();
+#endif
+        sm100::mma_commit(&bar_y[buf]);  // accumulators ready, M buffer and X tile free
+        sm100::mma_commit(&xfree[buf]);
       }
     }
   } else {
     // ------------------------------------------------------------ math warps
-    const int mw = warp - 2;           // 0..7
-    const int q = warp & 3;            // TMEM lane quarter
-    const int hf = mw >> 2;            // column-chunk parity owned by this warp
-    const int row = q * 32 + lane;     // tile row == TMEM lane
-    const int l = R * 128 + row;       // row within the chunk
+    constexpr int CW = OUT_CW, CL = CW / 4, CP = CW / 8;
+    const int mw = warp - 2;        // 0 .. OUT_MW-1
+    const int q = warp & 3;         // TMEM lane quarter
+    const int kw = mw >> 2;         // column slice: CW columns of every 32-column chunk
+    const int row = q * 32 + lane;  // tile row == TMEM lane
+    const int l = R * 128 + row;    // row within the chunk
     const int t = c * TC_L + l;
     const bool valid = t < p.T;
-    const int jd = 4 * R + q;          // this warp's diagonal 32-column chunk
+    const int jd = 4 * R + q;  // this quarter's diagonal 32-column chunk
+    const int nj = NS / 32;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const long csb = (long)p.Nc * TC_L;
-    float *wcs = reinterpret_cast<float *>(sm + OutSmem::WC) + mw * 768;
-    float *wcf = wcs + 256;
-    float *wdt = wcs + 512;
+    // warp table, entry CW j + e = column 32j + CW kw + e: cs*log2e, cf, dt;
+    // cr[j] = cs_r*log2e (r = last column of chunk j)
+    float *wcs = reinterpret_cast<float *>(sm + OutSmem::WC) + mw * (4 * 8 * CW);
+    float *wcf = wcs + 8 * CW;
+    float *wdt = wcs + 16 * CW;
+    float *wcr = wcs + 24 * CW;
     float *sq_s = reinterpret_cast<float *>(sm + OutSmem::SQ);
-    uint8_t *mbuf = sm + OutSmem::BM;
+    float *d_s = reinterpret_cast<float *>(sm + OutSmem::DH);
+    // G row of this thread: NS bf16 in 16-byte pieces XOR-swizzled by row
+    // (conflict-free); pieces 4j + CP kw + [0, CP) are this warp's slice of chunk j
+    uint8_t *grow = sm + OutSmem::GB + row * (NS * 2);
+    const int gsw = row & 7;
+    auto gpiece = [&](int pc) -> uint4 * {
+      return reinterpret_cast<uint4 *>(grow + ((pc ^ gsw) << 4));
+    };
     const long trow = (long)b * p.T + (valid ? t : 0);
     const bf16 *xrow = act + trow * act_ld;
     const bf16 *zrow = p.z + trow * p.z_ld;
     float ssq = 0.f;
 
-    // per-head column constants for this warp's chunks j = hf, hf+2, .. <= jd
     struct Pref {
-      float cs[4], dt[4], csl;
+      float cs[CL], dt[CL];
+      float cr, csl;
     };
+    // lane -> chunk j = lane/4, columns 32j + CW kw + CL (lane%4) + [0, CL)
+    const int fj = lane >> 2, fcol = 32 * fj + CW * kw + CL * (lane & 3);
     auto fetch = [&](int i, Pref &f) {
       const int h = h0 + i;
       const float *csg = p.cs + ((long)b * p.H + h) * csb + (long)c * TC_L;
       const float *dtg = p.dtT + ((long)b * p.H + h) * csb + (long)c * TC_L;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = hf + 2 * u;
-        if (j <= jd) {
-          f.cs[u] = csg[j * 32 + lane];
-          f.dt[u] = dtg[j * 32 + lane];
-        }
+      if constexpr (CL == 4) {
+        const float4 a = *reinterpret_cast<const float4 *>(csg + fcol);
+        const float4 d = *reinterpret_cast<const float4 *>(dtg + fcol);
+        f.cs[0] = a.x, f.cs[1] = a.y, f.cs[2] = a.z, f.cs[3] = a.w;
+        f.dt[0] = d.x, f.dt[1] = d.y, f.dt[2] = d.z, f.dt[3] = d.w;
+      } else {
+        const float2 a = *reinterpret_cast<const float2 *>(csg + fcol);
+        const float2 d = *reinterpret_cast<const float2 *>(dtg + fcol);
+        f.cs[0] = a.x, f.cs[1] = a.y;
+        f.dt[0] = d.x, f.dt[1] = d.y;
       }
+      f.cr = csg[32 * fj + 31];
       f.csl = csg[l];
     };
-    // write cs*log2e, dt and cf[s] = e^{cs_r - cs_s} dt_s (r = last index of
-    // s's 32-chunk) into the warp's table; returns this row's cs_l * log2e
+    // cf[s] = e^{cs_r - cs_s} dt_s
     auto commit = [&](const Pref &f) -> float {
       __syncwarp();  // every lane is done reading the previous head's table
+      const float vr = f.cr * kLog2e;
+      uint32_t *wcfb = reinterpret_cast<uint32_t *>(wcf);  // cf as bf16 pairs
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = hf + 2 * u;
-        if (j <= jd) {
-          const int s = j * 32 + lane;
-          const float v = f.cs[u] * kLog2e;
-          const float vr = __shfl_sync(0xffffffffu, v, 31);
-          wcs[s] = v;
-          wdt[s] = f.dt[u];
-          wcf[s] = ex2(vr - v) * f.dt[u];
-        }
+      for (int k = 0; k < CL; k += 2) {
+        const float v0 = f.cs[k] * kLog2e, v1 = f.cs[k + 1] * kLog2e;
+        wcs[CL * lane + k] = v0;
+        wcs[CL * lane + k + 1] = v1;
+        wdt[CL * lane + k] = f.dt[k];
+        wdt[CL * lane + k + 1] = f.dt[k + 1];
+        __nv_bfloat162 cf2 = __floats2bfloat162_rn(ex2(vr - v0) * f.dt[k], ex2(vr - v1) * f.dt[k + 1]);
+        wcfb[(CL * lane + k) / 2] = *reinterpret_cast<uint32_t *>(&cf2);
       }
+      if ((lane & 3) == 0) wcr[fj] = vr;
       __syncwarp();
       return f.csl * kLog2e;
     };
-    // M = G * decay * dt into the smem M buffer (K-major, SWIZZLE_128B)
-    auto build_m = [&](float csl) {
-      auto emit = [&](int s0, const uint32_t(&pk)[16]) {
-        uint8_t *blk = mbuf + (s0 >> 6) * 16384;
-        const int ch0 = (s0 & 63) >> 3;
+    auto ld_table = [&](const float *tab, int j, float (&v)[CW]) {
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
-          *reinterpret_cast<uint4 *>(blk + sw128_off(row, ch0 + cc)) =
-              make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
-      };
-      auto off_diag = [&](int s0, const uint32_t(&r)[32], uint32_t(&pk)[16]) {
-        const float rf = ex2(csl - wcs[s0 + 31]);
+      for (int k = 0; k < CW / 4; ++k) {
+        const float4 a = *reinterpret_cast<const float4 *>(tab + CW * j + 4 * k);
+        v[4 * k] = a.x, v[4 * k + 1] = a.y, v[4 * k + 2] = a.z, v[4 * k + 3] = a.w;
+      }
+    };
+    auto ld_g = [&](int j, uint32_t (&gw)[CW / 2]) {
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const float m0 = __uint_as_float(r[e]) * rf * wcf[s0 + e];
-          const float m1 = __uint_as_float(r[e + 1]) * rf * wcf[s0 + e + 1];
+      for (int k = 0; k < CP; ++k) {
+        const uint4 g = *gpiece(4 * j + CP * kw + k);
+        gw[4 * k] = g.x, gw[4 * k + 1] = g.y, gw[4 * k + 2] = g.z, gw[4 * k + 3] = g.w;
+      }
+    };
+    auto st_m = [&](uint32_t taddr, const uint32_t (&pk)[CW / 2], bool on) {
+      if constexpr (CW == 16) sm100::tmem_st8_if(taddr, pk, on);
+      else sm100::tmem_st4_if(taddr, *reinterpret_cast<const uint32_t(*)[4]>(pk), on);
+    };
+    // M = G * decay * dt for this warp's slice of head hh -> TMEM M buffer hh & 1.
+    // The off-diagonal chunks are computed branch-free (NJ is a compile-time
+    // constant per row tile) so their loads and math interleave; chunks at or
+    // past the diagonal are computed but not stored.
+    auto build_m = [&](auto rt, int hh, float csl) {
+      constexpr int NJ = 4 * (decltype(rt)::value + 1);
+      const uint32_t mt = tmem + lane_off + TM_M + (hh & 1) * 128 + (CW / 2) * kw;
+      {  // diagonal chunk: per-element decay, causal mask
+        uint32_t gw[CW / 2], pd[CW / 2];
+        float cs[CW], dt[CW];
+        ld_g(jd, gw);
+        ld_table(wcs, jd, cs);
+        ld_table(wdt, jd, dt);
+        const int s0 = 32 * jd + CW * kw;
+#pragma unroll
+        for (int e = 0; e < CW / 2; ++e) {
+          const int s = s0 + 2 * e;
+          const float g0 = __uint_as_float(gw[e] << 16);
+          const float g1 = __uint_as_float(gw[e] & 0xffff0000u);
+          const float m0 = s <= l ? g0 * ex2(csl - cs[2 * e]) * dt[2 * e] : 0.f;
+          const float m1 = s + 1 <= l ? g1 * ex2(csl - cs[2 * e + 1]) * dt[2 * e + 1] : 0.f;
           __nv_bfloat162 v = __floats2bfloat162_rn(m0, m1);
-          pk[e >> 1] = *reinterpret_cast<uint32_t *>(&v);
+          pd[e] = *reinterpret_cast<uint32_t *>(&v);
         }
-      };
-      int j = hf;
-      for (; j + 2 < jd; j += 4) {  // two off-diagonal chunks, both TMEM loads in flight
-        uint32_t r0[32], r1[32], pk[16];
-        sm100::tmem_ld32(tmem + lane_off + TM_G + j * 32, r0);
-        sm100::tmem_ld32(tmem + lane_off + TM_G + (j + 2) * 32, r1);
-        sm100::tmem_ld_wait();
-        off_diag(j * 32, r0, pk);
-        emit(j * 32, pk);
-        off_diag((j + 2) * 32, r1, pk);
-        emit((j + 2) * 32, pk);
+        st_m(mt + 16 * jd, pd, true);
+#if SSD200_OUT_TRACE
+        if (p.trace && blockIdx.x == 0 && lane == 0 && mw == 0 && hh < 16) p.trace[6144 + hh * 16 + 2] = clk64();
+#endif
       }
-      for (; j <= jd; j += 2) {
-        uint32_t r[32], pk[16];
-        sm100::tmem_ld32(tmem + lane_off + TM_G + j * 32, r);
-        sm100::tmem_ld_wait();
-        const int s0 = j * 32;
-        if (j < jd) {
-          off_diag(s0, r, pk);
-        } else {
+      // off-diagonal chunks: M = (G * cf) * rf on packed bf16 pairs (M is bf16 anyway)
+      const uint32_t *wcfb = reinterpret_cast<const uint32_t *>(wcf);
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const int s = s0 + e;
-            const float m0 = s <= l ? __uint_as_float(r[e]) * ex2(csl - wcs[s]) * wdt[s] : 0.f;
-            const float m1 =
-                s + 1 <= l ? __uint_as_float(r[e + 1]) * ex2(csl - wcs[s + 1]) * wdt[s + 1] : 0.f;
-            __nv_bfloat162 v = __floats2bfloat162_rn(m0, m1);
-            pk[e >> 1] = *reinterpret_cast<uint32_t *>(&v);
-          }
+      for (int j = 0; j < NJ - 1; ++j) {
+        uint32_t gw[CW / 2], cw[CW / 2], pk[CW / 2];
+        ld_g(j, gw);
+#pragma unroll
+        for (int k = 0; k < CW / 8; ++k) {
+          const uint4 a = *reinterpret_cast<const uint4 *>(wcfb + (CW / 2) * j + 4 * k);
+          cw[4 * k] = a.x, cw[4 * k + 1] = a.y, cw[4 * k + 2] = a.z, cw[4 * k + 3] = a.w;
         }
-        emit(s0, pk);
+        const __nv_bfloat162 rf2 = __float2bfloat162_rn(ex2(csl - wcr[j]));
+#pragma unroll
+        for (int e = 0; e < CW / 2; ++e) {
+          const __nv_bfloat162 m = __hmul2(__hmul2(*reinterpret_cast<const __nv_bfloat162 *>(&gw[e]),
+                                                   *reinterpret_cast<const __nv_bfloat162 *>(&cw[e])),
+                                           rf2);
+          pk[e] = *reinterpret_cast<const uint32_t *>(&m);
+        }
+        st_m(mt + 16 * j, pk, j < jd);
+#if SSD200_OUT_TRACE
+        if (p.trace && blockIdx.x == 0 && lane == 0 && mw == 0 && hh < 16) p.trace[6144 + hh * 16 + 3 + j] = clk64();
+#endif
       }
-      for (; j < NS / 32; j += 2) {  // chunks above the diagonal are zero
-        const uint32_t zpk[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-        emit(j * 32, zpk);
+#if SSD200_OUT_TRACE
+      const unsigned long long t_st = clk64();
+#endif
+      sm100::tmem_st_wait();
+#if SSD200_OUT_TRACE
+      if (p.trace && blockIdx.x == 0 && lane == 0 && hh - 1 < 16 && hh >= 1) {
+        p.trace[2048 + (mw * 16 + hh - 1) * 8 + 4] = t_st;
+        p.trace[2048 + (mw * 16 + hh - 1) * 8 + 5] = clk64();
       }
-      sm100::fence_proxy_async();
+#endif
       sm100::tc_fence_before();
-      sm100::mbar_arrive(bar_m);
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&mrdy[hh & 1]);
+    };
+    auto build = [&](int hh, float csl) {
+      if (R) build_m(std::integral_constant<int, 1>{}, hh, csl);
+      else build_m(std::integral_constant<int, 0>{}, hh, csl);
     };
 
     Pref nxt;
     fetch(0, nxt);
     float csl = commit(nxt);
+    if (p.HG > 1) fetch(1, nxt);
+    // ---- G: TMEM f32 -> bf16 smem rows (this warp's column slices)
     sm100::mbar_wait(bar_g, 0);
     sm100::tc_fence_after();
-    build_m(csl);
-    const int pc = hf * 32;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j < nj && j <= jd) {
+        uint32_t r[CW];
+        if constexpr (CW == 16) sm100::tmem_ld16(tmem + lane_off + TM_M + 32 * j + CW * kw, r);
+        else sm100::tmem_ld8(tmem + lane_off + TM_M + 32 * j + CW * kw,
+                             *reinterpret_cast<uint32_t(*)[8]>(r));
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int k = 0; k < CP; ++k) {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(r[8 * k + 2 * e]),
+                                                     __uint_as_float(r[8 * k + 2 * e + 1]));
+            w[e] = *reinterpret_cast<uint32_t *>(&v);
+          }
+          *gpiece(4 * j + CP * kw + k) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+    }
+    for (int k = threadIdx.x - 64; k < p.HG; k += OUT_MATH) d_s[k] = p.D[h0 + k];
+    sm100::tc_fence_before();
+    named_bar(1, OUT_MATH);  // every G column read out of TMEM before M overwrites it
+    sm100::tc_fence_after();
+    {  // chunks above the diagonal are zero in both M buffers for every head
+      const uint32_t zero[CW / 2] = {};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const bool on = j < nj && j > jd;
+        st_m(tmem + lane_off + TM_M + 16 * j + (CW / 2) * kw, zero, on);
+        st_m(tmem + lane_off + TM_M + 128 + 16 * j + (CW / 2) * kw, zero, on);
+      }
+    }
+    build(0, csl);
+    constexpr int EW = OUT_EW;  // epilogue columns per warp
+    const int pc = kw * EW;
     for (int i = 0; i < p.HG; ++i) {
       const int buf = i & 1, h = h0 + i;
-      if (i + 1 < p.HG) fetch(i + 1, nxt);  // global loads in flight during the wait
-      uint4 xv[4], zv[4];                    // x (D skip) and z (gate) rows of head i
+      uint4 xv[EW / 8], zv[EW / 8];  // x (D skip) and z (gate) of head i, columns [pc, pc+EW)
       const uint4 *xg = reinterpret_cast<const uint4 *>(xrow + h * TC_P + pc);
       const uint4 *zg = reinterpret_cast<const uint4 *>(zrow + h * TC_P + pc);
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
+      for (int cc = 0; cc < EW / 8; ++cc) {
         xv[cc] = xg[cc];
         zv[cc] = zg[cc];
       }
       const float el = ex2(csl);
-      const float Dh = p.D[h];
-      sm100::mbar_wait(&bar_y[buf], (i >> 1) & 1);  // MMA(i) done: M buffer free
-      sm100::tc_fence_after();
-      if (i + 1 < p.HG) {
+      const float Dh = d_s[i];
+#if SSD200_OUT_TRACE
+      unsigned long long *tw = (p.trace && blockIdx.x == 0 && lane == 0 && i < 16)
+                                   ? p.trace + 2048 + (mw * 16 + i) * 8
+                                   : nullptr;
+      if (tw) tw[0] = clk64();
+#endif
+      if (i + 1 < p.HG) {  // M_{i+1} into the other buffer while the tensor core runs head i
         csl = commit(nxt);
-        build_m(csl);                                 // tensor core starts head i+1
+#if SSD200_OUT_TRACE
+        if (p.trace && blockIdx.x == 0 && lane == 0 && mw == 0 && i + 1 < 16) p.trace[6144 + (i + 1) * 16 + 0] = clk64();
+#endif
+        if (i + 2 < p.HG) fetch(i + 2, nxt);
+#if SSD200_OUT_TRACE
+        if (p.trace && blockIdx.x == 0 && lane == 0 && mw == 0 && i + 1 < 16) p.trace[6144 + (i + 1) * 16 + 1] = clk64();
+#endif
+        build(i + 1, csl);
       }
-      // ---- epilogue(i) on columns p in [32 hf, 32 hf + 32), overlapping MMA(i+1)
+#if SSD200_OUT_TRACE
+      if (tw) tw[1] = clk64();
+#endif
+      sm100::mbar_wait(&bar_y[buf], (i >> 1) & 1);  // MMA(i) done
+#if SSD200_OUT_TRACE
+      if (tw) tw[2] = clk64();
+#endif
+      sm100::tc_fence_after();
+      // ---- epilogue(i) on columns [pc, pc+EW) in 16-column steps, overlapping MMA(i+1)
       const uint32_t ydt = tmem + lane_off + TM_Y + buf * 128 + pc;
-      uint32_t yd[32], yo[32];
-      sm100::tmem_ld32(ydt, yd);
-      sm100::tmem_ld32(ydt + 64, yo);
-      sm100::tmem_ld_wait();
-      sm100::tc_fence_before();
-      sm100::mbar_arrive(&yfree[buf]);
+      uint32_t *urow =
+          reinterpret_cast<uint32_t *>(p.u_out + ((long)b * p.T + t) * p.d_inner + h * TC_P + pc);
       const __nv_bfloat162 *xe = reinterpret_cast<const __nv_bfloat162 *>(xv);
       const __nv_bfloat162 *ze = reinterpret_cast<const __nv_bfloat162 *>(zv);
-      uint32_t out[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float2 xf = __bfloat1622float2(xe[j]);
-        const float2 zf = __bfloat1622float2(ze[j]);
-        const float y0 = __uint_as_float(yd[2 * j]) + el * __uint_as_float(yo[2 * j]) + Dh * xf.x;
-        const float y1 =
-            __uint_as_float(yd[2 * j + 1]) + el * __uint_as_float(yo[2 * j + 1]) + Dh * xf.y;
-        const float u0 = y0 * silu_fast(zf.x), u1 = y1 * silu_fast(zf.y);
-        ssq += u0 * u0 + u1 * u1;
-        __nv_bfloat162 v = __floats2bfloat162_rn(u0, u1);
-        out[j] = *reinterpret_cast<uint32_t *>(&v);
-      }
-      if (valid) {
-        bf16 *urow = p.u_out + ((long)b * p.T + t) * p.d_inner + h * TC_P + pc;
+      for (int hs = 0; hs < EW / 16; ++hs) {
+        uint32_t yd[16], yo[16];
+        sm100::tmem_ld16(ydt + 16 * hs, yd);
+        sm100::tmem_ld16(ydt + 64 + 16 * hs, yo);
+        sm100::tmem_ld_wait();
+        if (hs == EW / 16 - 1) {
+          sm100::tc_fence_before();
+          sm100::mbar_arrive(&yfree[buf]);
+        }
+        uint32_t out[8];
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
-          *reinterpret_cast<uint4 *>(urow + cc * 8) =
-              make_uint4(out[4 * cc], out[4 * cc + 1], out[4 * cc + 2], out[4 * cc + 3]);
+        for (int j = 0; j < 8; ++j) {
+          const float2 xf = __bfloat1622float2(xe[8 * hs + j]);
+          const float2 zf = __bfloat1622float2(ze[8 * hs + j]);
+          const float y0 = __uint_as_float(yd[2 * j]) + el * __uint_as_float(yo[2 * j]) + Dh * xf.x;
+          const float y1 =
+              __uint_as_float(yd[2 * j + 1]) + el * __uint_as_float(yo[2 * j + 1]) + Dh * xf.y;
+          const float u0 = y0 * silu_tanh(zf.x), u1 = y1 * silu_tanh(zf.y);
+          ssq += u0 * u0 + u1 * u1;
+          __nv_bfloat162 v = __floats2bfloat162_rn(u0, u1);
+          out[j] = *reinterpret_cast<uint32_t *>(&v);
+        }
+        if (valid) {
+          uint4 *u4 = reinterpret_cast<uint4 *>(urow + 8 * hs);
+          u4[0] = make_uint4(out[0], out[1], out[2], out[3]);
+          u4[1] = make_uint4(out[4], out[5], out[6], out[7]);
+        }
       }
+#if SSD200_OUT_TRACE
+      if (tw) tw[3] = clk64();
+#endif
     }
-    if (hf == 1) sq_s[row] = ssq;
+    if (kw > 0) sq_s[(kw - 1) * 128 + row] = ssq;
     named_bar(1, OUT_MATH);
-    if (hf == 0 && valid) p.ssq[((long)b * p.T + t) * p.NG + g] = ssq + sq_s[row];
+    if (kw == 0 && valid) {
+      float s = ssq;
+#pragma unroll
+      for (int k = 1; k < OUT_KW; ++k) s += sq_s[(k - 1) * 128 + row];
+      p.ssq[((long)b * p.T + t) * p.NG + g] = s;
+    }
   }
   __syncthreads();
   if (warp == 1) {
