@@ -1208,7 +1208,7 @@ static int mega_bt(int B) { return B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8; }
 
 static int mega_stages(const ssd200_dims_t *d, int B, size_t *smem) {
   const size_t xb = (size_t)mega_bt(B) * (d->d_inner > d->d_model ? d->d_inner : d->d_model) * 2;
-  const size_t cap = 220 * 1024;
+  const size_t cap = 216 * 1024;  // + ~8 KB of static smem stays under the 227 KB CTA limit
   int S = 3;
   while (S > 2 && (size_t)S * MEGA_STAGE + xb > cap) --S;
   *smem = (size_t)S * MEGA_STAGE + xb;
@@ -1230,7 +1230,7 @@ static size_t mega_carve(const ssd200_dims_t *d, int B, void *ws, MegaArgs *a) {
     a->act = act;
     a->dt = dt;
     a->u = u;
-    a->usq = usq;
+    a->upart = usq;  // (grid, B) <= (B, d_inner) floats
     a->amax_val = pv;
     a->amax_idx = pi;
   }
@@ -1262,16 +1262,19 @@ int ssd200_decode_step(const ssd200_dims_t *d, const ssd200_layer_t *layers_dev,
   const size_t need = mega_carve(d, batch, nullptr, nullptr);
   REQUIRE(workspace_bytes >= need, SSD200_EWORKSPACE, "decode_step workspace %zu < %zu",
           workspace_bytes, need);
+  REQUIRE(num_sms() <= d->d_inner && (d->d_inner + num_sms() - 1) / num_sms() <= MEGA_MAX_NK &&
+              (d->d_inner + num_sms() - 1) / num_sms() / d->head_dim + 2 <= MEGA_MAX_DT,
+          SSD200_EUNSUPPORTED, "decode_step: d_inner / head_dim outside the fused step's split");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   mega_embed<<<batch, 256, 0, st>>>(tokens, (const bf16 *)embedding, d->d_model, (float *)hidden,
                                     (bf16 *)hidden_lp, barrier_state);
   LAUNCH_CHECK("mega_embed");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(decode_mega<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(decode_mega<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(decode_mega<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(decode_mega<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(decode_mega<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
+    cudaFuncSetAttribute(decode_mega<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
+    cudaFuncSetAttribute(decode_mega<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
+    cudaFuncSetAttribute(decode_mega<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
     attr = true;
   }
   Widths w = widths(d);
@@ -1304,7 +1307,7 @@ int ssd200_decode_step(const ssd200_dims_t *d, const ssd200_layer_t *layers_dev,
   a.logits = (float *)logits;
   a.argmax_out = argmax_out;
   a.bar_count = barrier_state;
-  a.bar_epoch = barrier_state + 1;
+  a.bc_flag = barrier_state + 1;
   a.trace = static_cast<unsigned long long *>(g_mega_trace);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(num_sms());

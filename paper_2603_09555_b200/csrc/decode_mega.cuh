@@ -2,16 +2,26 @@
 // kernel runs the whole token step — every layer's in_proj / SSM update /
 // out_proj and the tied head — decode.py:77-144.
 //
-// One CTA per SM.  Warp 8 is a producer that streams, in order, this CTA's
-// row groups of every weight matrix the step touches (W_in[0], W_out[0],
-// W_in[1], ..., E) with cp.async.bulk into a 3-deep 64 KB smem ring.  The
+// One CTA per SM.  The last warp is a producer that streams, in order, this
+// CTA's weight rows of every matrix the step touches (W_in[0], W_out[0],
+// W_in[1], ..., E) with cp.async.bulk into a 64 KB-stage smem ring.  The
 // weights never depend on activations, so the producer runs ahead across the
-// grid barriers and HBM stays busy while the consumers synchronise.
-// Warps 0..7 consume: phases separated by a sense-reversing grid barrier
-//   P1  u = h_lp . W_in^T + conv window / SiLU / dt epilogue   (per row group)
-//   P2  SSM state update + y + D skip + gate, sum u^2          (per (b, h, row split))
-//   P3  hidden += rstd * (u . W_out'^T), bf16 shadow           (per row group)
-//   H   logits = rmsnorm(hidden) . E^T, argmax partials; last barrier; pick.
+// synchronisation points and HBM stays busy while the consumers wait.
+//
+// Work split per layer (16 consumer warps):
+//   A  each CTA owns a contiguous range of d_inner channels [k0, k1): it
+//      computes the in_proj rows of its own z and x channels and of the dt of
+//      the heads they touch, plus a 1/grid share of the B / C rows (streamed
+//      first).  B / C go through the conv and are published to global memory
+//      with a release-counter (no grid barrier); z, x (post conv) and dt stay
+//      in shared memory.  Once every B / C row is published, the CTA runs the
+//      SSM update of its own channels (h <- e^{a dt} h + dt x B, y = C.h + D x,
+//      u = y silu(z)) with purely local inputs and writes u + its sum u^2.
+//   -- grid barrier --
+//   B  hidden += rstd * (u . W_out'^T), bf16 shadow (rows of d_model split over
+//      CTAs).
+//   -- grid barrier --
+//   H  logits = rmsnorm(hidden) . E^T, argmax partials; last barrier; pick.
 #pragma once
 
 #include "common.cuh"
@@ -24,6 +34,8 @@ constexpr int MEGA_CT = MEGA_CW * 32;          // consumer threads
 constexpr int MEGA_THREADS = MEGA_CT + 32;     // + one producer warp
 constexpr uint32_t MEGA_STAGE = 64 * 1024;
 constexpr int MEGA_STAGES = 3;  // ring capacity; `stages` (2 or 3) is used
+constexpr int MEGA_MAX_NK = 64;   // own d_inner channels per CTA
+constexpr int MEGA_MAX_DT = 16;   // heads touched by one CTA's channels
 
 struct MegaArgs {
   int B, L, V, stages;
@@ -38,12 +50,13 @@ struct MegaArgs {
   float *conv;       // (L, B, conv_dim, k-1) in place
   float *z, *act, *dt;  // scratch (B, d_inner) / (B, conv_dim) / (B, H)
   bf16 *u;           // (B, d_inner)
-  float *usq;        // (B, d_inner) u^2 per element (summed by the out_proj prologue)
+  float *upart;      // (grid, B) per-CTA partial sums of u^2 of the current layer
   float *logits;     // (B, V) or null
   float *amax_val;   // (grid, B)
   int *amax_idx;
   int64_t *argmax_out;  // (B) or null
-  unsigned *bar_count, *bar_epoch;
+  unsigned *bar_count;
+  unsigned *bc_flag;  // B / C rows published so far this step (release counter)
   unsigned long long *trace;  // debug: per-phase %globaltimer stamps of CTA 0 (or null)
 };
 
@@ -65,11 +78,19 @@ __device__ __forceinline__ void mega_grid_sync(const MegaArgs &a, unsigned &inde
   named_barrier_sync(1, MEGA_CT);
   if (threadIdx.x == 0) {
     const unsigned target = (++index) * gridDim.x;
+    if (a.trace && index == 4) a.trace[5400 + blockIdx.x] = gtimer();
+#ifdef MEGA_DIAG_NOFENCE
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar_count) : "memory");
+#else
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar_count) : "memory");
+#endif
+    // relaxed polling (no per-iteration fence), one acquire fence once it flips
     unsigned cur;
     do {
-      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(a.bar_count) : "memory");
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(a.bar_count) : "memory");
     } while (cur < target);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    if (a.trace && index == 4) a.trace[5600 + blockIdx.x] = gtimer();
   }
   named_barrier_sync(1, MEGA_CT);
 }
@@ -78,7 +99,7 @@ __device__ __forceinline__ void mega_grid_sync(const MegaArgs &a, unsigned &inde
 __global__ void mega_embed(const int64_t *__restrict__ tok, const bf16 *__restrict__ E,
                            int d_model, float *__restrict__ hid, bf16 *__restrict__ hid_lp,
                            unsigned *bar_count) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) *bar_count = 0u;
+  if (blockIdx.x == 0 && threadIdx.x < 2) bar_count[threadIdx.x] = 0u;  // barrier + B/C flag
   const int r = blockIdx.x;
   const bf16 *src = E + (size_t)tok[r] * d_model;
   for (int c = threadIdx.x; c < d_model; c += blockDim.x) {
@@ -88,31 +109,32 @@ __global__ void mega_embed(const int64_t *__restrict__ tok, const bf16 *__restri
   }
 }
 
-__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-// L2 prefetch of a large contiguous range in <= 1 MB pieces (16-byte granular)
-__device__ __forceinline__ void prefetch_range(const void *p, size_t bytes) {
-  const char *c = static_cast<const char *>(p);
-  const uintptr_t a0 = reinterpret_cast<uintptr_t>(c) & ~(uintptr_t)15;
-  size_t n = (bytes + (reinterpret_cast<uintptr_t>(c) - a0) + 15) & ~(size_t)15;
-  const char *q = reinterpret_cast<const char *>(a0);
-  while (n) {
-    const uint32_t chunk = n > (1u << 20) ? (1u << 20) : (uint32_t)n;
-    prefetch_l2(q, chunk);
-    q += chunk;
-    n -= chunk;
-  }
-}
-
-// this CTA's share [g0, g1) of `groups` row groups
-__device__ __forceinline__ void mega_share(int groups, int &g0, int &g1) {
-  g0 = (int)((long)groups * blockIdx.x / gridDim.x);
-  g1 = (int)((long)groups * (blockIdx.x + 1) / gridDim.x);
-}
-
 // rows per 64 KB stage for reduction length K (bf16)
 __device__ __forceinline__ int mega_rows(int K) { return (int)(MEGA_STAGE / (K * 2)); }
+
+// This CTA's in_proj rows for one layer, in stream order: its share of the
+// B / C rows first (other CTAs wait for them), then the dt rows of the heads
+// its channels touch, then its z rows and x rows.
+struct MegaOwn {
+  int nbc, bc0, ndt, h_lo, nk, k0;
+  __device__ MegaOwn(const MegaArgs &a) {
+    const int gn2 = 2 * a.G * a.N;
+    bc0 = (int)((long)gn2 * blockIdx.x / gridDim.x);
+    nbc = (int)((long)gn2 * (blockIdx.x + 1) / gridDim.x) - bc0;
+    k0 = (int)((long)a.d_inner * blockIdx.x / gridDim.x);
+    nk = (int)((long)a.d_inner * (blockIdx.x + 1) / gridDim.x) - k0;
+    h_lo = k0 / a.P;
+    ndt = nk ? (k0 + nk - 1) / a.P - h_lo + 1 : 0;
+  }
+  __device__ int count() const { return nbc + ndt + 2 * nk; }
+  __device__ int row(int i, const MegaArgs &a) const {
+    if (i < nbc) return 2 * a.d_inner + bc0 + i;
+    i -= nbc;
+    if (i < ndt) return 2 * a.d_inner + 2 * a.G * a.N + h_lo + i;
+    i -= ndt;
+    return i < nk ? k0 + i : a.d_inner + k0 + (i - nk);
+  }
+};
 
 // BT: batch rows computed (a.B rounded up to 1, 2, 4 or 8; extra rows are zero)
 template <int BT>
@@ -122,11 +144,17 @@ __global__ void __launch_bounds__(MEGA_THREADS, 1) decode_mega(MegaArgs a) {
   __shared__ float s_scale[DEC_MAX_B];
   __shared__ float s_best[MEGA_CW][DEC_MAX_B];
   __shared__ int s_bidx[MEGA_CW][DEC_MAX_B];
+  __shared__ float s_z[DEC_MAX_B][MEGA_MAX_NK];  // own channels: gate z
+  __shared__ float s_x[DEC_MAX_B][MEGA_MAX_NK];  // own channels: x after conv + SiLU
+  __shared__ float s_dt[DEC_MAX_B][MEGA_MAX_DT];
+  __shared__ float s_uu[DEC_MAX_B][MEGA_MAX_NK];  // own channels: u^2
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int B = a.B;
   uint8_t *ring = msm;
   const int S = a.stages;
   bf16 *xs = reinterpret_cast<bf16 *>(msm + (size_t)S * MEGA_STAGE);  // (B, K<=d_inner)
+  const MegaOwn own(a);
+  const int gn = a.G * a.N;
   if (threadIdx.x == 0) {
     for (int s = 0; s < MEGA_STAGES; ++s) {
       mbar_init_s(&full[s], 1);
@@ -138,72 +166,57 @@ __global__ void __launch_bounds__(MEGA_THREADS, 1) decode_mega(MegaArgs a) {
 
   if (warp == MEGA_CW) {
     // ------------------------------------------------ producer: the weight stream
+    // Segment j of the step: 2l = this CTA's W_in rows of layer l, 2l+1 = its
+    // W_out share, 2L = its share of E; rows are bulk-copied into the ring.
+    // (L2 prefetching ahead of the ring was measured to slow the step down:
+    // it competes with the copies and lengthens every synchronisation.)
     if (lane == 0) {
-      int s = 0;
+      int s = 0, pstage = 0;
       uint32_t ph = 0;
-      auto stream = [&](const bf16 *W, int N, int K) {
-        const int rows = mega_rows(K);
-        const int groups = (N + rows - 1) / rows;
-        int g0, g1;
-        mega_share(groups, g0, g1);
-        for (int gi = g0; gi < g1; ++gi) {
-          const int r0 = gi * rows, nr = min(rows, N - r0);
+      const int nseg = 2 * a.L + 1;
+      auto share = [&](int N, int &r0, int &nr) {  // this CTA's contiguous share of N rows
+        r0 = (int)((long)N * blockIdx.x / gridDim.x);
+        nr = (int)((long)N * (blockIdx.x + 1) / gridDim.x) - r0;
+      };
+      int r0_out, nr_out, r0_e, nr_e;
+      share(a.d_model, r0_out, nr_out);
+      share(a.V, r0_e, nr_e);
+      auto seg_w = [&](int j) -> const bf16 * {
+        return j == 2 * a.L ? a.E
+                            : static_cast<const bf16 *>((j & 1) ? a.layers[j >> 1].W_out
+                                                                : a.layers[j >> 1].W_in);
+      };
+      auto seg_k = [&](int j) { return (j < 2 * a.L && (j & 1)) ? a.d_inner : a.d_model; };
+      auto seg_n = [&](int j) { return j == 2 * a.L ? nr_e : (j & 1) ? nr_out : own.count(); };
+      auto seg_row = [&](int j, int i) {
+        return j == 2 * a.L ? r0_e + i : (j & 1) ? r0_out + i : own.row(i, a);
+      };
+      for (int j = 0; j < nseg; ++j) {
+        const bf16 *W = seg_w(j);
+        const int K = seg_k(j), nrows = seg_n(j), per = mega_rows(K);
+        for (int i0 = 0; i0 < nrows; i0 += per) {
+          const int nr = min(per, nrows - i0);
           mbar_wait_s(&empty[s], ph ^ 1);
+          if (a.trace && blockIdx.x == 0 && pstage < 512) a.trace[6000 + pstage] = gtimer();
+          ++pstage;
           mbar_expect_s(&full[s], (uint32_t)nr * K * 2);
           for (int r = 0; r < nr; ++r)
-            bulk_g2s(ring + (size_t)s * MEGA_STAGE + (size_t)r * K * 2, W + (size_t)(r0 + r) * K,
-                     (uint32_t)K * 2, &full[s]);
+            bulk_g2s(ring + (size_t)s * MEGA_STAGE + (size_t)r * K * 2,
+                     W + (size_t)seg_row(j, i0 + r) * K, (uint32_t)K * 2, &full[s]);
           if (++s == S) {
             s = 0;
             ph ^= 1;
           }
         }
-      };
-      // L2 prefetch of this CTA's share of one layer (weights + SSM state rows):
-      // HBM keeps streaming one layer ahead of the smem ring, whatever the
-      // consumers are waiting on.
-      auto share_bytes = [&](int N, int K, size_t &off, size_t &len) {
-        const int rows = mega_rows(K);
-        const int groups = (N + rows - 1) / rows;
-        int g0, g1;
-        mega_share(groups, g0, g1);
-        const int r0 = g0 * rows, r1 = min(N, g1 * rows);
-        off = (size_t)r0 * K * 2;
-        len = r1 > r0 ? (size_t)(r1 - r0) * K * 2 : 0;
-      };
-      auto prefetch_layer = [&](int l) {
-        size_t off, len;
-        share_bytes(a.d_in_proj, a.d_model, off, len);
-        if (len) prefetch_range(static_cast<const char *>(a.layers[l].W_in) + off, len);
-        share_bytes(a.d_model, a.d_inner, off, len);
-        if (len) prefetch_range(static_cast<const char *>(a.layers[l].W_out) + off, len);
-        const long rows_tot = (long)a.B * a.H * a.P;
-        const long q0 = rows_tot * blockIdx.x / gridDim.x, q1 = rows_tot * (blockIdx.x + 1) / gridDim.x;
-        if (q1 > q0)
-          prefetch_range(a.ssm + ((size_t)l * rows_tot + q0) * a.N, (size_t)(q1 - q0) * a.N * 4);
-      };
-      prefetch_layer(0);
-      for (int l = 0; l < a.L; ++l) {
-        if (l + 1 < a.L) prefetch_layer(l + 1);
-        stream(static_cast<const bf16 *>(a.layers[l].W_in), a.d_in_proj, a.d_model);
-        if (a.trace && blockIdx.x == 0) a.trace[4096 + 2 * l] = gtimer();
-        stream(static_cast<const bf16 *>(a.layers[l].W_out), a.d_model, a.d_inner);
-        if (a.trace && blockIdx.x == 0) a.trace[4096 + 2 * l + 1] = gtimer();
+        if (a.trace && blockIdx.x == 0) a.trace[4096 + j] = gtimer();
       }
-      {
-        size_t off, len;
-        share_bytes(a.V, a.d_model, off, len);  // the tied head's share of E
-        if (len) prefetch_range(reinterpret_cast<const char *>(a.E) + off, len);
-      }
-      stream(a.E, a.V, a.d_model);
-      if (a.trace && blockIdx.x == 0) a.trace[4096 + 2 * a.L] = gtimer();
     }
     return;
   }
 
-  // ------------------------------------------------ consumers (warps 0..7)
+  // ------------------------------------------------ consumers (warps 0..MEGA_CW-1)
   unsigned bar_idx = 0;
-  int s = 0;
+  int s = 0, cstage = 0;
   uint32_t ph = 0;
   float best[DEC_MAX_B];
   int bidx[DEC_MAX_B];
@@ -212,24 +225,24 @@ __global__ void __launch_bounds__(MEGA_THREADS, 1) decode_mega(MegaArgs a) {
     best[b] = -INFINITY;
     bidx[b] = 0x7fffffff;
   }
-  // one GEMV phase over this CTA's row groups; epi(n, b, v) per (row, batch)
-  auto gemv = [&](int N, int K, auto &&pre, auto &&epi) {
-    const int rows = mega_rows(K);
-    const int groups = (N + rows - 1) / rows;
+  // one GEMV over a row list of nrows rows (row i -> matrix row rowf(i));
+  // pre(n, ok) prefetches epilogue inputs, epi(n, b, v, e) per (row, batch row)
+  auto gemv = [&](int K, int nrows, auto &&rowf, auto &&pre, auto &&epi, auto &&post) {
+    const int per = mega_rows(K);
     const int kchunks = K / 256;
-    int g0, g1;
-    mega_share(groups, g0, g1);
-    for (int gi = g0; gi < g1; ++gi) {
+    for (int i0 = 0; i0 < nrows; i0 += per) {
       const uint8_t *stage = ring + (size_t)s * MEGA_STAGE;
-      const int nrows = min(rows, N - gi * rows);
+      const int nr = min(per, nrows - i0);
       bool waited = false;
-      for (int rr = warp; rr < rows; rr += MEGA_CW) {
-        const int n = gi * rows + rr;
-        const bool ok = rr < nrows;
+      for (int rr = warp; rr < per; rr += MEGA_CW) {
+        const bool ok = rr < nr;
+        const int n = ok ? rowf(i0 + rr) : 0;
         auto e = pre(n, ok);
         if (!waited) {
           mbar_wait_s(&full[s], ph);
           waited = true;
+          if (a.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && cstage < 512)
+            a.trace[6600 + cstage] = gtimer();
         }
         if (ok) {
           // 4 chunks of loads in flight, 4 independent accumulators per batch row
@@ -261,9 +274,11 @@ __global__ void __launch_bounds__(MEGA_THREADS, 1) decode_mega(MegaArgs a) {
             if (lane == b) v = t;
           }
           if (lane < B) epi(n, lane, v, e);
+          post(n);
         }
       }
       if (!waited) mbar_wait_s(&full[s], ph);
+      ++cstage;
       __syncwarp();
       if (lane == 0) mbar_arrive_s(&empty[s]);
       if (++s == S) {
@@ -272,9 +287,11 @@ __global__ void __launch_bounds__(MEGA_THREADS, 1) decode_mega(MegaArgs a) {
       }
     }
   };
-  struct NoPre {
+  struct Pre {
     float old, w0, w1, w2, w3, c0, c1, c2, bias;
   };
+  auto no_post = [](int) {};
+  const int gn2 = 2 * gn;
 
   for (int l = 0; l < a.L; ++l) {
     const ssd200_layer_t lw = a.layers[l];
@@ -282,7 +299,7 @@ __global__ void __launch_bounds__(MEGA_THREADS, 1) decode_mega(MegaArgs a) {
     const float *conv_b = static_cast<const float *>(lw.conv_b);
     const float *dt_bias = static_cast<const float *>(lw.dt_bias);
     float *conv = a.conv + (size_t)l * B * a.conv_dim * (a.k - 1);
-    // ---------------- P1: in_proj + conv / dt epilogue
+    // ---------------- A: this CTA's in_proj rows + conv / dt epilogue
     MEGA_TRACE(l * 8 + 0);
     {
       const uint4 *src = reinterpret_cast<const uint4 *>(a.hidden_lp);
@@ -292,9 +309,9 @@ __global__ void __launch_bounds__(MEGA_THREADS, 1) decode_mega(MegaArgs a) {
       named_barrier_sync(1, MEGA_CT);
       MEGA_TRACE(l * 8 + 1);
       gemv(
-          a.d_in_proj, a.d_model,
+          a.d_model, own.count(), [&](int i) { return own.row(i, a); },
           [&](int n, bool ok) {
-            NoPre e{};
+            Pre e{};
             if (ok && lane < B && a.k == 4 && n >= a.d_inner && n < a.d_inner + a.conv_dim) {
               const int ch = n - a.d_inner;
               const float *ci = conv + ((size_t)lane * a.conv_dim + ch) * 3;
@@ -309,15 +326,16 @@ __global__ void __launch_bounds__(MEGA_THREADS, 1) decode_mega(MegaArgs a) {
             }
             return e;
           },
-          [&](int n, int b, float v, const NoPre &e) {
+          [&](int n, int b, float v, const Pre &e) {
             if (n < a.d_inner) {
-              a.z[(size_t)b * a.d_inner + n] = v;
+              s_z[b][n - own.k0] = v;
             } else if (n < a.d_inner + a.conv_dim) {
               const int ch = n - a.d_inner, km = a.k - 1;
               float *co = conv + ((size_t)b * a.conv_dim + ch) * km;
+              float act;
               if (a.k == 4) {  // taps oldest first (numerics.py:187-188)
                 const float t = e.c0 * e.w0 + e.c1 * e.w1 + e.c2 * e.w2 + v * e.w3;
-                a.act[(size_t)b * a.conv_dim + ch] = silu(t + e.bias);
+                act = silu(t + e.bias);
                 co[0] = e.c1;
                 co[1] = e.c2;
                 co[2] = v;
@@ -327,107 +345,136 @@ __global__ void __launch_bounds__(MEGA_THREADS, 1) decode_mega(MegaArgs a) {
                 win[km] = v;
                 float t = 0.f;
                 for (int j = 0; j <= km; ++j) t += win[j] * conv_w[(size_t)ch * a.k + j];
-                a.act[(size_t)b * a.conv_dim + ch] = silu(t + conv_b[ch]);
+                act = silu(t + conv_b[ch]);
                 for (int j = 0; j < km; ++j) co[j] = win[j + 1];
               }
+              if (ch < a.d_inner)
+                s_x[b][ch - own.k0] = act;
+              else
+                a.act[(size_t)b * a.conv_dim + ch] = act;  // B / C: read by every CTA
             } else {
               const int h = n - a.d_inner - a.conv_dim;
-              a.dt[(size_t)b * a.H + h] = clamp_(softplus(v + dt_bias[h]), a.dt_lo, a.dt_hi);
+              s_dt[b][h - own.h_lo] = clamp_(softplus(v + dt_bias[h]), a.dt_lo, a.dt_hi);
+            }
+          },
+          [&](int n) {
+            if (n >= 2 * a.d_inner && n < a.d_inner + a.conv_dim) {  // publish a B / C row
+              __syncwarp();
+              if (lane == 0)
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bc_flag) : "memory");
             }
           });
     }
     MEGA_TRACE(l * 8 + 2);
-    if (a.trace && l == 1 && threadIdx.x == 0) a.trace[5000 + blockIdx.x] = gtimer();
-    mega_grid_sync(a, bar_idx);
-    if (a.trace && l == 1 && threadIdx.x == 0) a.trace[5200 + blockIdx.x] = gtimer();
+    // ---------------- SSM update of this CTA's channels (every B / C row published)
+    if (threadIdx.x == 0) {
+      const unsigned target = (unsigned)(l + 1) * gn2;
+      unsigned cur;
+      do {
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(a.bc_flag) : "memory");
+      } while (cur < target);
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    named_barrier_sync(1, MEGA_CT);
     MEGA_TRACE(l * 8 + 3);
-    // ---------------- P2: SSM step + D skip + gate, one warp per (b, h, p) row
     {
       const float *A = static_cast<const float *>(lw.a);
       const float *Dv = static_cast<const float *>(lw.D);
-      float *ssm = a.ssm + (size_t)l * B * a.H * a.P * a.N;
-      // stage B / C of every (batch row, group): G * N <= 256 floats each
-      float *sbc = reinterpret_cast<float *>(xs);  // (B, 2, G*N)
-      const int gn = a.G * a.N;
-      for (int i = threadIdx.x; i < B * 2 * gn; i += MEGA_CT) {
-        const int b = i / (2 * gn), j = i % (2 * gn);
-        sbc[i] = a.act[(size_t)b * a.conv_dim + a.d_inner + j];
+      float *sbc = reinterpret_cast<float *>(xs);  // (B, 2, G*N) from L2 (written by other CTAs)
+      for (int i = threadIdx.x; i < B * gn2; i += MEGA_CT) {
+        const int b = i / gn2, j = i % gn2;
+        sbc[i] = __ldcg(&a.act[(size_t)b * a.conv_dim + a.d_inner + j]);
       }
       named_barrier_sync(1, MEGA_CT);
-      const int total = B * a.H * a.P;
       const int hpg = a.H / a.G;
-      // contiguous rows per CTA (their state was L2-prefetched by the producer)
-      const int q0 = (int)((long)total * blockIdx.x / gridDim.x);
-      const int q1 = (int)((long)total * (blockIdx.x + 1) / gridDim.x);
-      for (int r = q0 + warp; r < q1; r += MEGA_CW) {
-        const int b = r / (a.H * a.P);
-        const int hp = r % (a.H * a.P);
-        const int h = hp / a.P, pp = hp % a.P;
-        const int g = h / hpg;
-        const float *bs = sbc + (size_t)b * 2 * gn + g * a.N;
-        const float *cs = sbc + (size_t)b * 2 * gn + gn + g * a.N;
-        const float dt = a.dt[(size_t)b * a.H + h];
-        const float xv = a.act[(size_t)b * a.conv_dim + h * a.P + pp];
-        const float zv = a.z[(size_t)b * a.d_inner + h * a.P + pp];
-        const float decay = expf(A[h] * dt);  // decode.py:126-129
-        const float dx = dt * xv;
-        float4 *st = reinterpret_cast<float4 *>(ssm + ((((size_t)b * a.H + h) * a.P) + pp) * a.N);
-        float acc = 0.f;
-        for (int n4 = lane; n4 < a.N / 4; n4 += 32) {
-          float4 hv = st[n4];
-          const int n = n4 * 4;
-          hv.x = decay * hv.x + dx * bs[n];
-          hv.y = decay * hv.y + dx * bs[n + 1];
-          hv.z = decay * hv.z + dx * bs[n + 2];
-          hv.w = decay * hv.w + dx * bs[n + 3];
-          st[n4] = hv;
-          acc = fmaf(cs[n], hv.x, acc);
-          acc = fmaf(cs[n + 1], hv.y, acc);
-          acc = fmaf(cs[n + 2], hv.z, acc);
-          acc = fmaf(cs[n + 3], hv.w, acc);
+      const int hl = lane & 15, half = lane >> 4;
+      const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
+      const int rows = B * own.nk;
+      float *ssm_l = a.ssm + (size_t)l * B * a.d_inner * a.N;
+      for (int r0 = 2 * warp; r0 < rows; r0 += 2 * MEGA_CW) {
+        const int r = r0 + half;
+        if (r < rows) {
+          const int b = r / own.nk, kk = r % own.nk, k = own.k0 + kk;
+          const int h = k / a.P;
+          const int g = h / hpg;
+          const float *bs = sbc + (size_t)b * gn2 + g * a.N;
+          const float *cs = sbc + (size_t)b * gn2 + gn + g * a.N;
+          const float dt = s_dt[b][h - own.h_lo];
+          const float xv = s_x[b][kk], zv = s_z[b][kk];
+          const float Ah = A[h], Dh = Dv[h];
+          float4 *st = reinterpret_cast<float4 *>(ssm_l + ((size_t)b * a.d_inner + k) * a.N);
+          float4 hv[4];
+          const int nq = a.N / 64;  // float4 per lane (N <= 256)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < nq) hv[q] = st[hl + 16 * q];
+          const float decay = expf(Ah * dt);  // decode.py:126-129
+          const float dx = dt * xv;
+          float acc = 0.f;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q < nq) {
+              const int n = 4 * (hl + 16 * q);
+              hv[q].x = decay * hv[q].x + dx * bs[n];
+              hv[q].y = decay * hv[q].y + dx * bs[n + 1];
+              hv[q].z = decay * hv[q].z + dx * bs[n + 2];
+              hv[q].w = decay * hv[q].w + dx * bs[n + 3];
+              st[hl + 16 * q] = hv[q];
+              acc = fmaf(cs[n], hv[q].x, acc);
+              acc = fmaf(cs[n + 1], hv[q].y, acc);
+              acc = fmaf(cs[n + 2], hv[q].z, acc);
+              acc = fmaf(cs[n + 3], hv[q].w, acc);
+            }
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(hmask, acc, o);
+          if (hl == 0) {
+            const float y = acc + Dh * xv;  // decode.py:132
+            const float uu = y * silu(zv);
+            a.u[(size_t)b * a.d_inner + k] = __float2bfloat16_rn(uu);
+            s_uu[b][kk] = uu * uu;
+          }
         }
-        acc = warp_sum(acc);
-        if (lane == 0) {
-          const float y = acc + Dv[h] * xv;  // decode.py:132
-          const float uu = y * silu(zv);
-          a.u[(size_t)b * a.d_inner + h * a.P + pp] = __float2bfloat16_rn(uu);
-          a.usq[(size_t)b * a.d_inner + h * a.P + pp] = uu * uu;
-        }
+      }
+      named_barrier_sync(1, MEGA_CT);
+      if (warp < B) {  // fixed-order sum (deterministic)
+        float t = 0.f;
+        for (int kk = lane; kk < own.nk; kk += 32) t += s_uu[warp][kk];
+        t = warp_sum(t);
+        if (lane == 0) a.upart[(size_t)blockIdx.x * B + warp] = t;
       }
     }
     MEGA_TRACE(l * 8 + 4);
     mega_grid_sync(a, bar_idx);
     MEGA_TRACE(l * 8 + 5);
-    // ---------------- P3: out_proj + norm row scale + residual
+    // ---------------- B: out_proj + norm row scale + residual
     {
       const uint4 *src = reinterpret_cast<const uint4 *>(a.u);
       uint4 *dst = reinterpret_cast<uint4 *>(xs);
       for (int i = threadIdx.x; i < BT * a.d_inner / 8; i += MEGA_CT)
-        dst[i] = i < B * a.d_inner / 8 ? src[i] : make_uint4(0, 0, 0, 0);
-      if (warp < B) {
-        const float4 *q = reinterpret_cast<const float4 *>(a.usq + (size_t)warp * a.d_inner);
+        dst[i] = i < B * a.d_inner / 8 ? __ldcg(src + i) : make_uint4(0, 0, 0, 0);
+      if (warp < B) {  // fixed-order sum of the per-CTA partials (deterministic)
         float t = 0.f;
-        for (int j = lane; j < a.d_inner / 4; j += 32) {
-          const float4 v = q[j];
-          t += (v.x + v.y) + (v.z + v.w);
-        }
+        for (int i = lane; i < (int)gridDim.x; i += 32) t += __ldcg(&a.upart[(size_t)i * B + warp]);
         t = warp_sum(t);
         if (lane == 0) s_scale[warp] = 1.f / sqrtf(t / (float)a.d_inner + a.eps);
       }
       named_barrier_sync(1, MEGA_CT);
       MEGA_TRACE(l * 8 + 6);
+      const int r0 = (int)((long)a.d_model * blockIdx.x / gridDim.x);
+      const int nr = (int)((long)a.d_model * (blockIdx.x + 1) / gridDim.x) - r0;
       gemv(
-          a.d_model, a.d_inner,
+          a.d_inner, nr, [&](int i) { return r0 + i; },
           [&](int n, bool ok) {
-            NoPre e{};
+            Pre e{};
             if (ok && lane < B) e.old = a.hidden[(size_t)lane * a.d_model + n];
             return e;
           },
-          [&](int n, int b, float v, const NoPre &e) {
+          [&](int n, int b, float v, const Pre &e) {
             const float nv = e.old + s_scale[b] * v;
             a.hidden[(size_t)b * a.d_model + n] = nv;
             a.hidden_lp[(size_t)b * a.d_model + n] = __float2bfloat16_rn(nv);
-          });
+          },
+          no_post);
     }
     MEGA_TRACE(l * 8 + 7);
     mega_grid_sync(a, bar_idx);
@@ -453,9 +500,11 @@ __global__ void __launch_bounds__(MEGA_THREADS, 1) decode_mega(MegaArgs a) {
                     : __float2bfloat16_rn(0.f);
     }
     named_barrier_sync(1, MEGA_CT);
+    const int hr0 = (int)((long)a.V * blockIdx.x / gridDim.x);
+    const int hnr = (int)((long)a.V * (blockIdx.x + 1) / gridDim.x) - hr0;
     gemv(
-        a.V, a.d_model, [&](int, bool) { return NoPre{}; },
-        [&](int n, int b, float v, const NoPre &) {
+        a.d_model, hnr, [&](int i) { return hr0 + i; }, [&](int, bool) { return Pre{}; },
+        [&](int n, int b, float v, const Pre &) {
           if (a.logits) a.logits[(size_t)b * a.V + n] = v;
 #pragma unroll
           for (int bb = 0; bb < DEC_MAX_B; ++bb)
@@ -463,7 +512,8 @@ __global__ void __launch_bounds__(MEGA_THREADS, 1) decode_mega(MegaArgs a) {
               best[bb] = v;
               bidx[bb] = n;
             }
-        });
+        },
+        no_post);
 #pragma unroll
     for (int bb = 0; bb < DEC_MAX_B; ++bb)
       if (lane == bb) {

@@ -24,10 +24,12 @@ def main():
     ap.add_argument("--model", default="1.3b")
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--layers", type=int, default=0)
+    ap.add_argument("--prefetch", type=int, default=1)
     args = ap.parse_args()
     kw = {"n_layers": args.layers} if args.layers else {}
     cfg = m.named_config(args.model, compute="bf16", **kw)
     params = m.synthetic_init(cfg, seed=0)
+    _abi.lib().ssd200_set_option(3, args.prefetch)
     prompt = torch.randint(0, cfg.vocab_size, (args.batch, 16), device="cuda")
     _, cache = m.prefill(params, prompt, cfg, logits=None)
     dec = m.GreedyDecoder(params, cfg, cache, 20, use_graph=False)
@@ -67,6 +69,22 @@ def main():
     print("producer done W_in/W_out per layer (us from t0):",
           " ".join(f"{(p-t0)/1e3:.0f}" for p in prod[:8]), "... E at", f"{(prod[-1]-t0)/1e3:.0f}")
 
+
+
+    arr = t[5400:5400 + nsm]
+    rel = t[5600:5600 + nsm]
+    if arr.min() > 0:
+        print(f"layer-1 P1 barrier: CTA arrival min {(arr.min()-t0)/1e3:.1f} max {(arr.max()-t0)/1e3:.1f} us; "
+              f"release seen min {(rel.min()-t0)/1e3:.1f} max {(rel.max()-t0)/1e3:.1f} us; "
+              f"thread-0 P1 end -> CTA arrival: max {(arr - p1e).max()/1e3:.2f} us")
+
+
+    ps = t[6000:6000 + 40]
+    cs = t[6600:6600 + 40]
+    print("pf_ahead", int(t[7000]), "pf_bytes", int(t[7001]), "cp_bytes", int(t[7002]))
+    print("stage k: producer slot acquired / consumer warp0 data ready (us from t0)")
+    for k in range(0, 24):
+        print(f"  {k:2d} {(ps[k]-t0)/1e3:8.2f} {(cs[k]-t0)/1e3:8.2f}")
 
 if __name__ == "__main__":
     main()
