@@ -56,9 +56,8 @@ typedef struct ssd200_dims {
 
 typedef struct ssd200_layer {
   const void *W_in, *conv_w, *conv_b, *dt_bias, *a, *D, *norm_w, *W_out;
-  /* bf16 decode only (ssd200_decode_step): W_out with norm_w folded in, in
-   * the reference (d_inner, d_model) layout, read by the K-split out_proj.
-   * May be NULL everywhere else. */
+  /* optional: W_out with norm_w folded in, reference (d_inner, d_model)
+   * layout.  Reserved for a K-split decode out_proj; may be NULL. */
   const void *W_out_t;
 } ssd200_layer_t;
 
@@ -113,9 +112,9 @@ int ssd200_head(const ssd200_dims_t *d, int vocab, const void *hidden, int64_t h
  * decode.py:77-144 for batch <= 8: embed tokens, every layer (in_proj,
  * conv/SSM update in place, gate, out_proj + norm + residual), final norm,
  * tied head, argmax (ties -> lowest id).  layers_dev is a DEVICE array of
- * n_layers ssd200_layer_t whose W_out_t must be set.  ssm (n_layers, B, H, P,
- * N) and conv (n_layers, B, conv_dim, k-1) are updated in place; hidden
- * (B, d_model) f32 and hidden_lp are scratch.  barrier_state: two uint32
+ * n_layers ssd200_layer_t.  ssm (n_layers, B, H, P, N) and conv
+ * (n_layers, B, conv_dim, k-1) are updated in place; hidden (B, d_model) f32
+ * and hidden_lp are scratch.  barrier_state: two uint32
  * owned by the caller (reset by every call).  Returns
  * SSD200_EUNSUPPORTED for configurations the fused step does not cover
  * (the per-layer entry points handle those). */

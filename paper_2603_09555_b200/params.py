@@ -36,8 +36,8 @@ class LayerParams:
     norm_w: torch.Tensor
     W_out: torch.Tensor
     a: torch.Tensor = field(default=None)  # -exp(A_log), compute dtype (f32 in bf16 mode)
-    # bf16 only: norm_w-folded W_out in the reference (d_inner, d_model) layout,
-    # streamed by the fused decode step's K-split out_proj
+    # optional norm_w-folded W_out in the reference (d_inner, d_model) layout
+    # (ssd200_layer_t.W_out_t; unused by the current kernels)
     W_out_t: torch.Tensor = field(default=None)
 
 
@@ -116,7 +116,6 @@ def from_reference(params, cfg: ModelConfig, device="cuda") -> ModelParams:
                 norm_w=small(lp.norm_w),
                 W_out=big(W_out, transpose=True),
                 a=small(decay_coefficient(_np(lp.A_log), cfg)),
-                W_out_t=big(W_out) if mode == "bf16" else None,
             )
         )
     return ModelParams(
@@ -204,7 +203,6 @@ def synthetic_init(cfg: ModelConfig, seed: int = 0, device="cuda") -> ModelParam
                 norm_w=torch.ones(cfg.d_inner, device=dev, dtype=wd),
                 W_out=w_out.contiguous(),
                 a=torch.as_tensor(decay_coefficient(a_log.cpu().numpy(), cfg), dtype=wd).to(dev),
-                W_out_t=w_out.t().contiguous() if mode == "bf16" else None,
             )
         )
     return ModelParams(
