@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--decode-steps", type=int, default=64)
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--fused-conv", default="auto", choices=("auto", "on", "off"),
+                    help="conv1d fused into the in_proj epilogue (default: by width)")
     return ap.parse_args()
 
 
@@ -294,6 +296,7 @@ def run_prefill(args, rank, world, local):
     host_tok = torch.randint(0, cfg.vocab_size, (B, T), generator=g, dtype=torch.int64).pin_memory()
     dev_tok = host_tok.cuda()
     lib = _abi.lib()
+    lib.ssd200_set_option(1, {"auto": 0, "on": 1, "off": 0}[args.fused_conv])
 
     # per-phase CUDA events around every layer's phases (5 phases x 2)
     L = cfg.n_layers

@@ -143,8 +143,8 @@ int ssd200_set_phase_events(void *const *events, int n_phases);
 /* Debug: device buffer (>= 8192 uint64) that ssd200_decode_step fills with
  * %globaltimer stamps of CTA 0's phases; NULL disables. */
 int ssd200_debug_trace(void *device_buffer);
-/* Implementation choices (thread-local): option 1 = force the conv1d+SiLU
- * fused into the in_proj GEMM epilogue (default: only when d_model >= 2048);
+/* Implementation choices (thread-local): option 1 = conv1d+SiLU fused into
+ * the in_proj GEMM epilogue (1) instead of the separate conv kernel (0, default);
  * option 2 = force the fused chunk-state + inter-chunk pass scan kernel
  * (default: when batch * heads fills the GPU). */
 int ssd200_set_option(int option, int value);

@@ -26,7 +26,7 @@ thread_local uint64_t g_launches = 0;
 thread_local void *const *g_phase_ev = nullptr;
 thread_local int g_nphase = 0;
 thread_local void *g_mega_trace = nullptr;  // debug: device buffer of >= 8192 u64
-thread_local bool g_force_fused_conv = false;  // tests: exercise the fused-conv in_proj
+thread_local int g_force_fused_conv = 0;  // option 1: 1 = fused-conv in_proj epilogue (else separate)
 thread_local bool g_force_chunkscan = false;   // tests: exercise the fused state+pass scan
 
 enum { PH_IN_PROJ = 0, PH_CONV = 1, PH_SCAN = 2, PH_NORM = 3, PH_OUT_PROJ = 4 };
@@ -540,7 +540,10 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
   // conv fused into the in_proj epilogue only when the K loop (d_model) is
   // long enough to hide the extra epilogue work; otherwise the standalone
   // streaming conv kernel is faster (measured: 370M d_model 1024 -> separate).
-  const bool fuse_conv = tc_ssd_eligible(d) && k == 4 && (d->d_model >= 2048 || g_force_fused_conv);
+  // conv1d + SiLU fused into the in_proj epilogue: measured slower than the
+  // separate TMA-tiled conv kernel at 370M and 2.7B (the epilogue becomes the
+  // GEMM's bottleneck), so it is opt-in
+  const bool fuse_conv = tc_ssd_eligible(d) && k == 4 && g_force_fused_conv == 1;
   phase_mark(PH_IN_PROJ, 0, st);
   int rc;
   if (fuse_conv) {
@@ -1341,7 +1344,7 @@ int ssd200_debug_trace(void *device_buffer) {
 int ssd200_set_option(int option, int value) {
   switch (option) {
     case 1:  // force the conv1d fused into the in_proj epilogue (else size-based)
-      g_force_fused_conv = value != 0;
+      g_force_fused_conv = value;
       return SSD200_OK;
     case 2:  // force the fused chunk-state + pass scan kernel (else size-based)
       g_force_chunkscan = value != 0;

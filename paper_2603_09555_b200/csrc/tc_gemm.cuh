@@ -74,7 +74,10 @@ template <int BN> struct TcCfg {
   static constexpr uint32_t B_BYTES = BN * BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+  // per epilogue warp: a 32-row x 16-word transpose buffer (padded) so that
+  // global stores of the epilogue are row-contiguous (coalesced)
+  static constexpr uint32_t XPOSE_BYTES = 8 * 32 * 17 * 4;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + XPOSE_BYTES + 1024 + 256;
 };
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
@@ -179,7 +182,8 @@ __global__ void __launch_bounds__(320, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t *sA = smem;
   uint8_t *sB = smem + STAGES * Cfg::A_BYTES;
-  uint64_t *full = reinterpret_cast<uint64_t *>(sB + STAGES * Cfg::B_BYTES);
+  uint32_t *sX = reinterpret_cast<uint32_t *>(sB + STAGES * Cfg::B_BYTES);  // transpose buffers
+  uint64_t *full = reinterpret_cast<uint64_t *>(sB + STAGES * Cfg::B_BYTES + Cfg::XPOSE_BYTES);
   uint64_t *empty = full + STAGES;
   uint64_t *tfull = empty + STAGES;
   uint64_t *tempty = tfull + 2;
@@ -283,15 +287,24 @@ __global__ void __launch_bounds__(320, 1)
         for (int gg = 0; gg < ep.ng; ++gg) s += ep.ssq[(size_t)m * ep.ng + gg];
         rowscale = 1.f / sqrtf(s * ep.inv_d + ep.eps);
       }
-      float4 hv[8];
-      auto fetch = [&](int cc, float4(&dst)[8]) {
+      // transposed view of a 32 x 32 chunk: lanes 0-15 / 16-31 take rows 2i / 2i+1,
+      // column (lane & 15) of each 16-column half -> row-contiguous global accesses
+      uint32_t *xpb = sX + (warp - 2) * (32 * 17);
+      const int m_w = m_blk * RSTRIDE - HALO + q * 32;  // global row of this warp's lane 0
+      const int tc = lane & 15, tr = lane >> 4;
+      float hv[32];  // residual, transposed layout: [half h][pair i] -> hv[16 h + i]
+      auto fetch = [&](int cc, float(&dst)[32]) {
         const int n0 = n_blk * BN + cc;
-        if (RESID && m < M && vec_ok && n0 + 32 <= N && cc < BN) {
-          const float4 *src =
-              reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(ep.C) +
-                                               (size_t)m * ep.ldc + n0);
+        if (RESID && cc < BN && n0 < N) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) dst[j] = src[j];
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int mr = m_w + 2 * i + tr, n = n0 + 16 * h + tc;
+              dst[16 * h + i] = (mr < M && n < N)
+                                    ? reinterpret_cast<const float *>(ep.C)[(size_t)mr * ep.ldc + n]
+                                    : 0.f;
+            }
         }
       };
       fetch(half * 32, hv);
@@ -302,7 +315,7 @@ __global__ void __launch_bounds__(320, 1)
       for (int cc = half * 32; cc < BN; cc += 64) {
         const int n0 = n_blk * BN + cc;
         if (n0 >= N) break;  // warp-uniform
-        float4 hn[8];
+        float hn[32];
         fetch(cc + 64, hn);  // next residual chunk in flight during this one
         uint32_t r[32];
         sm100::tmem_ld32(trow + cc, r);
@@ -351,11 +364,20 @@ __global__ void __launch_bounds__(320, 1)
               else
                 pk[j >> 1] = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(o));
             }
-            if (out_row) {
-              uint4 *dst = reinterpret_cast<uint4 *>(ep.act + (size_t)m * ep.conv_dim + c0);
+            {  // post-conv xBC, stored row-contiguously through the transpose buffer
 #pragma unroll
-              for (int j = 0; j < 4; ++j)
-                dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+              for (int j = 0; j < 16; ++j) xpb[lane * 17 + j] = pk[j];
+              __syncwarp();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const int ir = q * 32 + 2 * i + tr, mr = m_w + 2 * i + tr;
+                if (ir >= HALO && mr < M)
+                  reinterpret_cast<uint32_t *>(ep.act + (size_t)mr * ep.conv_dim + c0)[tc] =
+                      xpb[(2 * i + tr) * 17 + tc];
+              }
+              __syncwarp();
+            }
+            if (out_row) {
               if (t >= ep.T - 3) {  // pre-activation conv tail, newest last (model.py:144-147)
                 float *tail = ep.conv_tail + ((size_t)(m / ep.T) * ep.conv_dim + c0) * 3 +
                               (t - (ep.T - 3));
@@ -363,33 +385,65 @@ __global__ void __launch_bounds__(320, 1)
                 for (int j = 0; j < 32; ++j) tail[j * 3] = __uint_as_float(r[j]);
               }
             }
+          } else if (n0 + 32 <= ep.d_inner && vec_ok) {
+            // z columns (bf16), stored row-contiguously
+            bf16 *C = reinterpret_cast<bf16 *>(ep.C);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              xpb[lane * 17 + j] = pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int ir = q * 32 + 2 * i + tr, mr = m_w + 2 * i + tr;
+              if (ir >= HALO && mr < M)
+                reinterpret_cast<uint32_t *>(C + (size_t)mr * ep.ldc + n0)[tc] =
+                    xpb[(2 * i + tr) * 17 + tc];
+            }
+            __syncwarp();
           } else if (out_row) {
-            // z columns (bf16) or dt columns (f32 softplus), like TC_EPI_INPROJ
+            // dt columns (f32 softplus) and ragged z chunks, like TC_EPI_INPROJ
             tc_store_chunk<TC_EPI_INPROJ>(ep, r, m, n0, N, 1.f);
           }
-        } else if (m < M) {
-          if (RESID && vec_ok && n0 + 32 <= N) {
-            float *dst = reinterpret_cast<float *>(ep.C) + (size_t)m * ep.ldc + n0;
-            bf16 *lp = ep.C_lp + (size_t)m * ep.ldc + n0;
+        } else if constexpr (RESID) {
+          // hidden += acc * rowscale: f32 + bf16 shadow, stored row-contiguously
+          float *C = reinterpret_cast<float *>(ep.C);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              float4 o = hv[j];
-              o.x += __uint_as_float(r[4 * j + 0]) * rowscale;
-              o.y += __uint_as_float(r[4 * j + 1]) * rowscale;
-              o.z += __uint_as_float(r[4 * j + 2]) * rowscale;
-              o.w += __uint_as_float(r[4 * j + 3]) * rowscale;
-              reinterpret_cast<float4 *>(dst)[j] = o;
-              uint2 pk;
-              pk.x = pack_bf16x2(o.x, o.y);
-              pk.y = pack_bf16x2(o.z, o.w);
-              reinterpret_cast<uint2 *>(lp)[j] = pk;
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              xpb[lane * 17 + j] = __float_as_uint(__uint_as_float(r[16 * h + j]) * rowscale);
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int mr = m_w + 2 * i + tr, n = n0 + 16 * h + tc;
+              if (mr < M && n < N) {
+                const float o = hv[16 * h + i] + __uint_as_float(xpb[(2 * i + tr) * 17 + tc]);
+                C[(size_t)mr * ep.ldc + n] = o;
+                ep.C_lp[(size_t)mr * ep.ldc + n] = __float2bfloat16_rn(o);
+              }
             }
-          } else {
-            tc_store_chunk<EPI>(ep, r, m, n0, N, rowscale);
+            __syncwarp();
           }
+        } else if (EPI == TC_EPI_INPROJ && n0 + 32 <= ep.n_split && vec_ok) {
+          // bf16 z / xBC columns, stored row-contiguously (16 bf16 pairs per row)
+          bf16 *C = reinterpret_cast<bf16 *>(ep.C);
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            xpb[lane * 17 + j] = pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int mr = m_w + 2 * i + tr;
+            if (mr < M)
+              reinterpret_cast<uint32_t *>(C + (size_t)mr * ep.ldc + n0)[tc] =
+                  xpb[(2 * i + tr) * 17 + tc];
+          }
+          __syncwarp();
+        } else if (m < M) {
+          tc_store_chunk<EPI>(ep, r, m, n0, N, rowscale);
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) hv[j] = hn[j];
+        for (int j = 0; j < 32; ++j) hv[j] = hn[j];
       }
       if constexpr (EPI == TC_EPI_INPROJ_CONV)  // exchange buffers free for the next tile
         asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
