@@ -286,8 +286,9 @@ void launch_conv(const TI *in, long ld_in, const T *w, const T *bias, TO *out, l
 // Production Mamba-2 head dims: the tcgen05 scan (ssd_tc.cuh) handles these;
 // anything else runs the generic CUDA-core scan.
 inline bool tc_ssd_eligible(const ssd200_dims_t *d) {
+  // (H % 8: the in_proj row pitch 2 d_inner + 2 N + H stays 16-byte aligned for TMA)
   return d->head_dim == TC_P && d->d_state == TC_N && d->chunk_size == TC_L &&
-         d->n_groups == 1 && d->conv_kernel >= 1;
+         d->n_groups == 1 && d->conv_kernel >= 1 && d->n_heads % 8 == 0;
 }
 
 struct TcScanWs {
@@ -375,8 +376,12 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
   a.u_out = u_out;
   a.ssq = ssq;
   a.trace = static_cast<unsigned long long *>(g_mega_trace);
-  CUtensorMap tm_act, tm_prev;
+  CUtensorMap tm_act, tm_prev, tm_z, tm_u;
   int rc = make_map_3d(&tm_act, act, B, Tn, conv_dim, conv_dim, 128);
+  if (rc) return rc;
+  rc = make_map_3d(&tm_z, z, B, Tn, d->d_inner, z_ld, 128);
+  if (rc) return rc;
+  rc = make_map_3d(&tm_u, u_out, B, Tn, d->d_inner, d->d_inner, 32);
   if (rc) return rc;
   rc = make_map_2d(&tm_prev, ws.prev, (long)B * a.Nc * H * TC_P, TC_N, TC_N, 64);
   if (rc) return rc;
@@ -400,8 +405,8 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
   // outputs (+ D skip + gate)
   a.NG = pick_groups(H, (long)B * a.Nc * 2, 2 * sms, OutSmem::MAX_HG);
   a.HG = H / a.NG;
-  ssd_tc_out<<<B * a.Nc * 2 * a.NG, OUT_THREADS, OutSmem::TOTAL, st>>>(tm_act, tm_prev, a, act,
-                                                                        conv_dim);
+  ssd_tc_out<<<B * a.Nc * 2 * a.NG, OUT_THREADS, OutSmem::TOTAL, st>>>(tm_act, tm_prev, tm_z,
+                                                                        tm_u, a);
   LAUNCH_CHECK("ssd_tc_out");
   *ng_out = a.NG;
   return SSD200_OK;

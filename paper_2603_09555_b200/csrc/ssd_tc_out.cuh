@@ -55,7 +55,8 @@ struct OutSmem {
   static constexpr uint32_t GB = 32768;       // B rows 2 x [NS s][64 n]; then G bf16 [128 l][NS s]
   static constexpr uint32_t X0 = GB + 65536;  // 2 x [256 s][64 p]
   static constexpr uint32_t P0 = X0 + 2 * 32768;  // 2 x (2 x [64 p][64 n])
-  static constexpr uint32_t WC = P0 + 2 * 16384;  // per warp 4 x 8 OUT_CW f32 (cs2, cf, dt, cr)
+  static constexpr uint32_t Z0 = P0 + 2 * 16384;  // gate z of the current head [128 l][64 p]
+  static constexpr uint32_t WC = Z0 + 16384;       // per warp 4 x 8 OUT_CW f32 (cs2, cf, dt, cr)
   static constexpr uint32_t SQ = WC + OUT_MW * 4 * 8 * OUT_CW * 4;  // ssq of slices 1..
   static constexpr uint32_t DH = SQ + (OUT_KW - 1) * 512;  // D of the group's heads (<= 128)
   static constexpr uint32_t BAR = DH + 512;
@@ -72,7 +73,8 @@ __device__ __forceinline__ uint8_t *smem_align1k(uint8_t *raw) {
 
 __global__ void __launch_bounds__(OUT_THREADS, 1)
     ssd_tc_out(const __grid_constant__ CUtensorMap tm_act, const __grid_constant__ CUtensorMap tm_prev,
-               TcSsdArgs p, const bf16 *__restrict__ act, long act_ld) {
+               const __grid_constant__ CUtensorMap tm_z, const __grid_constant__ CUtensorMap tm_u,
+               TcSsdArgs p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t *sm = smem_align1k(smem_raw);
   uint64_t *bar_cb = reinterpret_cast<uint64_t *>(sm + OutSmem::BAR);
@@ -84,7 +86,9 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
   uint64_t *bar_y = bar_cb + 10;  // [2] accumulator set ready
   uint64_t *yfree = bar_cb + 12;  // [2] accumulator set read out
   uint64_t *mrdy = bar_cb + 14;   // [2] M buffer written (one arrival per math warp)
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bar_cb + 16);
+  uint64_t *bar_z = bar_cb + 16;  // z tile landed
+  uint64_t *zfree = bar_cb + 17;  // z tile read (one arrival per math warp)
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bar_cb + 18);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half_grid = gridDim.x >> 1;
@@ -100,17 +104,21 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tm_act);
     sm100::tma_prefetch(&tm_prev);
+    sm100::tma_prefetch(&tm_z);
+    sm100::tma_prefetch(&tm_u);
     sm100::mbar_init(bar_cb, 1);
     sm100::mbar_init(bar_g, 1);
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&bar_x[i], 1);
-      sm100::mbar_init(&xfree[i], 1);
+      sm100::mbar_init(&xfree[i], 1 + OUT_MW);  // MMA commit + every math warp's D-skip read
       sm100::mbar_init(&bar_p[i], 1);
       sm100::mbar_init(&pfree[i], 1);
       sm100::mbar_init(&bar_y[i], 1);
       sm100::mbar_init(&yfree[i], OUT_MATH);
       sm100::mbar_init(&mrdy[i], OUT_MW);
     }
+    sm100::mbar_init(bar_z, 1);
+    sm100::mbar_init(zfree, 4);  // one arrival per lane quarter once its u store has read smem
     sm100::fence_barrier_init();
   }
   if (warp == 1) sm100::tmem_alloc<512>(tslot);
@@ -144,6 +152,9 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
         for (int q = 0; q <= R; ++q)
           sm100::tma_load_3d(sm + OutSmem::X0 + buf * 32768 + q * 16384, &tm_act, &bar_x[buf],
                              h * TC_P, c * TC_L + q * 128, b);
+        sm100::mbar_wait(zfree, (i & 1) ^ 1);  // single buffer: head i-1's epilogue read it
+        sm100::mbar_arrive_expect_tx(bar_z, 16384);
+        sm100::tma_load_3d(sm + OutSmem::Z0, &tm_z, bar_z, h * TC_P, c * TC_L + R * 128, b);
       }
     }
   } else if (warp == 1) {
@@ -239,9 +250,6 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
     auto gpiece = [&](int pc) -> uint4 * {
       return reinterpret_cast<uint4 *>(grow + ((pc ^ gsw) << 4));
     };
-    const long trow = (long)b * p.T + (valid ? t : 0);
-    const bf16 *xrow = act + trow * act_ld;
-    const bf16 *zrow = p.z + trow * p.z_ld;
     float ssq = 0.f;
 
     struct Pref {
@@ -424,13 +432,6 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
     for (int i = 0; i < p.HG; ++i) {
       const int buf = i & 1, h = h0 + i;
       uint4 xv[EW / 8], zv[EW / 8];  // x (D skip) and z (gate) of head i, columns [pc, pc+EW)
-      const uint4 *xg = reinterpret_cast<const uint4 *>(xrow + h * TC_P + pc);
-      const uint4 *zg = reinterpret_cast<const uint4 *>(zrow + h * TC_P + pc);
-#pragma unroll
-      for (int cc = 0; cc < EW / 8; ++cc) {
-        xv[cc] = xg[cc];
-        zv[cc] = zg[cc];
-      }
       const float el = ex2(csl);
       const float Dh = d_s[i];
 #if SSD200_OUT_TRACE
@@ -453,15 +454,25 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
 #if SSD200_OUT_TRACE
       if (tw) tw[1] = clk64();
 #endif
+      sm100::mbar_wait(bar_z, i & 1);  // z tile of head i (TMA, SWIZZLE_128B)
+#pragma unroll
+      for (int cc = 0; cc < EW / 8; ++cc)
+        zv[cc] = *reinterpret_cast<const uint4 *>(sm + OutSmem::Z0 + sw128_off(row, pc / 8 + cc));
       sm100::mbar_wait(&bar_y[buf], (i >> 1) & 1);  // MMA(i) done
+      {  // D-skip x from the X tile the MMA just consumed (row l of the chunk), then release it
+        const uint8_t *xt = sm + OutSmem::X0 + buf * 32768 + R * 16384;
+#pragma unroll
+        for (int cc = 0; cc < EW / 8; ++cc)
+          xv[cc] = *reinterpret_cast<const uint4 *>(xt + sw128_off(row, pc / 8 + cc));
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&xfree[buf]);
+      }
 #if SSD200_OUT_TRACE
       if (tw) tw[2] = clk64();
 #endif
       sm100::tc_fence_after();
       // ---- epilogue(i) on columns [pc, pc+EW) in 16-column steps, overlapping MMA(i+1)
       const uint32_t ydt = tmem + lane_off + TM_Y + buf * 128 + pc;
-      uint32_t *urow =
-          reinterpret_cast<uint32_t *>(p.u_out + ((long)b * p.T + t) * p.d_inner + h * TC_P + pc);
       const __nv_bfloat162 *xe = reinterpret_cast<const __nv_bfloat162 *>(xv);
       const __nv_bfloat162 *ze = reinterpret_cast<const __nv_bfloat162 *>(zv);
 #pragma unroll
@@ -487,11 +498,22 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
           __nv_bfloat162 v = __floats2bfloat162_rn(u0, u1);
           out[j] = *reinterpret_cast<uint32_t *>(&v);
         }
-        if (valid) {
-          uint4 *u4 = reinterpret_cast<uint4 *>(urow + 8 * hs);
-          u4[0] = make_uint4(out[0], out[1], out[2], out[3]);
-          u4[1] = make_uint4(out[4], out[5], out[6], out[7]);
-        }
+        // u overwrites this thread's own z positions of the tile (read above)
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          *reinterpret_cast<uint4 *>(sm + OutSmem::Z0 + sw128_off(row, pc / 8 + 2 * hs + k)) =
+              make_uint4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+      }
+      // the quarter's 32 x 64 u tile leaves through TMA (rows past T are clipped);
+      // the z buffer is released once the store has read it
+      sm100::fence_proxy_async();
+      named_bar(4 + q, 32 * OUT_KW);
+      if (kw == 0 && lane == 0) {
+        sm100::tma_store_3d(&tm_u, sm + OutSmem::Z0 + q * 4096, h * TC_P,
+                            c * TC_L + R * 128 + q * 32, b);
+        sm100::bulk_commit();
+        sm100::bulk_wait_read0();
+        sm100::mbar_arrive(zfree);
       }
 #if SSD200_OUT_TRACE
       if (tw) tw[3] = clk64();
