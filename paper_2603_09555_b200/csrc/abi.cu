@@ -383,7 +383,7 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
   if (rc) return rc;
   rc = make_map_3d(&tm_u, u_out, B, Tn, d->d_inner, d->d_inner, 32);
   if (rc) return rc;
-  rc = make_map_2d(&tm_prev, ws.prev, (long)B * a.Nc * H * TC_P, TC_N, TC_N, 64);
+  rc = make_map_2d(&tm_prev, ws.prev, (long)B * a.Nc * H * TC_N, TC_P, TC_P, 128);
   if (rc) return rc;
   const long sms = num_sms();
   // chunk cumsums

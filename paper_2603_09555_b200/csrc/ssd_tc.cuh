@@ -36,7 +36,7 @@ struct TcSsdArgs {
   float *dtT;         // (B, H, Nc*L) dt transposed (0 past T)
   float *cs_end;      // (B, H, Nc)
   float *S;           // (B, Nc, H, P, N) f32: each chunk's own end state
-  bf16 *prev;         // (B, Nc, H, P, N) bf16: state entering each chunk
+  bf16 *prev;         // (B, Nc, H, N, P) bf16: state entering each chunk (transposed)
   float *final_state; // (B, H, P, N)
   bf16 *u_out;        // (rows, d_inner)
   float *ssq;         // (rows, NG) partial sum of u^2
@@ -328,7 +328,9 @@ __global__ __launch_bounds__(256) void ssd_tc_pass(TcSsdArgs p) {
     for (int j = 0; j < 8; ++j) {
       const int c = c0 + j;
       if (c < p.Nc) {
-        p.prev[(((long)b * p.Nc + c) * p.H + h) * PN + e] = __float2bfloat16_rn(s);
+        // prev is stored [n][p] per (b, c, h); e indexes S's [p][n] layout
+        p.prev[(((long)b * p.Nc + c) * p.H + h) * PN + (e % TC_N) * TC_P + e / TC_N] =
+            __float2bfloat16_rn(s);
         s = expf(dec[j]) * s + own[j];
       }
     }
@@ -469,15 +471,22 @@ __global__ void __launch_bounds__(192, 1)
       sm100::tc_fence_before();
       sm100::mbar_arrive(&tfree[st]);
       const float decay = expf(ceg[c]);
-      bf16 *pv = p.prev + (((long)b * Nc + c) * p.H + h) * TC_P * TC_N + n;
+      // state entering chunk c, stored [n][p]: this thread's 64 values are contiguous
+      uint4 *pv = reinterpret_cast<uint4 *>(
+          p.prev + ((((long)b * Nc + c) * p.H + h) * TC_N + n) * TC_P);
 #pragma unroll
-      for (int pp = 0; pp < 32; ++pp) {
-        pv[(long)pp * TC_N] = __float2bfloat16_rn(s[pp]);  // state entering chunk c
-        s[pp] = decay * s[pp] + __uint_as_float(r0[pp]);
+      for (int g = 0; g < TC_P / 8; ++g) {
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 v = __floats2bfloat162_rn(s[8 * g + 2 * e], s[8 * g + 2 * e + 1]);
+          w[e] = *reinterpret_cast<uint32_t *>(&v);
+        }
+        pv[g] = make_uint4(w[0], w[1], w[2], w[3]);
       }
 #pragma unroll
       for (int pp = 0; pp < 32; ++pp) {
-        pv[(long)(pp + 32) * TC_N] = __float2bfloat16_rn(s[pp + 32]);
+        s[pp] = decay * s[pp] + __uint_as_float(r0[pp]);
         s[pp + 32] = decay * s[pp + 32] + __uint_as_float(r1[pp]);
       }
     }

@@ -54,7 +54,7 @@ struct OutSmem {
   static constexpr uint32_t CR = 0;           // C rows of the tile: 2 x [128 l][64 n] (SW128)
   static constexpr uint32_t GB = 32768;       // B rows 2 x [NS s][64 n]; then G bf16 [128 l][NS s]
   static constexpr uint32_t X0 = GB + 65536;  // 2 x [256 s][64 p]
-  static constexpr uint32_t P0 = X0 + 2 * 32768;  // 2 x (2 x [64 p][64 n])
+  static constexpr uint32_t P0 = X0 + 2 * 32768;  // 2 x [128 n][64 p]
   static constexpr uint32_t Z0 = P0 + 2 * 16384;  // gate z of the current head [128 l][64 p]
   static constexpr uint32_t WC = Z0 + 16384;       // per warp 4 x 8 OUT_CW f32 (cs2, cf, dt, cr)
   static constexpr uint32_t SQ = WC + OUT_MW * 4 * 8 * OUT_CW * 4;  // ssq of slices 1..
@@ -143,10 +143,8 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
         const uint32_t par = ((i >> 1) & 1) ^ 1;
         sm100::mbar_wait(&pfree[buf], par);
         sm100::mbar_arrive_expect_tx(&bar_p[buf], 16384);
-        const int prow = (((b * p.Nc + c) * p.H + h) * TC_P);
-        for (int nb = 0; nb < 2; ++nb)
-          sm100::tma_load_2d(sm + OutSmem::P0 + buf * 16384 + nb * 8192, &tm_prev, &bar_p[buf],
-                             nb * 64, prow);
+        const int prow = (((b * p.Nc + c) * p.H + h) * TC_N);  // prev (b, c, h) as [n][p]
+        sm100::tma_load_2d(sm + OutSmem::P0 + buf * 16384, &tm_prev, &bar_p[buf], 0, prow);
         sm100::mbar_wait(&xfree[buf], par);
         sm100::mbar_arrive_expect_tx(&bar_x[buf], NS * 128);
         for (int q = 0; q <= R; ++q)
@@ -173,7 +171,7 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
       }
       sm100::mma_commit(bar_g);
       constexpr uint32_t idy = sm100::idesc_bf16(128, TC_P, false, true);
-      constexpr uint32_t ido = sm100::idesc_bf16(128, TC_P, false, false);
+      constexpr uint32_t ido = sm100::idesc_bf16(128, TC_P, false, true);
       for (int i = 0; i < p.HG; ++i) {
         const int buf = i & 1;
         const uint32_t par = (i >> 1) & 1;
@@ -198,7 +196,7 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
 #pragma unroll
         for (int k = 0; k < TC_N / 16; ++k) {  // Yoff = C_R . prev^T (independent of M)
           const uint64_t ad = sm100::sw128_desc(cr + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = sm100::sw128_desc(pb + (k >> 2) * 8192 + (k & 3) * 32, 16, 1024);
+          const uint64_t bd = sm100::sw128_desc(pb + k * 2048, 8192, 1024);  // [n][p]: MN-major
           sm100::mma_bf16(yo, ad, bd, ido, k > 0);
         }
         sm100::mma_commit(&pfree[buf]);
