@@ -427,26 +427,37 @@ __global__ void __launch_bounds__(192, 1)
     const float *csg = p.cs + ((long)b * p.H + h) * csb;
     const float *dtg = p.dtT + ((long)b * p.H + h) * csb;
     const float *ceg = p.cs_end + ((long)b * p.H + h) * Nc;
-    auto scale = [&](int c) {
+    // row weights w_l = dt_l e^{cs_end - cs_l} of a chunk: loaded one chunk ahead
+    // so the global-load latency stays off the scale step
+    struct RowW {
+      float dt[2], cs[2], cend;
+    };
+    auto load_w = [&](int c, RowW &f) {
+      if (c >= Nc) return;
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        const long t = (long)c * TC_L + tid + rr * 128;
+        f.dt[rr] = t < p.T ? dtg[t] : 0.f;
+        f.cs[rr] = csg[t];
+      }
+      f.cend = ceg[c];
+    };
+    auto scale = [&](int c, const RowW &f) {
       const int st = c & 1;
       sm100::mbar_wait(&full[st], (c >> 1) & 1);
-      const float cend = ceg[c];
       uint8_t *xb = sm + st * ScanSmem::STG + ScanSmem::XO;
 #pragma unroll
       for (int rr = 0; rr < 2; ++rr) {
         const int l = tid + rr * 128;
-        const long t = (long)c * TC_L + l;
-        const float w = t < p.T ? dtg[t] * ex2((cend - csg[t]) * kLog2e) : 0.f;
+        const __nv_bfloat162 w2 =
+            __float2bfloat162_rn(f.dt[rr] * ex2((f.cend - f.cs[rr]) * kLog2e));
         uint4 *row = reinterpret_cast<uint4 *>(xb + l * 128);
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
+        for (int ch = 0; ch < 8; ++ch) {  // packed bf16 multiply (X is a bf16 MMA operand)
           uint4 v = row[ch];
           __nv_bfloat162 *e = reinterpret_cast<__nv_bfloat162 *>(&v);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float2 f = __bfloat1622float2(e[j]);
-            e[j] = __floats2bfloat162_rn(f.x * w, f.y * w);
-          }
+          for (int j = 0; j < 4; ++j) e[j] = __hmul2(e[j], w2);
           row[ch] = v;
         }
       }
@@ -457,9 +468,24 @@ __global__ void __launch_bounds__(192, 1)
     const long sbase = ((long)b * p.H + h) * TC_P * TC_N + n;
 #pragma unroll
     for (int pp = 0; pp < TC_P; ++pp) s[pp] = p.init ? p.init[sbase + (long)pp * TC_N] : 0.f;
-    scale(0);
+    // chunk k's weights live in wa (k even) / wb (k odd); chunk k+2's are fetched
+    // right after scale(k), two chunks before they are needed
+    RowW wa, wb;
+    load_w(0, wa);
+    load_w(1, wb);
+    scale(0, wa);
+    load_w(2, wa);
     for (int c = 0; c < Nc; ++c) {
-      if (c + 1 < Nc) scale(c + 1);
+      if (c + 1 < Nc) {
+        const int k = c + 1;
+        if (k & 1) {
+          scale(k, wb);
+          load_w(k + 2, wb);
+        } else {
+          scale(k, wa);
+          load_w(k + 2, wa);
+        }
+      }
       const int st = c & 1;
       sm100::mbar_wait(&sfull[st], (c >> 1) & 1);
       sm100::tc_fence_after();
