@@ -389,7 +389,8 @@ def run_prefill(args, rank, world, local):
     launch_ms = phase_ms[dom] / L
     achieved = phase_flops[dom] / (launch_ms / 1e3) / 1e12 if phase_flops[dom] else None
     peak = pk["bf16_tflops_sustained"]
-    kernel_key = {0: "tc_gemm_kernel<256,2>", 1: "conv_silu_prefill", 2: "ssd_scan", 3: "gated_norm_kernel", 4: "tc_gemm_kernel<256,3>"}[dom]
+    kernel_key = {0: "tc_gemm_kernel<256,2>", 1: "conv_silu_tma", 2: "ssd_scan",
+                  3: "gated_norm_kernel", 4: "tc_gemm_kernel<256,4>"}[dom]
     roof = {
         "kernel": f"{PHASES[dom]} ({kernel_key})",
         "bound": "tensor",

@@ -31,7 +31,7 @@ GROUPS = {
     "ssd_scan": ("ssd_tc_cumsum", "ssd_tc_chunkscan", "ssd_tc_out"),
     "tc_gemm_kernel<256,2>": ("void tc_gemm_kernel<256, 2>",),
     "tc_gemm_kernel<256,4>": ("void tc_gemm_kernel<256, 4>",),
-    "conv_silu_prefill": ("conv_silu_tma",),
+    "conv_silu_tma": ("conv_silu_tma",),
 }
 
 
@@ -54,6 +54,9 @@ def rows(report):
                 continue
             if m.startswith("dram__bytes"):
                 v *= UNIT.get(units[i], 1)
+            if m == "gpu__time_duration.sum":  # normalise to microseconds
+                v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+                      "second": 1e6, "s": 1e6}.get(units[i], 1.0)
             d[m] = v
         res.append(d)
     return res
