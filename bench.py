@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--decode-steps", type=int, default=64)
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shard", default="batch", choices=("batch", "heads"),
+                    help="N>1 prefill: batch rows per rank (weak scaling, default) or SSD head "
+                         "groups of one batch with an all-reduce after out_proj (strong scaling)")
     ap.add_argument("--fused-conv", default="auto", choices=("auto", "on", "off"),
                     help="conv1d fused into the in_proj epilogue (default: by width)")
     return ap.parse_args()
@@ -421,6 +424,69 @@ def run_prefill(args, rank, world, local):
     }
 
 
+def run_prefill_heads(args, rank, world, local):
+    """Head-group-sharded prefill: every rank runs the same
+    batch on its heads; one NCCL all-reduce of [partial | sum u^2] per layer.
+    Strong scaling: value = the batch's tokens / max-over-ranks step time."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_09555_b200 as m
+    from paper_2603_09555_b200 import _abi, shard
+
+    cfg = m.named_config(args.model, compute="bf16")
+    params = shard.synthetic_shard(cfg, rank, world, seed=1234, device=f"cuda:{local}")
+    B, T = args.batch, args.seqlen
+    g = torch.Generator(device="cpu").manual_seed(0)
+    host_tok = torch.randint(0, cfg.vocab_size, (B, T), generator=g, dtype=torch.int64).pin_memory()
+    dev_tok = host_tok.cuda()
+    lib = _abi.lib()
+
+    def step(tok):
+        run = shard.HeadShardedPrefill(params, tok, cfg)
+        for i in range(cfg.n_layers):
+            buf = run.partial(i)
+            if world > 1:
+                dist.all_reduce(buf, op=dist.ReduceOp.SUM)
+            run.finish()
+        return run.logits()
+
+    for _ in range(args.warmup):
+        step(dev_tok)
+    barrier(world)
+    n0 = lib.ssd200_launch_count()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        s0.record()
+        for _ in range(args.steps):
+            step(dev_tok)
+        s1.record()
+        torch.cuda.synchronize()
+    launches = lib.ssd200_launch_count() - n0
+    ms = max_over_ranks(s0.elapsed_time(s1) / args.steps, world)
+    host_out = torch.empty((B, cfg.vocab_size), dtype=torch.float32).pin_memory()
+    barrier(world)
+    s0.record()
+    for _ in range(args.steps):
+        lg = step(host_tok.to(f"cuda:{local}", non_blocking=True))
+        host_out.copy_(lg, non_blocking=True)
+    s1.record()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(s0.elapsed_time(s1) / args.steps, world)
+    flops = m.flops_prefill(cfg, T, B, head_rows=1)
+    pk = peaks()
+    tf = flops / (ms / 1e3) / 1e12
+    return {
+        "value": B * T / (ms / 1e3), "ms": ms, "e2e_value": B * T / (e2e_ms / 1e3),
+        "h2d": B * T * 8, "d2h": B * cfg.vocab_size * 4, "launches": launches,
+        "roofline": {"kernel": "whole step (head-sharded)", "bound": "tensor", "achieved": tf / world,
+                     "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                     "frac": tf / world / pk["bf16_tflops_sustained"], "traffic": None},
+        "phases_ms": None, "step_tflops_per_gpu": tf / world,
+        "step_mfu": tf / world / pk["bf16_tflops"], "clocks": clk.summary(), "flops_step": flops,
+    }
+
+
 def run_decode(args, local):
     """1.3B cached decode: one CUDA-graph step (all layers + head + argmax)
     replayed; HBM bytes = weights once + state read/write + logits."""
@@ -469,7 +535,8 @@ def main():
     import torch
 
     rank, world, local = dist_setup(args.gpus)
-    res = run_prefill(args, rank, world, local)
+    heads = args.shard == "heads"
+    res = (run_prefill_heads if heads else run_prefill)(args, rank, world, local)
     dec = None
     if not args.no_decode:
         dec = run_decode(args, local)
@@ -488,24 +555,26 @@ def main():
             "warmup": args.warmup,
             "ms_per_step": res["ms"],
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if heads else "weak",
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic (random ids; device-drawn weights with the reference init distributions)",
             "config": {
                 "workload": f"Mamba-2 {args.model} bf16 chunked-SSD prefill (BASELINE configs[1] sweep point)",
-                "batch_per_gpu": args.batch,
-                "global_batch": args.batch * world,
+                "batch_per_gpu": args.batch if not heads else args.batch / world,
+                "global_batch": args.batch if heads else args.batch * world,
                 "seq_len": args.seqlen,
                 "chunk": 256,
                 "head": "tied head on the last position only",
-                "parallelism": f"batch-sharded x{world} (no data-path collective)",
+                "parallelism": (f"SSD-head-group-sharded x{world} (one NCCL all-reduce per layer)"
+                                if heads else f"batch-sharded x{world} (no data-path collective)"),
                 "l2": "working set > 126 MB L2 (activations + 0.74 GB weights per step); no flush",
             },
             "tflops_per_gpu": res["step_tflops_per_gpu"],
             "mfu": res["step_mfu"],
-            "e2e": {"value": res["e2e_value"], "unit": "tok/s", "h2d_bytes_per_step": res["h2d"] * world,
-                    "d2h_bytes_per_step": res["d2h"] * world},
+            "e2e": {"value": res["e2e_value"], "unit": "tok/s",
+                    "h2d_bytes_per_step": res["h2d"] * (1 if heads else world),
+                    "d2h_bytes_per_step": res["d2h"] * (1 if heads else world)},
             "roofline": res["roofline"],
             "phases_ms_per_step": res["phases_ms"],
             "cpu_baseline": cpu,

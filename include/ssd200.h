@@ -89,6 +89,26 @@ int ssd200_prefill_layer(const ssd200_dims_t *d, const ssd200_layer_t *w, void *
                          void *hidden_lp, void *ssm_out, void *conv_out, int batch, int seqlen,
                          void *workspace, size_t workspace_bytes, ssd200_stream_t stream);
 
+/* ---- head-group-sharded block_forward (bf16) --------------
+ * d describes THIS rank's shard (d_inner = local heads * head_dim, n_heads =
+ * local heads, a multiple of 8); w holds the shard's weights (its z/x/dt
+ * columns of W_in, its x conv channels + the replicated B/C ones, its D /
+ * dt_bias / a, and its rows of W_out with norm_w folded in).  Instead of
+ * updating hidden it writes, per row r, partial[r, 0:d_model] = u_local .
+ * W_out'_local and partial[r, d_model] = sum of u_local^2 (row pitch
+ * partial_ld, a multiple of 4, >= d_model + 1).  The caller sums partial
+ * over the ranks (one all-reduce) and applies ssd200_resid_norm_finish.
+ * Workspace: ssd200_prefill_layer_workspace(d, ...). */
+int ssd200_prefill_layer_partial(const ssd200_dims_t *d, const ssd200_layer_t *w,
+                                 const void *hidden_lp, float *partial, long partial_ld,
+                                 void *ssm_out, void *conv_out, int batch, int seqlen,
+                                 void *workspace, size_t workspace_bytes, ssd200_stream_t stream);
+/* hidden += partial[:, :d_model] * rsqrt(partial[:, d_model] / d_inner_full + eps),
+ * hidden_lp = bf16(hidden)  (model.py:166-173 after the all-reduce) */
+int ssd200_resid_norm_finish(int d_model, int d_inner_full, double eps, void *hidden,
+                             void *hidden_lp, const float *partial, long partial_ld, long rows,
+                             ssd200_stream_t stream);
+
 /* ---- one decode_step layer (decode.py:99-140) ----------------------------
  * ssm_out/conv_out may alias ssm_in/conv_in (in-place update for generate). */
 size_t ssd200_decode_layer_workspace(const ssd200_dims_t *d, int batch);

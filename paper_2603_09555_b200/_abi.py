@@ -69,6 +69,17 @@ SIGNATURES = [
         c_int,
         [ctypes.POINTER(Dims), ctypes.POINTER(Layer)] + [c_void_p] * 4 + [c_int, c_int, c_void_p, c_size_t, c_void_p],
     ),
+    (
+        "ssd200_prefill_layer_partial",
+        c_int,
+        [ctypes.POINTER(Dims), ctypes.POINTER(Layer), c_void_p, c_void_p, ctypes.c_long, c_void_p,
+         c_void_p, c_int, c_int, c_void_p, c_size_t, c_void_p],
+    ),
+    (
+        "ssd200_resid_norm_finish",
+        c_int,
+        [c_int, c_int, c_double, c_void_p, c_void_p, c_void_p, ctypes.c_long, ctypes.c_long, c_void_p],
+    ),
     ("ssd200_decode_layer_workspace", c_size_t, [ctypes.POINTER(Dims), c_int]),
     (
         "ssd200_decode_layer",

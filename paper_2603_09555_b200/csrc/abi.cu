@@ -518,10 +518,40 @@ int prefill_layer_simt(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidde
   return SSD200_OK;
 }
 
+// sum of the per-head-group partial sums of u^2 -> column `col` of a strided row
+__global__ void ssq_groups_kernel(const float *__restrict__ ssq, int ng, long rows,
+                                  float *__restrict__ dst, long ld, int col) {
+  const long r = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  float s = 0.f;
+  for (int g = 0; g < ng; ++g) s += ssq[r * ng + g];
+  dst[r * ld + col] = s;
+}
+
+// head-sharded residual update: hidden += partial * rsqrt(ssq / d_inner + eps)
+// (partial rows of width ld, ssq in column d_model), bf16 shadow (model.py:166-173)
+__global__ void resid_norm_finish_kernel(float *__restrict__ hidden, bf16 *__restrict__ lp,
+                                         const float *__restrict__ part, long ld, long rows,
+                                         int d_model, float inv_d, float eps) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * d_model) return;
+  const long r = i / d_model, n = i % d_model;
+  const float sc = rsqrtf(part[r * ld + d_model] * inv_d + eps);
+  const float v = hidden[i] + sc * part[r * ld + n];
+  hidden[i] = v;
+  lp[i] = __float2bfloat16_rn(v);
+}
+
+// partial != nullptr: head-group-sharded mode (no residual update; writes
+// partial[r, :d_model] = u_local . W_out'_local and partial[r, d_model] = sum u_local^2)
 int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hidden,
                        bf16 *hidden_lp, float *ssm_out, float *conv_out, int B, int Tn, void *ws,
-                       size_t ws_bytes, cudaStream_t st) {
+                       size_t ws_bytes, cudaStream_t st, float *partial = nullptr,
+                       long partial_ld = 0) {
   REQUIRE(hidden_lp, SSD200_EINVAL, "bf16 mode needs the hidden_lp shadow");
+  REQUIRE(!partial || tc_ssd_eligible(d), SSD200_EUNSUPPORTED,
+          "head-sharded prefill needs the tensor-core scan (P=64, N=128, L=256, G=1, local heads "
+          "a multiple of 8)");
   PrefillWs<float> o;
   size_t need = 0;
   REQUIRE(carve_prefill<float>(d, B, Tn, ws, ws_bytes, o, &need), SSD200_EWORKSPACE,
@@ -617,6 +647,18 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
     phase_mark(PH_NORM, 0, st);
     phase_mark(PH_NORM, 1, st);
     TcEpilogue er{};
+    phase_mark(PH_OUT_PROJ, 0, st);
+    if (partial) {  // this rank's share: unscaled partial + local sum u^2
+      ssq_groups_kernel<<<blocks_for(rows), 256, 0, st>>>(ssq, ng, rows, partial, partial_ld,
+                                                          d->d_model);
+      LAUNCH_CHECK("ssq_groups");
+      er.C = partial;
+      er.ldc = partial_ld;
+      rc = tc_gemm<TC_EPI_F32>(u_gated, d->d_inner, static_cast<const bf16 *>(w->W_out),
+                               d->d_inner, (int)rows, d->d_model, d->d_inner, er, st);
+      phase_mark(PH_OUT_PROJ, 1, st);
+      return rc;
+    }
     er.C = hidden;
     er.ldc = d->d_model;
     er.C_lp = hidden_lp;
@@ -624,7 +666,6 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
     er.ng = ng;
     er.inv_d = 1.f / (float)d->d_inner;
     er.eps = (float)d->norm_eps;
-    phase_mark(PH_OUT_PROJ, 0, st);
     rc = tc_gemm<TC_EPI_RESID_NORM>(u_gated, d->d_inner, static_cast<const bf16 *>(w->W_out),
                                     d->d_inner, (int)rows, d->d_model, d->d_inner, er, st);
     phase_mark(PH_OUT_PROJ, 1, st);
@@ -1128,6 +1169,36 @@ int ssd200_prefill_layer(const ssd200_dims_t *d, const ssd200_layer_t *w, void *
       return prefill_layer_bf16(d, w, (float *)hidden, (bf16 *)hidden_lp, (float *)ssm_out,
                                 (float *)conv_out, batch, seqlen, workspace, workspace_bytes, st);
   }
+}
+
+int ssd200_prefill_layer_partial(const ssd200_dims_t *d, const ssd200_layer_t *w,
+                                 const void *hidden_lp, float *partial, long partial_ld,
+                                 void *ssm_out, void *conv_out, int batch, int seqlen,
+                                 void *workspace, size_t workspace_bytes, ssd200_stream_t stream) {
+  int rc = check_dims(d);
+  if (rc) return rc;
+  REQUIRE(d->dtype == SSD200_BF16, SSD200_EUNSUPPORTED, "prefill_layer_partial: bf16 mode only");
+  REQUIRE(w && hidden_lp && partial && ssm_out && batch >= 1 && seqlen >= 1 &&
+              partial_ld >= d->d_model + 1 && partial_ld % 4 == 0,
+          SSD200_EINVAL, "prefill_layer_partial: bad arguments");
+  REQUIRE(d->conv_kernel == 1 || conv_out, SSD200_EINVAL, "prefill_layer_partial: conv_out is null");
+  return prefill_layer_bf16(d, w, nullptr, (bf16 *)const_cast<void *>(hidden_lp), (float *)ssm_out,
+                            (float *)conv_out, batch, seqlen, workspace, workspace_bytes,
+                            static_cast<cudaStream_t>(stream), partial, partial_ld);
+}
+
+int ssd200_resid_norm_finish(int d_model, int d_inner_full, double eps, void *hidden,
+                             void *hidden_lp, const float *partial, long partial_ld, long rows,
+                             ssd200_stream_t stream) {
+  REQUIRE(hidden && hidden_lp && partial && rows >= 1 && d_model >= 1 && d_inner_full >= 1 &&
+              partial_ld >= d_model + 1,
+          SSD200_EINVAL, "resid_norm_finish: bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  resid_norm_finish_kernel<<<blocks_for(rows * d_model), 256, 0, st>>>(
+      (float *)hidden, (bf16 *)hidden_lp, partial, partial_ld, rows, d_model,
+      1.f / (float)d_inner_full, (float)eps);
+  LAUNCH_CHECK("resid_norm_finish");
+  return SSD200_OK;
 }
 
 size_t ssd200_decode_layer_workspace(const ssd200_dims_t *d, int batch) {

@@ -112,3 +112,170 @@ def shard_layer_by_heads(layer, cfg: ModelConfig, rank: int, world: int) -> Simp
         heads=heads,
         dims=local_dims(cfg, heads),
     )
+
+
+# ------------------------------------------------------------------ head-group-sharded prefill
+
+
+def upload_shard(host, cfg: ModelConfig, rank: int, world: int, device="cuda"):
+    """bf16 device weights of this rank's head group (reference-layout host
+    weights in, e.g. ``random_init_host``).  The embedding and final norm are
+    replicated; every layer holds ``shard_layer_by_heads`` re-laid out like
+    ``params.from_reference`` (K-major bf16, norm_w folded into W_out)."""
+    from .params import LayerParams, ModelParams, decay_coefficient
+
+    if cfg.policy.compute != "bf16":
+        raise ValueError("head-group sharding runs the bf16 tensor-core path")
+    dev = torch.device(device)
+
+    def f32(x):
+        return torch.as_tensor(np.ascontiguousarray(np.asarray(x, dtype=np.float32))).to(dev)
+
+    def bf16_t(x):  # (K, N) host -> (N, K) bf16 device (K-major for the GEMMs)
+        t = torch.as_tensor(np.ascontiguousarray(np.asarray(x, dtype=np.float32)))
+        return t.t().to(torch.bfloat16).contiguous().to(dev)
+
+    layers, heads, dims = [], None, None
+    for lp in host.layers:
+        sh = shard_layer_by_heads(lp, cfg, rank, world)
+        heads, dims = sh.heads, sh.dims
+        w_out = sh.norm_w.astype(np.float32)[:, None] * sh.W_out.astype(np.float32)
+        layers.append(LayerParams(
+            W_in=bf16_t(sh.W_in), conv_w=f32(sh.conv_w), conv_b=f32(sh.conv_b),
+            dt_bias=f32(sh.dt_bias), A_log=f32(sh.A_log), D=f32(sh.D), norm_w=f32(sh.norm_w),
+            W_out=bf16_t(w_out), a=f32(decay_coefficient(sh.A_log, cfg)),
+        ))
+    emb = torch.as_tensor(np.asarray(host.embedding, dtype=np.float32)).to(torch.bfloat16).to(dev)
+    params = ModelParams(embedding=emb, layers=layers, final_norm_w=f32(host.final_norm_w),
+                         mode="bf16")
+    params.heads, params.local = heads, dims
+    return params
+
+
+def synthetic_shard(cfg: ModelConfig, rank: int, world: int, seed: int = 0, device="cuda"):
+    """Throughput-only device weights of one head shard (the distributions of
+    ``params.synthetic_init``), for benchmarking head-group sharding at sizes
+    where a host init would take minutes."""
+    from .params import LayerParams, ModelParams, decay_coefficient
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    dev = torch.device(device)
+    heads = head_slice(cfg.n_heads, rank, world)
+    loc = local_dims(cfg, heads)
+
+    def normal(shape, std=0.02):
+        return (torch.randn(shape, generator=g, device=dev) * std).to(torch.bfloat16).contiguous()
+
+    def uniform(shape, lo, hi):
+        return torch.rand(shape, generator=g, device=dev, dtype=torch.float64) * (hi - lo) + lo
+
+    bound = 1.0 / np.sqrt(cfg.conv_kernel)
+    layers = []
+    for _ in range(cfg.n_layers):
+        dt = uniform((loc.n_heads,), 1e-3, 1e-1)
+        a_log = torch.log(uniform((loc.n_heads,), 1.0, 16.0)).to(torch.float32)
+        layers.append(LayerParams(
+            W_in=normal((loc.d_in_proj, cfg.d_model)),
+            conv_w=uniform((loc.conv_dim, cfg.conv_kernel), -bound, bound).float(),
+            conv_b=torch.zeros(loc.conv_dim, device=dev),
+            dt_bias=torch.log(torch.expm1(dt)).float(),
+            A_log=a_log,
+            D=torch.randn(loc.n_heads, generator=g, device=dev),
+            norm_w=torch.ones(loc.d_inner, device=dev),
+            W_out=normal((cfg.d_model, loc.d_inner)),
+            a=torch.as_tensor(decay_coefficient(a_log.cpu().numpy(), cfg),
+                              dtype=torch.float32).to(dev),
+        ))
+    params = ModelParams(embedding=normal((cfg.vocab_size, cfg.d_model)), layers=layers,
+                         final_norm_w=torch.ones(cfg.d_model, device=dev), mode="bf16")
+    params.heads, params.local = heads, loc
+    return params
+
+
+def _local_dims_struct(cfg: ModelConfig, local):
+    from .model import dims_struct
+
+    d = dims_struct(cfg)
+    d.d_inner = local.d_inner
+    d.n_heads = local.n_heads
+    return d
+
+
+class HeadShardedPrefill:
+    """One rank's side of a head-group-sharded ``prefill`` (model.py:177-206),
+    driven layer by layer: ``partial(i)`` runs this rank's heads of layer i
+    (in_proj / conv / SSD / gate / partial out_proj) into ``self.buf`` =
+    ``[partial (rows, d_model) | sum u^2]``; the caller sums ``buf`` over the
+    ranks (one all-reduce) and calls ``finish()``; ``logits()`` runs the
+    replicated final norm + tied head on the last position."""
+
+    def __init__(self, shard_params, tokens, cfg: ModelConfig):
+        from .model import _Runner, check_tokens, layer_struct
+
+        self.cfg, self.params = cfg, shard_params
+        self.r = r = _Runner(shard_params, cfg)
+        tok = check_tokens(tokens, cfg, 2, r.dev)
+        self.B, self.T = tok.shape
+        self.rows = self.B * self.T
+        local = shard_params.local
+        self.dims_l = _local_dims_struct(cfg, local)
+        self.layers = [layer_struct(lp) for lp in shard_params.layers]
+        self.hidden, self.lp = r.embed(tok.reshape(-1))
+        self.ld = (cfg.d_model + 4) // 4 * 4  # 16-byte rows: [partial | sum u^2 | pad]
+        self.buf = torch.empty((self.rows, self.ld), dtype=torch.float32, device=r.dev)
+        self.ssm = torch.empty((cfg.n_layers, self.B, local.n_heads, cfg.head_dim, cfg.d_state),
+                               dtype=torch.float32, device=r.dev)
+        self.conv = torch.empty((cfg.n_layers, self.B, local.conv_dim, cfg.conv_kernel - 1),
+                                dtype=torch.float32, device=r.dev)
+        self.ws = r.workspace(r.lib.ssd200_prefill_layer_workspace(self.dims_l, self.B, self.T))
+
+    def partial(self, i: int) -> torch.Tensor:
+        from . import _abi
+
+        r = self.r
+        _abi.check(
+            r.lib.ssd200_prefill_layer_partial(
+                self.dims_l, self.layers[i], self.lp.data_ptr(), self.buf.data_ptr(), self.ld,
+                self.ssm[i].data_ptr(), self.conv[i].data_ptr() if self.conv.numel() else None,
+                self.B, self.T, self.ws.data_ptr(), self.ws.numel(), r.stream,
+            ),
+            "ssd200_prefill_layer_partial",
+        )
+        return self.buf
+
+    def finish(self):
+        from . import _abi
+
+        cfg, r = self.cfg, self.r
+        _abi.check(
+            r.lib.ssd200_resid_norm_finish(
+                cfg.d_model, cfg.d_inner, float(cfg.norm_eps), self.hidden.data_ptr(),
+                self.lp.data_ptr(), self.buf.data_ptr(), self.ld, self.rows, r.stream,
+            ),
+            "ssd200_resid_norm_finish",
+        )
+
+    def logits(self) -> torch.Tensor:
+        cfg = self.cfg
+        out = torch.empty((self.B, cfg.vocab_size), dtype=torch.float32, device=self.r.dev)
+        self.r.head(self.hidden, self.T * cfg.d_model, self.B, logits=out,
+                    base_offset=(self.T - 1) * cfg.d_model)
+        return out
+
+
+def prefill_head_sharded(shard_params, tokens, cfg: ModelConfig, group=None):
+    """Head-group-sharded ``prefill`` for this rank: every rank holds
+    ``upload_shard(...)`` of its heads and the same tokens; per layer ONE
+    all-reduce (sum) of ``[partial | sum u^2]`` over ``group`` (NCCL on the
+    GPU path) after the head-sharded out_proj.  Returns the last-position
+    logits (B, V) (replicated) and this rank's final SSM states
+    (n_layers, B, H_local, P, N)."""
+    import torch.distributed as dist
+
+    run = HeadShardedPrefill(shard_params, tokens, cfg)
+    for i in range(cfg.n_layers):
+        buf = run.partial(i)
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+        run.finish()
+    return run.logits(), run.ssm

@@ -352,3 +352,42 @@ def test_bf16_decode_vs_oracle():
         ref_full = orc.prefill(orc.round_weights_bf16(host), toks, cfg.with_policy(compute="f32"))[0][:, -1]
         rel = np.linalg.norm(_np(sl) - ref_full) / np.linalg.norm(ref_full)
         assert rel <= BF16_BOUND, (B, rel)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_bf16_head_sharded_prefill_matches_unsharded(world):
+    """Head-group sharding: each simulated rank computes its
+    heads and a partial out_proj; the partials + sums of u^2 are summed (the
+    all-reduce) and finished.  Equals the unsharded bf16 prefill up to the
+    summation order, and each rank's final states are its heads' slice."""
+    import paper_2603_09555_b200 as m
+    from paper_2603_09555_b200 import shard
+
+    d_model = 256 * world  # 8 heads of 64 per rank
+    cfg = m.ModelConfig(vocab_size=1024, d_model=d_model, n_layers=2, norm_eps=1e-5).with_policy(
+        compute="bf16")
+    host = m.random_init_host(cfg, 21)
+    rng = np.random.default_rng(4)
+    for lp in host.layers:  # non-unit norm weights exercise the norm_w folding
+        lp.norm_w = (1.0 + 0.2 * rng.standard_normal(cfg.d_inner)).astype(np.float32)
+    tok = rng.integers(0, cfg.vocab_size, size=(2, 300))
+    full = m.from_reference(host, cfg)
+    ref, cache = m.prefill(full, tok, cfg, logits="last")
+    runs = [shard.HeadShardedPrefill(shard.upload_shard(host, cfg, r, world), tok, cfg)
+            for r in range(world)]
+    for i in range(cfg.n_layers):
+        total = sum(run.partial(i).clone() for run in runs)  # the all-reduce
+        for run in runs:
+            run.buf.copy_(total)
+            run.finish()
+    got = runs[0].logits()
+    for run in runs[1:]:
+        assert torch.equal(run.logits(), got)  # replicated after the reduce
+    rel = (torch.linalg.norm(got - ref) / torch.linalg.norm(ref)).item()
+    assert rel <= BF16_BOUND, rel
+    for r, run in enumerate(runs):
+        hs = shard.head_slice(cfg.n_heads, r, world)
+        for i in range(cfg.n_layers):
+            a, b = run.ssm[i], cache.ssm_all[i][:, hs].float()
+            assert (torch.linalg.norm(a - b) / torch.linalg.norm(b)).item() <= BF16_BOUND
