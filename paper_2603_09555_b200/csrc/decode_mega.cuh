@@ -245,32 +245,56 @@ __global__ void __launch_bounds__(MEGA_THREADS, 1) decode_mega(MegaArgs a) {
             a.trace[6600 + cstage] = gtimer();
         }
         if (ok) {
-          // 4 chunks of loads in flight, 4 independent accumulators per batch row
-          float acc[BT][4];
+          // U chunks of loads in flight (fewer for wide batches: registers), W
+          // unpacked once per chunk and reused by every batch row
+          constexpr int U = BT <= 2 ? 4 : (BT == 4 ? 2 : 1);
+          float acc[BT][U];
 #pragma unroll
           for (int b = 0; b < BT; ++b)
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc[b][u] = 0.f;
+            for (int u = 0; u < U; ++u) acc[b][u] = 0.f;
           const uint4 *wr = reinterpret_cast<const uint4 *>(stage + (size_t)rr * K * 2) + lane;
           const uint4 *xr = reinterpret_cast<const uint4 *>(xs) + lane;
           const int kq = K / 8;  // uint4 per row
-          for (int c0 = 0; c0 < kchunks; c0 += 4) {
-            uint4 w[4];
+          for (int c0 = 0; c0 < kchunks; c0 += U) {
+            uint4 w[U];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < U; ++u)
               if (c0 + u < kchunks) w[u] = wr[(c0 + u) * 32];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < U; ++u)
               if (c0 + u < kchunks) {
+                float wf[8];
+                const __nv_bfloat162 *wp = reinterpret_cast<const __nv_bfloat162 *>(&w[u]);
 #pragma unroll
-                for (int b = 0; b < BT; ++b)
-                  acc[b][u] += dot8(w[u], xr[(size_t)b * kq + (c0 + u) * 32]);
+                for (int j = 0; j < 4; ++j) {
+                  const float2 f = __bfloat1622float2(wp[j]);
+                  wf[2 * j] = f.x;
+                  wf[2 * j + 1] = f.y;
+                }
+#pragma unroll
+                for (int b = 0; b < BT; ++b) {
+                  const uint4 xv = xr[(size_t)b * kq + (c0 + u) * 32];
+                  const __nv_bfloat162 *xp = reinterpret_cast<const __nv_bfloat162 *>(&xv);
+                  float t = acc[b][u];
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    const float2 f = __bfloat1622float2(xp[j]);
+                    t = fmaf(wf[2 * j], f.x, t);
+                    t = fmaf(wf[2 * j + 1], f.y, t);
+                  }
+                  acc[b][u] = t;
+                }
               }
           }
+#pragma unroll
+          for (int b = 0; b < BT; ++b)
+#pragma unroll
+            for (int u = 1; u < U; ++u) acc[b][0] += acc[b][u];
           float v = 0.f;
 #pragma unroll
           for (int b = 0; b < BT; ++b) {
-            const float t = warp_sum((acc[b][0] + acc[b][1]) + (acc[b][2] + acc[b][3]));
+            const float t = warp_sum(acc[b][0]);
             if (lane == b) v = t;
           }
           if (lane < B) epi(n, lane, v, e);
