@@ -735,6 +735,9 @@ bool carve_decode(const ssd200_dims_t *d, int B, void *ws, size_t cap, DecodeWs<
 }
 
 constexpr int GEMV_MAX_ROWS = 16;
+// bf16: beyond the streaming-GEMV batch sizes the tensor-core GEMM wins (measured
+// at B = 16: SIMT gemv_nk 315 us vs tc_gemm ~80 us for the 1.3B in_proj)
+constexpr int GEMV_BF16_MAX_ROWS = 8;
 
 // launch with programmatic stream serialization (PDL): the kernel may start
 // while its predecessor drains; it waits (griddepcontrol.wait) before reading
@@ -888,7 +891,7 @@ int decode_layer_impl(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidden
   if (lp) {
     REQUIRE(hidden_lp, SSD200_EINVAL, "bf16 mode needs the hidden_lp shadow");
     const bf16 *Win = static_cast<const bf16 *>(w->W_in);
-    if (B <= GEMV_MAX_ROWS) {
+    if (B <= GEMV_BF16_MAX_ROWS) {
       gemv_nk<float, bf16, bf16, EPI_STORE>
           <<<dim3(blocks_for(wd.d_in_proj, 32), blocks_for(B, 4)), 256, 0, st>>>(
               hidden_lp, d->d_model, Win, d->d_model, (float *)o.u, wd.d_in_proj, nullptr, B,
@@ -937,7 +940,7 @@ int decode_layer_impl(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidden
         (float)d->norm_eps);
     LAUNCH_CHECK("gated_norm (decode)");
     const bf16 *Wout = static_cast<const bf16 *>(w->W_out);
-    if (B <= GEMV_MAX_ROWS) {
+    if (B <= GEMV_BF16_MAX_ROWS) {
       gemv_nk<float, bf16, bf16, EPI_ADD>
           <<<dim3(blocks_for(d->d_model, 32), blocks_for(B, 4)), 256, 0, st>>>(
               o.normed_lp, d->d_inner, Wout, d->d_inner, (float *)hidden, d->d_model, hidden_lp,
