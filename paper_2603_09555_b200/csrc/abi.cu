@@ -179,7 +179,10 @@ int tc_gemm(const bf16 *A, long lda, const bf16 *B, long ldb, int M, int N, int 
             const TcEpilogue &ep, cudaStream_t st) {
   REQUIRE(M > 0 && N > 0 && K > 0, SSD200_EINVAL, "tc_gemm: empty problem");
   REQUIRE(K % 8 == 0, SSD200_EINVAL, "tc_gemm: K must be a multiple of 8");
-  if (N <= 128) return launch_tc_gemm_bn<128, EPI>(A, lda, B, ldb, M, N, K, ep, st);
+  // 128-wide tiles when 256-wide ones would leave SMs idle (few row tiles: decode batches)
+  const long tiles256 = (long)((M + 127) / 128) * ((N + 255) / 256);
+  if (N <= 128 || (EPI == TC_EPI_F32 && tiles256 < num_sms()))
+    return launch_tc_gemm_bn<128, EPI>(A, lda, B, ldb, M, N, K, ep, st);
   return launch_tc_gemm_bn<256, EPI>(A, lda, B, ldb, M, N, K, ep, st);
 }
 
