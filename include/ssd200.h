@@ -166,7 +166,9 @@ int ssd200_debug_trace(void *device_buffer);
 /* Implementation choices (thread-local): option 1 = conv1d+SiLU fused into
  * the in_proj GEMM epilogue (1) instead of the separate conv kernel (0, default);
  * option 2 = force the fused chunk-state + inter-chunk pass scan kernel
- * (default: when batch * heads fills the GPU). */
+ * (default: when batch * heads fills the GPU); option 3 = share each chunk's
+ * B tile across 4-CTA clusters by TMA multicast in that kernel (1, default)
+ * or load it per CTA (0). */
 int ssd200_set_option(int option, int value);
 
 #ifdef __cplusplus

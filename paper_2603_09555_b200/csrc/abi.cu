@@ -28,6 +28,7 @@ thread_local int g_nphase = 0;
 thread_local void *g_mega_trace = nullptr;  // debug: device buffer of >= 8192 u64
 thread_local int g_force_fused_conv = 0;  // option 1: 1 = fused-conv in_proj epilogue (else separate)
 thread_local bool g_force_chunkscan = false;   // tests: exercise the fused state+pass scan
+thread_local bool g_chunkscan_mc = true;       // option 3: B-tile multicast in the chunk scan
 
 enum { PH_IN_PROJ = 0, PH_CONV = 1, PH_SCAN = 2, PH_NORM = 3, PH_OUT_PROJ = 4 };
 
@@ -394,7 +395,22 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
   LAUNCH_CHECK("ssd_tc_cumsum");
   if ((long)B * H >= (sms * 3) / 4 || g_force_chunkscan) {
     // chunk states + inter-chunk pass fused: one CTA per (b, h), chunks in order
-    ssd_tc_chunkscan<<<B * H, 192, ScanSmem::TOTAL, st>>>(tm_act, a);
+    // clusters of 4 heads of one batch row share each chunk's B tile by multicast
+    const int mc = (H % 4 == 0 && g_chunkscan_mc) ? 4 : 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(B * H);
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = ScanSmem::TOTAL;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = mc;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, ssd_tc_chunkscan, tm_act, a, mc);
+    REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "ssd_tc_chunkscan: %s", cudaGetErrorString(e));
     LAUNCH_CHECK("ssd_tc_chunkscan");
   } else {
     // few (b, h) pairs: parallel chunk states, then the O(Nc) pass
@@ -1430,6 +1446,9 @@ int ssd200_set_option(int option, int value) {
       return SSD200_OK;
     case 2:  // force the fused chunk-state + pass scan kernel (else size-based)
       g_force_chunkscan = value != 0;
+      return SSD200_OK;
+    case 3:  // chunk scan: share each chunk's B tile across 4-CTA clusters by TMA multicast
+      g_chunkscan_mc = value != 0;
       return SSD200_OK;
     default:
       set_err("unknown option %d", option);

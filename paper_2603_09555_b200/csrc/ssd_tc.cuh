@@ -352,8 +352,11 @@ struct ScanSmem {
   static constexpr uint32_t TOTAL = BAR + 256 + 1024;
 };
 
+// mc = CTAs per cluster (1 or 4): the heads h..h+3 of one batch row share every
+// chunk's B tile, so with mc = 4 each CTA loads a quarter of it and multicasts it
+// to the cluster (and a stage is refilled only once all four have consumed it).
 __global__ void __launch_bounds__(192, 1)
-    ssd_tc_chunkscan(const __grid_constant__ CUtensorMap tm_act, TcSsdArgs p) {
+    ssd_tc_chunkscan(const __grid_constant__ CUtensorMap tm_act, TcSsdArgs p, int mc) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t *sm = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t *full = reinterpret_cast<uint64_t *>(sm + ScanSmem::BAR);  // [2] TMA landed
@@ -372,7 +375,7 @@ __global__ void __launch_bounds__(192, 1)
       sm100::mbar_init(&full[i], 1);
       sm100::mbar_init(&xsd[i], 128);
       sm100::mbar_init(&sfull[i], 1);
-      sm100::mbar_init(&stfree[i], 1);
+      sm100::mbar_init(&stfree[i], mc);  // every CTA of the cluster frees the stage
       sm100::mbar_init(&tfree[i], 128);
     }
     sm100::fence_barrier_init();
@@ -380,8 +383,11 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) sm100::tmem_alloc<128>(tslot);
   sm100::tc_fence_before();
   __syncthreads();
+  if (mc > 1) sm100::cluster_sync();  // barriers initialised cluster-wide before any multicast
   sm100::tc_fence_after();
   const uint32_t tmem = *tslot;
+  const uint16_t mask = (uint16_t)((1u << mc) - 1u);
+  const int crank = mc > 1 ? (int)sm100::cluster_rank() : 0;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -389,11 +395,18 @@ __global__ void __launch_bounds__(192, 1)
         const int st = c & 1;
         uint8_t *stg = sm + st * ScanSmem::STG;
         sm100::mbar_wait(&stfree[st], ((c >> 1) & 1) ^ 1);
+        if (p.trace && blockIdx.x == 0 && c < 64) p.trace[4096 + c * 8 + 0] = clk64();
         sm100::mbar_arrive_expect_tx(&full[st], ScanSmem::STG);
-        for (int j = 0; j < 2; ++j)
-          for (int q = 0; q < 2; ++q)
-            sm100::tma_load_3d(stg + j * 32768 + q * 16384, &tm_act, &full[st],
-                               p.d_inner + j * 64, c * TC_L + q * 128, b);
+        if (mc == 4) {  // this CTA's quarter of B, to all four CTAs
+          const int j = crank >> 1, q = crank & 1;
+          sm100::tma_load_3d_mc(stg + j * 32768 + q * 16384, &tm_act, &full[st],
+                                p.d_inner + j * 64, c * TC_L + q * 128, b, mask);
+        } else {
+          for (int j = 0; j < 2; ++j)
+            for (int q = 0; q < 2; ++q)
+              sm100::tma_load_3d(stg + j * 32768 + q * 16384, &tm_act, &full[st],
+                                 p.d_inner + j * 64, c * TC_L + q * 128, b);
+        }
         for (int q = 0; q < 2; ++q)
           sm100::tma_load_3d(stg + ScanSmem::XO + q * 16384, &tm_act, &full[st], h * TC_P,
                              c * TC_L + q * 128, b);
@@ -406,7 +419,9 @@ __global__ void __launch_bounds__(192, 1)
         const int st = c & 1;
         const uint32_t par = (c >> 1) & 1;
         sm100::mbar_wait(&xsd[st], par);
+        if (p.trace && blockIdx.x == 0 && c < 64) p.trace[4096 + c * 8 + 1] = clk64();
         sm100::mbar_wait(&tfree[st], par ^ 1);
+        if (p.trace && blockIdx.x == 0 && c < 64) p.trace[4096 + c * 8 + 2] = clk64();
         sm100::tc_fence_after();
         const uint32_t a0 = sm100::smem_u32(sm + st * ScanSmem::STG);
         const uint32_t x0 = a0 + ScanSmem::XO;
@@ -417,7 +432,10 @@ __global__ void __launch_bounds__(192, 1)
           sm100::mma_bf16(tmem + st * TC_P, ad, bd, idesc, k > 0);
         }
         sm100::mma_commit(&sfull[st]);
-        sm100::mma_commit(&stfree[st]);
+        if (mc > 1)
+          sm100::mma_commit_mc(&stfree[st], mask);  // the stage may be refilled cluster-wide
+        else
+          sm100::mma_commit(&stfree[st]);
       }
     }
   } else {
@@ -445,6 +463,7 @@ __global__ void __launch_bounds__(192, 1)
     auto scale = [&](int c, const RowW &f) {
       const int st = c & 1;
       sm100::mbar_wait(&full[st], (c >> 1) & 1);
+      if (p.trace && blockIdx.x == 0 && tid == 0 && c < 64) p.trace[4096 + c * 8 + 3] = clk64();
       uint8_t *xb = sm + st * ScanSmem::STG + ScanSmem::XO;
 #pragma unroll
       for (int rr = 0; rr < 2; ++rr) {
@@ -454,15 +473,19 @@ __global__ void __launch_bounds__(192, 1)
         uint4 *row = reinterpret_cast<uint4 *>(xb + l * 128);
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch) {  // packed bf16 multiply (X is a bf16 MMA operand)
-          uint4 v = row[ch];
+          // every 16-byte chunk of the row gets the same weight, so visit them in a
+          // lane-rotated order: the 8 lanes of a shared-memory phase hit 8 banks groups
+          const int pc = (ch + l) & 7;
+          uint4 v = row[pc];
           __nv_bfloat162 *e = reinterpret_cast<__nv_bfloat162 *>(&v);
 #pragma unroll
           for (int j = 0; j < 4; ++j) e[j] = __hmul2(e[j], w2);
-          row[ch] = v;
+          row[pc] = v;
         }
       }
       sm100::fence_proxy_async();
       sm100::mbar_arrive(&xsd[st]);
+      if (p.trace && blockIdx.x == 0 && tid == 0 && c < 64) p.trace[4096 + c * 8 + 4] = clk64();
     };
     float s[TC_P];
     const long sbase = ((long)b * p.H + h) * TC_P * TC_N + n;
@@ -488,6 +511,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       const int st = c & 1;
       sm100::mbar_wait(&sfull[st], (c >> 1) & 1);
+      if (p.trace && blockIdx.x == 0 && tid == 0 && c < 64) p.trace[4096 + c * 8 + 5] = clk64();
       sm100::tc_fence_after();
       uint32_t r0[32], r1[32];
       const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + st * TC_P;
@@ -515,11 +539,13 @@ __global__ void __launch_bounds__(192, 1)
         s[pp] = decay * s[pp] + __uint_as_float(r0[pp]);
         s[pp + 32] = decay * s[pp + 32] + __uint_as_float(r1[pp]);
       }
+      if (p.trace && blockIdx.x == 0 && tid == 0 && c < 64) p.trace[4096 + c * 8 + 6] = clk64();
     }
 #pragma unroll
     for (int pp = 0; pp < TC_P; ++pp) p.final_state[sbase + (long)pp * TC_N] = s[pp];
   }
   __syncthreads();
+  if (mc > 1) sm100::cluster_sync();  // no CTA leaves while peers may still signal it
   if (warp == 1) {
     __syncwarp();
     sm100::tc_fence_after();
