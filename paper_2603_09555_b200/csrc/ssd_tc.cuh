@@ -171,8 +171,7 @@ struct StateSmem {
 __global__ void __launch_bounds__(192, 1)
     ssd_tc_state(const __grid_constant__ CUtensorMap tm_act, TcSsdArgs p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                            ~(uintptr_t)1023);
+  uint8_t *sm = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t *bar_b = reinterpret_cast<uint64_t *>(sm + StateSmem::BAR);
   uint64_t *bar_x = bar_b + 1;     // [2] TMA X landed
   uint64_t *bar_xs = bar_b + 3;    // [2] X scaled by math
@@ -263,14 +262,15 @@ __global__ void __launch_bounds__(192, 1)
         uint4 *row = reinterpret_cast<uint4 *>(xb + l * 128);
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch) {
-          uint4 v = row[ch];
+          const int pc = (ch + l) & 7;  // lane-rotated chunk order: conflict-free phases
+          uint4 v = row[pc];
           __nv_bfloat162 *e = reinterpret_cast<__nv_bfloat162 *>(&v);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             float2 f = __bfloat1622float2(e[j]);
             e[j] = __floats2bfloat162_rn(f.x * w, f.y * w);
           }
-          row[ch] = v;
+          row[pc] = v;
         }
       }
       sm100::fence_proxy_async();

@@ -178,8 +178,9 @@ __global__ void __launch_bounds__(320, 1)
   using Cfg = TcCfg<BN>;
   constexpr int BM = Cfg::BM, BK = Cfg::BK, STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  // 1024-byte aligned, derived from smem_raw by an offset so that the compiler
+  // keeps the shared address space (LDS/STS rather than generic loads)
+  uint8_t *smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sA = smem;
   uint8_t *sB = smem + STAGES * Cfg::A_BYTES;
   uint32_t *sX = reinterpret_cast<uint32_t *>(sB + STAGES * Cfg::B_BYTES);  // transpose buffers
