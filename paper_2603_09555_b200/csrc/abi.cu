@@ -29,6 +29,7 @@ thread_local void *g_mega_trace = nullptr;  // debug: device buffer of >= 8192 u
 thread_local int g_force_fused_conv = 0;  // option 1: 1 = fused-conv in_proj epilogue (else separate)
 thread_local bool g_force_chunkscan = false;   // tests: exercise the fused state+pass scan
 thread_local bool g_chunkscan_mc = true;       // option 3: B-tile multicast in the chunk scan
+thread_local int g_out_waves = 1;              // option 4: target CTAs (x SMs) of the output kernel
 
 enum { PH_IN_PROJ = 0, PH_CONV = 1, PH_SCAN = 2, PH_NORM = 3, PH_OUT_PROJ = 4 };
 
@@ -422,7 +423,7 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
     LAUNCH_CHECK("ssd_tc_pass");
   }
   // outputs (+ D skip + gate)
-  a.NG = pick_groups(H, (long)B * a.Nc * 2, 2 * sms, OutSmem::MAX_HG);
+  a.NG = pick_groups(H, (long)B * a.Nc * 2, g_out_waves * sms, OutSmem::MAX_HG);
   a.HG = H / a.NG;
   ssd_tc_out<<<B * a.Nc * 2 * a.NG, OUT_THREADS, OutSmem::TOTAL, st>>>(tm_act, tm_prev, tm_z,
                                                                         tm_u, a);
@@ -1449,6 +1450,10 @@ int ssd200_set_option(int option, int value) {
       return SSD200_OK;
     case 3:  // chunk scan: share each chunk's B tile across 4-CTA clusters by TMA multicast
       g_chunkscan_mc = value != 0;
+      return SSD200_OK;
+    case 4:  // output kernel: split heads into groups until >= value x SMs CTAs exist
+      REQUIRE(value >= 1 && value <= 64, SSD200_EINVAL, "option 4 out of range");
+      g_out_waves = value;
       return SSD200_OK;
     default:
       set_err("unknown option %d", option);
