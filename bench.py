@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--shard", default="batch", choices=("batch", "heads"),
                     help="N>1 prefill: batch rows per rank (weak scaling, default) or SSD head "
                          "groups of one batch with an all-reduce after out_proj (strong scaling)")
+    ap.add_argument("--opt", action="append", default=[],
+                    help="library implementation option k=v (ssd200_set_option), repeatable")
     ap.add_argument("--fused-conv", default="auto", choices=("auto", "on", "off"),
                     help="conv1d fused into the in_proj epilogue (default: by width)")
     return ap.parse_args()
@@ -300,6 +302,9 @@ def run_prefill(args, rank, world, local):
     dev_tok = host_tok.cuda()
     lib = _abi.lib()
     lib.ssd200_set_option(1, {"auto": 0, "on": 1, "off": 0}[args.fused_conv])
+    for kv in args.opt:
+        k, v = kv.split("=")
+        lib.ssd200_set_option(int(k), int(v))
 
     # per-phase CUDA events around every layer's phases (5 phases x 2)
     L = cfg.n_layers

@@ -168,7 +168,9 @@ int ssd200_debug_trace(void *device_buffer);
  * option 2 = force the fused chunk-state + inter-chunk pass scan kernel
  * (default: when batch * heads fills the GPU); option 3 = share each chunk's
  * B tile across 4-CTA clusters by TMA multicast in that kernel (1, default)
- * or load it per CTA (0). */
+ * or load it per CTA (0); option 4 = output-kernel CTA target in multiples of
+ * the SM count (head-group split, default 1); option 5 = programmatic
+ * dependent launch between the prefill kernels (0 default, 1 on). */
 int ssd200_set_option(int option, int value);
 
 #ifdef __cplusplus

@@ -30,6 +30,7 @@ thread_local int g_force_fused_conv = 0;  // option 1: 1 = fused-conv in_proj ep
 thread_local bool g_force_chunkscan = false;   // tests: exercise the fused state+pass scan
 thread_local bool g_chunkscan_mc = true;       // option 3: B-tile multicast in the chunk scan
 thread_local int g_out_waves = 1;              // option 4: target CTAs (x SMs) of the output kernel
+thread_local bool g_use_pdl = false;           // option 5: programmatic dependent launch (measured neutral on the prefill chain; off)
 
 enum { PH_IN_PROJ = 0, PH_CONV = 1, PH_SCAN = 2, PH_NORM = 3, PH_OUT_PROJ = 4 };
 
@@ -153,6 +154,25 @@ int make_map_2d_plain(CUtensorMap *m, const void *ptr, long rows, long cols, lon
   return SSD200_OK;
 }
 
+// launch with programmatic stream serialization (PDL): the kernel may start
+// while its predecessor drains; it waits (griddepcontrol.wait) before reading
+// the predecessor's outputs.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_use_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 template <int BN, int EPI>
 int launch_tc_gemm_bn(const bf16 *A, long lda, const bf16 *B, long ldb, int M, int N, int K,
                       const TcEpilogue &ep, cudaStream_t st) {
@@ -170,7 +190,9 @@ int launch_tc_gemm_bn(const bf16 *A, long lda, const bf16 *B, long ldb, int M, i
   }
   const int tiles = ((M + Cfg::BM - 1) / Cfg::BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  tc_gemm_kernel<BN, EPI><<<grid, 320, Cfg::SMEM, st>>>(ta, tb, M, N, K, ep);
+  cudaError_t e = launch_pdl(tc_gemm_kernel<BN, EPI>, dim3(grid), dim3(320), Cfg::SMEM, st, ta,
+                             tb, M, N, K, ep);
+  REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "tc_gemm_kernel: %s", cudaGetErrorString(e));
   LAUNCH_CHECK("tc_gemm_kernel");
   return SSD200_OK;
 }
@@ -392,7 +414,9 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
   if (rc) return rc;
   const long sms = num_sms();
   // chunk cumsums
-  ssd_tc_cumsum<<<dim3(B * a.Nc, (H + 7) / 8), 256, 0, st>>>(a);
+  REQUIRE(launch_pdl(ssd_tc_cumsum, dim3(B * a.Nc, (H + 7) / 8), dim3(256), 0, st, a) ==
+              cudaSuccess,
+          SSD200_ELAUNCH, "ssd_tc_cumsum launch");
   LAUNCH_CHECK("ssd_tc_cumsum");
   if ((long)B * H >= (sms * 3) / 4 || g_force_chunkscan) {
     // chunk states + inter-chunk pass fused: one CTA per (b, h), chunks in order
@@ -403,13 +427,15 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
     cfg.blockDim = dim3(192);
     cfg.dynamicSmemBytes = ScanSmem::TOTAL;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = mc;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = g_use_pdl ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaError_t e = cudaLaunchKernelEx(&cfg, ssd_tc_chunkscan, tm_act, a, mc);
     REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "ssd_tc_chunkscan: %s", cudaGetErrorString(e));
     LAUNCH_CHECK("ssd_tc_chunkscan");
@@ -417,16 +443,21 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
     // few (b, h) pairs: parallel chunk states, then the O(Nc) pass
     a.NG = pick_groups(H, (long)B * a.Nc, 2 * sms);
     a.HG = H / a.NG;
-    ssd_tc_state<<<B * a.Nc * a.NG, 192, StateSmem::TOTAL, st>>>(tm_act, a);
+    REQUIRE(launch_pdl(ssd_tc_state, dim3(B * a.Nc * a.NG), dim3(192), StateSmem::TOTAL, st,
+                       tm_act, a) == cudaSuccess,
+            SSD200_ELAUNCH, "ssd_tc_state launch");
     LAUNCH_CHECK("ssd_tc_state");
-    ssd_tc_pass<<<dim3(B * H, TC_P * TC_N / 256), 256, 0, st>>>(a);
+    REQUIRE(launch_pdl(ssd_tc_pass, dim3(B * H, TC_P * TC_N / 256), dim3(256), 0, st, a) ==
+                cudaSuccess,
+            SSD200_ELAUNCH, "ssd_tc_pass launch");
     LAUNCH_CHECK("ssd_tc_pass");
   }
   // outputs (+ D skip + gate)
   a.NG = pick_groups(H, (long)B * a.Nc * 2, g_out_waves * sms, OutSmem::MAX_HG);
   a.HG = H / a.NG;
-  ssd_tc_out<<<B * a.Nc * 2 * a.NG, OUT_THREADS, OutSmem::TOTAL, st>>>(tm_act, tm_prev, tm_z,
-                                                                        tm_u, a);
+  REQUIRE(launch_pdl(ssd_tc_out, dim3(B * a.Nc * 2 * a.NG), dim3(OUT_THREADS), OutSmem::TOTAL, st,
+                     tm_act, tm_prev, tm_z, tm_u, a) == cudaSuccess,
+          SSD200_ELAUNCH, "ssd_tc_out launch");
   LAUNCH_CHECK("ssd_tc_out");
   *ng_out = a.NG;
   return SSD200_OK;
@@ -628,8 +659,11 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
   }
   if (!fuse_conv) {
     if (k > 1) {
-      conv_tail_kernel<float, bf16><<<blocks_for((long)B * wd.conv_dim * (k - 1)), 256, 0, st>>>(
-          u + d->d_inner, n_split, conv_out, B, Tn, (int)wd.conv_dim, k);
+      REQUIRE(launch_pdl(conv_tail_kernel<float, bf16>,
+                         dim3(blocks_for((long)B * wd.conv_dim * (k - 1))), dim3(256), 0, st,
+                         (const bf16 *)(u + d->d_inner), (long)n_split, conv_out, B, Tn,
+                         (int)wd.conv_dim, k) == cudaSuccess,
+              SSD200_ELAUNCH, "conv_tail launch");
       LAUNCH_CHECK("conv_tail");
     }
     if (k == 4 && n_split % 8 == 0 && d->d_inner % 8 == 0) {
@@ -638,10 +672,12 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
       rc = make_map_2d_plain(&tmx, u + d->d_inner, rows, wd.conv_dim, n_split, CONV_COLS,
                              CONV_ROWS + 3);
       if (rc) return rc;
-      conv_silu_tma<<<dim3(blocks_for(wd.conv_dim, CONV_COLS), blocks_for(rows, CONV_ROWS)), 256,
-                      0, st>>>(tmx, static_cast<const float *>(w->conv_w),
-                               static_cast<const float *>(w->conv_b), act, wd.conv_dim, Tn,
-                               (int)wd.conv_dim, rows);
+      REQUIRE(launch_pdl(conv_silu_tma,
+                         dim3(blocks_for(wd.conv_dim, CONV_COLS), blocks_for(rows, CONV_ROWS)),
+                         dim3(256), 0, st, tmx, static_cast<const float *>(w->conv_w),
+                         static_cast<const float *>(w->conv_b), act, (long)wd.conv_dim, Tn,
+                         (int)wd.conv_dim, rows) == cudaSuccess,
+              SSD200_ELAUNCH, "conv_silu_tma launch");
       LAUNCH_CHECK("conv_silu_tma");
     } else {
       launch_conv<float, bf16, bf16>(u + d->d_inner, n_split,
@@ -758,25 +794,6 @@ constexpr int GEMV_MAX_ROWS = 16;
 // bf16: beyond the streaming-GEMV batch sizes the tensor-core GEMM wins (measured
 // at B = 16: SIMT gemv_nk 315 us vs tc_gemm ~80 us for the 1.3B in_proj)
 constexpr int GEMV_BF16_MAX_ROWS = 8;
-
-// launch with programmatic stream serialization (PDL): the kernel may start
-// while its predecessor drains; it waits (griddepcontrol.wait) before reading
-// the predecessor's outputs.
-template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                       cudaStream_t st, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
-}
 
 inline bool dec_fast_eligible(const ssd200_dims_t *d, int B) {
   return d->dtype == SSD200_BF16 && B >= 1 && B <= DEC_MAX_B && d->d_model % 256 == 0 &&
@@ -1450,6 +1467,9 @@ int ssd200_set_option(int option, int value) {
       return SSD200_OK;
     case 3:  // chunk scan: share each chunk's B tile across 4-CTA clusters by TMA multicast
       g_chunkscan_mc = value != 0;
+      return SSD200_OK;
+    case 5:  // programmatic dependent launch between consecutive kernels (1 on, 0 off)
+      g_use_pdl = value != 0;
       return SSD200_OK;
     case 4:  // output kernel: split heads into groups until >= value x SMs CTAs exist
       REQUIRE(value >= 1 && value <= 64, SSD200_EINVAL, "option 4 out of range");

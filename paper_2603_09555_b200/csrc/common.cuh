@@ -65,6 +65,17 @@ __device__ __forceinline__ float silu_tanh(float x) {
   return fmaf(h, t, h);
 }
 
+// programmatic dependent launch: a kernel launched with programmatic stream
+// serialisation may start while its predecessor drains; it lets its own
+// successor launch early (launch_dependents) and waits for the predecessor's
+// results (wait) before touching them.  Both are no-ops without PDL.
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 template <typename T> __device__ __forceinline__ T clamp_(T v, T lo, T hi) {
   return v < lo ? lo : (v > hi ? hi : v);
 }

@@ -343,6 +343,8 @@ __global__ __launch_bounds__(256, 2) void conv_silu_bf16x8(const bf16 *__restric
 template <typename T, typename TI>
 __global__ void conv_tail_kernel(const TI *__restrict__ xbc, long ld_in, T *__restrict__ tail,
                                  int Bsz, int Tlen, int C, int k) {
+  griddep_launch();
+  griddep_wait();
   long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const int km = k - 1;
   if (i >= (long)Bsz * C * km) return;

@@ -80,6 +80,8 @@ __global__ void __launch_bounds__(256) conv_silu_tma(const __grid_constant__ CUt
     sm100::fence_barrier_init();
   }
   __syncthreads();
+  griddep_launch();
+  griddep_wait();
   if (threadIdx.x == 0) {
     sm100::mbar_arrive_expect_tx(&bar, (CONV_ROWS + 3) * CONV_COLS * 2);
     sm100::tma_load_2d(&tile[0][0], &tm_xbc, &bar, c0, (int)(r0 - 3));
@@ -129,6 +131,8 @@ __global__ void __launch_bounds__(256) conv_silu_tma(const __grid_constant__ CUt
 // ------------------------------------------------------------------ cumsum
 // grid (B*Nc, ceil(H/8)), 256 threads: one warp per (b, chunk, head).
 __global__ __launch_bounds__(256) void ssd_tc_cumsum(TcSsdArgs p) {
+  griddep_launch();
+  griddep_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x / p.Nc, c = blockIdx.x % p.Nc;
   const int h = blockIdx.y * 8 + warp;
@@ -203,6 +207,8 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tslot;
+  griddep_launch();
+  griddep_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -308,6 +314,8 @@ __global__ void __launch_bounds__(192, 1)
 // ------------------------------------------------------------------ state pass
 // grid (B*H, P*N/256), 256 threads; sequential over chunks, loads batched.
 __global__ __launch_bounds__(256) void ssd_tc_pass(TcSsdArgs p) {
+  griddep_launch();
+  griddep_wait();
   const int bh = blockIdx.x;
   const int b = bh / p.H, h = bh % p.H;
   const int e = blockIdx.y * 256 + threadIdx.x;
@@ -386,6 +394,8 @@ __global__ void __launch_bounds__(192, 1)
   if (mc > 1) sm100::cluster_sync();  // barriers initialised cluster-wide before any multicast
   sm100::tc_fence_after();
   const uint32_t tmem = *tslot;
+  griddep_launch();
+  griddep_wait();
   const uint16_t mask = (uint16_t)((1u << mc) - 1u);
   const int crank = mc > 1 ? (int)sm100::cluster_rank() : 0;
 

@@ -126,6 +126,8 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tslot;
+  griddep_launch();
+  griddep_wait();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer

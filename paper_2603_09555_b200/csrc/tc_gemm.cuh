@@ -215,6 +215,8 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_launch();  // the next kernel's CTAs may take SMs as ours retire
+  griddep_wait();    // the predecessor's outputs (A, residual, ssq) are visible
 
   if (warp == 0) {
     if (lane == 0) {
