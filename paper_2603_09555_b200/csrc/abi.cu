@@ -158,8 +158,8 @@ int make_map_2d_plain(CUtensorMap *m, const void *ptr, long rows, long cols, lon
 // while its predecessor drains; it waits (griddepcontrol.wait) before reading
 // the predecessor's outputs.
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                       cudaStream_t st, Args... args) {
+cudaError_t launch_ex(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                      cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -167,10 +167,22 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = g_use_pdl ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+// decode kernels: always PDL (their weight streams start before the wait)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  return launch_ex(true, kern, grid, block, smem, st, args...);
+}
+// prefill kernels: PDL per option 5
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pf(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                      cudaStream_t st, Args... args) {
+  return launch_ex(g_use_pdl, kern, grid, block, smem, st, args...);
 }
 
 template <int BN, int EPI>
@@ -190,7 +202,7 @@ int launch_tc_gemm_bn(const bf16 *A, long lda, const bf16 *B, long ldb, int M, i
   }
   const int tiles = ((M + Cfg::BM - 1) / Cfg::BM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  cudaError_t e = launch_pdl(tc_gemm_kernel<BN, EPI>, dim3(grid), dim3(320), Cfg::SMEM, st, ta,
+  cudaError_t e = launch_pf(tc_gemm_kernel<BN, EPI>, dim3(grid), dim3(320), Cfg::SMEM, st, ta,
                              tb, M, N, K, ep);
   REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "tc_gemm_kernel: %s", cudaGetErrorString(e));
   LAUNCH_CHECK("tc_gemm_kernel");
@@ -414,7 +426,7 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
   if (rc) return rc;
   const long sms = num_sms();
   // chunk cumsums
-  REQUIRE(launch_pdl(ssd_tc_cumsum, dim3(B * a.Nc, (H + 7) / 8), dim3(256), 0, st, a) ==
+  REQUIRE(launch_pf(ssd_tc_cumsum, dim3(B * a.Nc, (H + 7) / 8), dim3(256), 0, st, a) ==
               cudaSuccess,
           SSD200_ELAUNCH, "ssd_tc_cumsum launch");
   LAUNCH_CHECK("ssd_tc_cumsum");
@@ -443,11 +455,11 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
     // few (b, h) pairs: parallel chunk states, then the O(Nc) pass
     a.NG = pick_groups(H, (long)B * a.Nc, 2 * sms);
     a.HG = H / a.NG;
-    REQUIRE(launch_pdl(ssd_tc_state, dim3(B * a.Nc * a.NG), dim3(192), StateSmem::TOTAL, st,
+    REQUIRE(launch_pf(ssd_tc_state, dim3(B * a.Nc * a.NG), dim3(192), StateSmem::TOTAL, st,
                        tm_act, a) == cudaSuccess,
             SSD200_ELAUNCH, "ssd_tc_state launch");
     LAUNCH_CHECK("ssd_tc_state");
-    REQUIRE(launch_pdl(ssd_tc_pass, dim3(B * H, TC_P * TC_N / 256), dim3(256), 0, st, a) ==
+    REQUIRE(launch_pf(ssd_tc_pass, dim3(B * H, TC_P * TC_N / 256), dim3(256), 0, st, a) ==
                 cudaSuccess,
             SSD200_ELAUNCH, "ssd_tc_pass launch");
     LAUNCH_CHECK("ssd_tc_pass");
@@ -455,7 +467,7 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
   // outputs (+ D skip + gate)
   a.NG = pick_groups(H, (long)B * a.Nc * 2, g_out_waves * sms, OutSmem::MAX_HG);
   a.HG = H / a.NG;
-  REQUIRE(launch_pdl(ssd_tc_out, dim3(B * a.Nc * 2 * a.NG), dim3(OUT_THREADS), OutSmem::TOTAL, st,
+  REQUIRE(launch_pf(ssd_tc_out, dim3(B * a.Nc * 2 * a.NG), dim3(OUT_THREADS), OutSmem::TOTAL, st,
                      tm_act, tm_prev, tm_z, tm_u, a) == cudaSuccess,
           SSD200_ELAUNCH, "ssd_tc_out launch");
   LAUNCH_CHECK("ssd_tc_out");
@@ -659,7 +671,7 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
   }
   if (!fuse_conv) {
     if (k > 1) {
-      REQUIRE(launch_pdl(conv_tail_kernel<float, bf16>,
+      REQUIRE(launch_pf(conv_tail_kernel<float, bf16>,
                          dim3(blocks_for((long)B * wd.conv_dim * (k - 1))), dim3(256), 0, st,
                          (const bf16 *)(u + d->d_inner), (long)n_split, conv_out, B, Tn,
                          (int)wd.conv_dim, k) == cudaSuccess,
@@ -672,7 +684,7 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
       rc = make_map_2d_plain(&tmx, u + d->d_inner, rows, wd.conv_dim, n_split, CONV_COLS,
                              CONV_ROWS + 3);
       if (rc) return rc;
-      REQUIRE(launch_pdl(conv_silu_tma,
+      REQUIRE(launch_pf(conv_silu_tma,
                          dim3(blocks_for(wd.conv_dim, CONV_COLS), blocks_for(rows, CONV_ROWS)),
                          dim3(256), 0, st, tmx, static_cast<const float *>(w->conv_w),
                          static_cast<const float *>(w->conv_b), act, (long)wd.conv_dim, Tn,
