@@ -200,9 +200,16 @@ __global__ void __launch_bounds__(MEGA_THREADS, 1) decode_mega(MegaArgs a) {
           if (a.trace && blockIdx.x == 0 && pstage < 512) a.trace[6000 + pstage] = gtimer();
           ++pstage;
           mbar_expect_s(&full[s], (uint32_t)nr * K * 2);
-          for (int r = 0; r < nr; ++r)
-            bulk_g2s(ring + (size_t)s * MEGA_STAGE + (size_t)r * K * 2,
-                     W + (size_t)seg_row(j, i0 + r) * K, (uint32_t)K * 2, &full[s]);
+          // one bulk copy per run of memory-contiguous rows (the TMA queue holds a
+          // bounded number of copies in flight, so bigger copies mean more bytes)
+          for (int r = 0; r < nr;) {
+            const int row0 = seg_row(j, i0 + r);
+            int run = 1;
+            while (r + run < nr && seg_row(j, i0 + r + run) == row0 + run) ++run;
+            bulk_g2s(ring + (size_t)s * MEGA_STAGE + (size_t)r * K * 2, W + (size_t)row0 * K,
+                     (uint32_t)run * K * 2, &full[s]);
+            r += run;
+          }
           if (++s == S) {
             s = 0;
             ph ^= 1;
