@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--seqlen", type=int, default=8192)
     ap.add_argument("--decode-model", default="1.3b")
     ap.add_argument("--decode-batch", type=int, default=1)
+    ap.add_argument("--decode-sweep", default="8,64,256",
+                    help="extra decode batch sizes reported under decode.sweep ('' = none)")
     ap.add_argument("--decode-steps", type=int, default=64)
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -492,7 +494,7 @@ def run_prefill_heads(args, rank, world, local):
     }
 
 
-def run_decode(args, local):
+def run_decode(args, local, B=None, params=None):
     """1.3B cached decode: one CUDA-graph step (all layers + head + argmax)
     replayed; HBM bytes = weights once + state read/write + logits."""
     import torch
@@ -500,8 +502,10 @@ def run_decode(args, local):
     import paper_2603_09555_b200 as m
 
     cfg = m.named_config(args.decode_model, compute="bf16")
-    params = m.synthetic_init(cfg, seed=7, device=f"cuda:{local}")
-    B = args.decode_batch
+    if params is None:
+        params = m.synthetic_init(cfg, seed=7, device=f"cuda:{local}")
+    if B is None:
+        B = args.decode_batch
     prompt = torch.randint(0, cfg.vocab_size, (B, 16), device=f"cuda:{local}")
     _, cache = m.prefill(params, prompt, cfg, logits=None)
     dec = m.GreedyDecoder(params, cfg, cache, args.decode_steps + 8)
@@ -517,6 +521,7 @@ def run_decode(args, local):
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / n
+    del dec, cache
     nbytes = m.decode_step_bytes(cfg, B)
     gbs = nbytes / (ms / 1e3) / 1e9
     pk = peaks()
@@ -528,7 +533,10 @@ def run_decode(args, local):
         "hbm_gbs": gbs,
         "hbm_frac": gbs / pk["hbm_gbs"],
         "bytes_per_step": nbytes,
-        "note": "CUDA-graph step: embed + 48 layers (GEMV in_proj, conv, SSM update in place, gated norm, GEMV out_proj) + head + argmax",
+        "note": ("CUDA-graph step: one persistent kernel (embed + 48 layers + head + argmax)"
+                 if B <= 8 else
+                 "CUDA-graph step: per layer tensor-core in_proj, conv, fused SSM update + gate, "
+                 "out_proj with norm + residual epilogue; head + argmax"),
     }
 
 
@@ -545,6 +553,19 @@ def main():
     dec = None
     if not args.no_decode:
         dec = run_decode(args, local)
+        sweep = [int(x) for x in args.decode_sweep.split(",") if x.strip()]
+        if sweep:
+            import paper_2603_09555_b200 as m
+
+            dcfg = m.named_config(args.decode_model, compute="bf16")
+            dparams = m.synthetic_init(dcfg, seed=7, device=f"cuda:{local}")
+            dec["sweep"] = []
+            for b in sweep:
+                r = run_decode(args, local, B=b, params=dparams)
+                dec["sweep"].append({k: r[k] for k in ("batch", "ms_per_step", "tok_per_s",
+                                                       "hbm_gbs", "hbm_frac", "bytes_per_step")})
+            del dparams
+            torch.cuda.empty_cache()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, secs, desc = cpu_prefill_sample(args.model, T=args.seqlen, layers=1)

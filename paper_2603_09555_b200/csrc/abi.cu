@@ -30,6 +30,8 @@ thread_local int g_force_fused_conv = 0;  // option 1: 1 = fused-conv in_proj ep
 thread_local bool g_force_chunkscan = false;   // tests: exercise the fused state+pass scan
 thread_local bool g_chunkscan_mc = true;       // option 3: B-tile multicast in the chunk scan
 thread_local int g_out_waves = 1;              // option 4: target CTAs (x SMs) of the output kernel
+thread_local bool g_dec_pdl = true;            // option 8: PDL between the decode kernels
+thread_local int g_dec_split_in = 0, g_dec_split_out = 0;  // options 6 / 7: wide-decode split-K (0 auto)
 thread_local bool g_use_pdl = false;           // option 5: programmatic dependent launch (measured neutral on the prefill chain; off)
 
 enum { PH_IN_PROJ = 0, PH_CONV = 1, PH_SCAN = 2, PH_NORM = 3, PH_OUT_PROJ = 4 };
@@ -176,7 +178,7 @@ cudaError_t launch_ex(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, s
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t st, Args... args) {
-  return launch_ex(true, kern, grid, block, smem, st, args...);
+  return launch_ex(g_dec_pdl, kern, grid, block, smem, st, args...);
 }
 // prefill kernels: PDL per option 5
 template <typename... KArgs, typename... Args>
@@ -187,7 +189,7 @@ cudaError_t launch_pf(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
 
 template <int BN, int EPI>
 int launch_tc_gemm_bn(const bf16 *A, long lda, const bf16 *B, long ldb, int M, int N, int K,
-                      const TcEpilogue &ep, cudaStream_t st) {
+                      const TcEpilogue &ep, cudaStream_t st, bool pdl) {
   using Cfg = TcCfg<BN>;
   CUtensorMap ta, tb;
   int rc = make_map_2d(&ta, A, M, K, lda, Cfg::BM);
@@ -200,10 +202,11 @@ int launch_tc_gemm_bn(const bf16 *A, long lda, const bf16 *B, long ldb, int M, i
                          (int)Cfg::SMEM);
     attr_set = true;
   }
-  const int tiles = ((M + Cfg::BM - 1) / Cfg::BM) * ((N + BN - 1) / BN);
+  const int ks = (EPI == TC_EPI_F32 && ep.ksplit > 1) ? ep.ksplit : 1;
+  const int tiles = ((M + Cfg::BM - 1) / Cfg::BM) * ((N + BN - 1) / BN) * ks;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  cudaError_t e = launch_pf(tc_gemm_kernel<BN, EPI>, dim3(grid), dim3(320), Cfg::SMEM, st, ta,
-                             tb, M, N, K, ep);
+  cudaError_t e = launch_ex(pdl || g_use_pdl, tc_gemm_kernel<BN, EPI>, dim3(grid), dim3(320),
+                            Cfg::SMEM, st, ta, tb, M, N, K, ep);
   REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "tc_gemm_kernel: %s", cudaGetErrorString(e));
   LAUNCH_CHECK("tc_gemm_kernel");
   return SSD200_OK;
@@ -212,14 +215,19 @@ int launch_tc_gemm_bn(const bf16 *A, long lda, const bf16 *B, long ldb, int M, i
 // D (M,N) = A (M,K) . B (N,K)^T, bf16 operands, fused epilogue.
 template <int EPI>
 int tc_gemm(const bf16 *A, long lda, const bf16 *B, long ldb, int M, int N, int K,
-            const TcEpilogue &ep, cudaStream_t st) {
+            const TcEpilogue &ep, cudaStream_t st, bool pdl = false) {
+  pdl = pdl && g_dec_pdl;
   REQUIRE(M > 0 && N > 0 && K > 0, SSD200_EINVAL, "tc_gemm: empty problem");
   REQUIRE(K % 8 == 0, SSD200_EINVAL, "tc_gemm: K must be a multiple of 8");
+  REQUIRE(ep.ksplit <= 1 || (EPI == TC_EPI_F32 && ep.ksplit <= (K + 63) / 64), SSD200_EINVAL,
+          "tc_gemm: split-K needs the F32 epilogue and at least one K block per split");
+  if (EPI == TC_EPI_F32 && ep.ksplit > 1)  // split-K: always 128-wide tiles (most tiles)
+    return launch_tc_gemm_bn<128, EPI>(A, lda, B, ldb, M, N, K, ep, st, pdl);
   // 128-wide tiles when 256-wide ones would leave SMs idle (few row tiles: decode batches)
   const long tiles256 = (long)((M + 127) / 128) * ((N + 255) / 256);
   if (N <= 128 || (EPI == TC_EPI_F32 && tiles256 < num_sms()))
-    return launch_tc_gemm_bn<128, EPI>(A, lda, B, ldb, M, N, K, ep, st);
-  return launch_tc_gemm_bn<256, EPI>(A, lda, B, ldb, M, N, K, ep, st);
+    return launch_tc_gemm_bn<128, EPI>(A, lda, B, ldb, M, N, K, ep, st, pdl);
+  return launch_tc_gemm_bn<256, EPI>(A, lda, B, ldb, M, N, K, ep, st, pdl);
 }
 
 // --------------------------------------------------------------- SSD scan
@@ -786,14 +794,53 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
 template <typename T> struct DecodeWs {
   T *u, *act, *y, *normed_T;
   bf16 *normed_lp;
+  float *part;       // wide-batch bf16: out_proj split-K partials
+  float *ssq;        // wide-batch bf16: (B, H) sum u^2
 };
+
+// split-K factors of the wide-batch (B > DEC_MAX_B) bf16 decode GEMMs: enough
+// (row tile x column tile x K range) work units to cover the SMs, >= 4 K blocks
+// of 64 per range.  The weights are read once either way; only the f32
+// partials (a few MB) are extra traffic.
+struct DecSplits {
+  int in, out;
+};
+inline DecSplits dec_splits(const ssd200_dims_t *d, int B) {
+  Widths w = widths(d);
+  auto pick = [](long tiles, int K) {
+    const long kb = (K + 63) / 64;
+    long s = (long)num_sms() / (tiles > 0 ? tiles : 1);
+    if (s > kb / 4) s = kb / 4;
+    return (int)(s < 1 ? 1 : s);
+  };
+  const long mt = (B + 127) / 128;
+  DecSplits r;
+  r.in = pick(mt * ((w.d_in_proj + 127) / 128), d->d_model);
+  r.out = pick(mt * ((d->d_model + 127) / 128), d->d_inner);
+  if (g_dec_split_in > 0 && g_dec_split_in <= (d->d_model + 63) / 64) r.in = g_dec_split_in;
+  if (g_dec_split_out > 0 && g_dec_split_out <= (d->d_inner + 63) / 64) r.out = g_dec_split_out;
+  return r;
+}
+
+inline bool dec_big_eligible(const ssd200_dims_t *d) {
+  return (d->head_dim == 8 || d->head_dim == 16 || d->head_dim == 32 || d->head_dim == 64) &&
+         d->d_state % 4 == 0 &&
+         d->d_state <= 256 && d->n_heads % d->n_groups == 0 && d->d_inner % 4 == 0 &&
+         d->n_heads % 4 == 0 && d->conv_kernel == 4 &&
+         DssLayout(d->head_dim, d->d_state, 16).total * 2 <= 200u * 1024u;
+}
 
 template <typename T>
 bool carve_decode(const ssd200_dims_t *d, int B, void *ws, size_t cap, DecodeWs<T> &o,
                   size_t *need) {
   Widths w = widths(d);
   Carve cv(ws, cap);
-  o.u = cv.take<T>((size_t)B * w.d_in_proj);
+  const bool big = std::is_same<T, float>::value && d->dtype == SSD200_BF16 && B > DEC_MAX_B &&
+                   dec_big_eligible(d);
+  const DecSplits sp = big ? dec_splits(d, B) : DecSplits{1, 1};
+  o.u = cv.take<T>((size_t)sp.in * B * w.d_in_proj);
+  o.part = big ? cv.take<float>((size_t)sp.out * B * d->d_model) : nullptr;
+  o.ssq = big ? cv.take<float>((size_t)B * d->n_heads) : nullptr;
   o.act = cv.take<T>((size_t)B * w.conv_dim);
   o.y = cv.take<T>((size_t)B * d->d_inner);
   o.normed_T = cv.take<T>((size_t)B * d->d_inner);
@@ -911,6 +958,116 @@ int decode_layer_fast(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hi
   return launch_dec_stream<DEC_EPI_OUT>(o2, st);
 }
 
+// wide-batch bf16 decode layer (B > DEC_MAX_B), 4 PDL-chained launches:
+//   tc_gemm F32 split-K in_proj -> dec_ssm_stream (TMA-pipelined conv + state
+//   update + gate + sum u^2) -> tc_gemm F32 split-K out_proj -> dec_out_finish
+//   (norm row scale + residual, B / C conv windows rolled).
+// Split-K keeps every SM streaming weights at B = 16..128, where the
+// (row tile x column tile) grid alone covers a fraction of the SMs.
+int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hidden,
+                     bf16 *hidden_lp, const float *ssm_in, float *ssm_out, const float *conv_in,
+                     float *conv_out, int B, DecodeWs<float> &o, cudaStream_t st) {
+  Widths wd = widths(d);
+  const DecSplits sp = dec_splits(d, B);
+  const long s_in = (long)B * wd.d_in_proj, s_out = (long)B * d->d_model;
+  {
+    TcEpilogue ep{};
+    ep.C = o.u;
+    ep.ldc = wd.d_in_proj;
+    ep.ksplit = sp.in;
+    ep.split_stride = s_in;
+    int rc = tc_gemm<TC_EPI_F32>(hidden_lp, d->d_model, static_cast<const bf16 *>(w->W_in),
+                                 d->d_model, B, (int)wd.d_in_proj, d->d_model, ep, st, true);
+    if (rc) return rc;
+  }
+  DecStreamArgs sa{};
+  sa.B = B;
+  sa.H = d->n_heads;
+  sa.P = d->head_dim;
+  sa.G = d->n_groups;
+  sa.N = d->d_state;
+  sa.d_inner = d->d_inner;
+  sa.conv_dim = (int)wd.conv_dim;
+  sa.proj = o.u;
+  sa.ldp = wd.d_in_proj;
+  sa.sstride = s_in;
+  sa.nsplit = sp.in;
+  sa.conv_in = conv_in;
+  sa.conv_out = conv_out;
+  sa.conv_w = static_cast<const float *>(w->conv_w);
+  sa.conv_b = static_cast<const float *>(w->conv_b);
+  sa.dt_bias = static_cast<const float *>(w->dt_bias);
+  sa.a = static_cast<const float *>(w->a);
+  sa.D = static_cast<const float *>(w->D);
+  sa.dt_lo = (float)d->dt_min;
+  sa.dt_hi = (float)d->dt_max;
+  sa.ssm_in = ssm_in;
+  sa.ssm_out = ssm_out;
+  sa.u = o.normed_lp;
+  sa.ssq = o.ssq;
+  const DssLayout lay(d->head_dim, d->d_state, sp.in);
+  sa.stage_bytes = lay.total;
+  int stages = (int)((200u * 1024u) / lay.total);
+  sa.stages = stages > DSS_MAX_STAGES ? DSS_MAX_STAGES : stages;
+  REQUIRE(sa.stages >= 2, SSD200_EUNSUPPORTED, "decode state tile too large for the smem ring");
+  const size_t smem = (size_t)sa.stages * lay.total;
+  cudaError_t e;
+  const int ntiles = B * d->n_heads;
+  const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  REQUIRE((ntiles + grid - 1) / grid <= DSS_MAX_TILES, SSD200_EUNSUPPORTED,
+          "decode: %d state tiles per CTA exceed %d", (ntiles + grid - 1) / grid, DSS_MAX_TILES);
+  const int nq = d->d_state <= 128 ? 1 : 2, rpw = d->head_dim / 8;
+  e = cudaErrorInvalidValue;
+#define DSS_CASE(NQ, RPW)                                                                      \
+  if (nq == NQ && rpw == RPW) {                                                                \
+    static bool attr = false;                                                                  \
+    if (!attr) {                                                                               \
+      cudaFuncSetAttribute(dec_ssm_stream<NQ, RPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           210 * 1024);                                                        \
+      attr = true;                                                                             \
+    }                                                                                          \
+    e = launch_pdl(dec_ssm_stream<NQ, RPW>, dim3(grid), dim3(288), smem, st, sa);              \
+  }
+  DSS_CASE(1, 1) DSS_CASE(1, 2) DSS_CASE(1, 4) DSS_CASE(1, 8)
+  DSS_CASE(2, 1) DSS_CASE(2, 2) DSS_CASE(2, 4) DSS_CASE(2, 8)
+#undef DSS_CASE
+  REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_ssm_stream: %s", cudaGetErrorString(e));
+  LAUNCH_CHECK("dec_ssm_stream");
+
+  TcEpilogue er{};
+  er.C = o.part;
+  er.ldc = d->d_model;
+  er.ksplit = sp.out;
+  er.split_stride = s_out;
+  int rc = tc_gemm<TC_EPI_F32>(o.normed_lp, d->d_inner, static_cast<const bf16 *>(w->W_out),
+                               d->d_inner, B, d->d_model, d->d_inner, er, st, true);
+  if (rc) return rc;
+  DecFinishArgs fa{};
+  fa.part = o.part;
+  fa.nsplit = sp.out;
+  fa.sstride = s_out;
+  fa.ssq = o.ssq;
+  fa.H = d->n_heads;
+  fa.inv_d = 1.f / (float)d->d_inner;
+  fa.eps = (float)d->norm_eps;
+  fa.hidden = hidden;
+  fa.lp = hidden_lp;
+  fa.d_model = d->d_model;
+  fa.proj = o.u;
+  fa.ldp = wd.d_in_proj;
+  fa.psstride = s_in;
+  fa.pnsplit = sp.in;
+  fa.d_inner = d->d_inner;
+  fa.conv_dim = (int)wd.conv_dim;
+  fa.conv_in = conv_in;
+  fa.conv_out = conv_out;
+  const int gbx = (d->d_model + 255) / 256 + (int)((wd.conv_dim - d->d_inner + 255) / 256);
+  e = launch_pdl(dec_out_finish, dim3(gbx, B), dim3(256), 0, st, fa);
+  REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_out_finish: %s", cudaGetErrorString(e));
+  LAUNCH_CHECK("dec_out_finish");
+  return SSD200_OK;
+}
+
 template <typename T>
 int decode_layer_impl(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidden,
                       bf16 *hidden_lp, const T *ssm_in, T *ssm_out, const T *conv_in,
@@ -934,6 +1091,11 @@ int decode_layer_impl(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidden
       }
       return decode_layer_fast(d, w, hidden, hidden_lp, ssm_in, ssm_out, conv_in, conv_out, B, o,
                                st);
+    }
+    if (lp && B > DEC_MAX_B && dec_big_eligible(d)) {
+      REQUIRE(hidden_lp, SSD200_EINVAL, "bf16 mode needs the hidden_lp shadow");
+      return decode_layer_big(d, w, hidden, hidden_lp, ssm_in, ssm_out, conv_in, conv_out, B, o,
+                              st);
     }
   }
   // in_proj
@@ -970,6 +1132,7 @@ int decode_layer_impl(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidden
   }
   // conv window roll + readout
   REQUIRE(k >= 1 && k <= 16, SSD200_EUNSUPPORTED, "conv_kernel");
+
   decode_conv<T, T><<<blocks_for((long)B * wd.conv_dim), 256, 0, st>>>(
       o.u, wd.d_in_proj, d->d_inner, conv_in, conv_out, static_cast<const T *>(w->conv_w),
       static_cast<const T *>(w->conv_b), o.act, B, (int)wd.conv_dim, k);
@@ -1085,6 +1248,10 @@ int head_bf16(const ssd200_dims_t *d, int V, const float *hidden, long hrs, cons
   }
   bf16 *normed = cv.take<bf16>((size_t)rows * d->d_model);
   float *lg = logits ? logits : cv.take<float>((size_t)rows * V);
+  constexpr int AM_CHUNK = 2048;
+  const int nparts = (V + AM_CHUNK - 1) / AM_CHUNK;
+  float *pv = cv.take<float>((size_t)rows * nparts);
+  int *pi = cv.take<int>((size_t)rows * nparts);
   REQUIRE(cv.ok(), SSD200_EWORKSPACE, "head workspace %zu < %zu", ws_bytes, cv.used);
   rmsnorm_rows<float, bf16><<<rows, 256, 0, st>>>(hidden, hrs, fw, normed, d->d_model,
                                                   d->d_model, (float)d->norm_eps);
@@ -1101,9 +1268,15 @@ int head_bf16(const ssd200_dims_t *d, int V, const float *hidden, long hrs, cons
     int rc = tc_gemm<TC_EPI_F32>(normed, d->d_model, E, d->d_model, rows, V, d->d_model, ep, st);
     if (rc) return rc;
   }
-  if (amax) {
-    argmax_rows<float><<<rows, 256, 0, st>>>(lg, V, V, amax);
-    LAUNCH_CHECK("argmax_rows");
+  if (amax) {  // (chunk, row) partial maxima, then one warp per row
+    cudaError_t e = launch_pdl(argmax_part, dim3(nparts, rows), dim3(256), 0, st,
+                               (const float *)lg, (long)V, V, AM_CHUNK, pv, pi);
+    REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "argmax_part: %s", cudaGetErrorString(e));
+    LAUNCH_CHECK("argmax_part");
+    e = launch_pdl(argmax_final, dim3(rows), dim3(32), 0, st, (const float *)pv,
+                   (const int *)pi, nparts, amax);
+    REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "argmax_final: %s", cudaGetErrorString(e));
+    LAUNCH_CHECK("argmax_final");
   }
   return SSD200_OK;
 }
@@ -1291,7 +1464,10 @@ size_t ssd200_head_workspace(const ssd200_dims_t *d, int vocab, int rows) {
   if (check_dims(d) || rows < 1 || vocab < 1) return 0;
   size_t elt = d->dtype == SSD200_F64 ? 8 : 4;
   size_t nel = d->dtype == SSD200_BF16 ? 2 : elt;
-  return align_up((size_t)rows * d->d_model * nel) + align_up((size_t)rows * vocab * elt);
+  // + argmax partials: (chunk or CTA, row) value / index pairs
+  const size_t parts = (size_t)rows * ((vocab + 2047) / 2048 + 2 * 1024);
+  return align_up((size_t)rows * d->d_model * nel) + align_up((size_t)rows * vocab * elt) +
+         2 * align_up(parts * 4);
 }
 
 int ssd200_head(const ssd200_dims_t *d, int vocab, const void *hidden, int64_t hidden_row_stride,
@@ -1482,6 +1658,15 @@ int ssd200_set_option(int option, int value) {
       return SSD200_OK;
     case 5:  // programmatic dependent launch between consecutive kernels (1 on, 0 off)
       g_use_pdl = value != 0;
+      return SSD200_OK;
+    case 6:  // wide-batch decode: in_proj split-K factor (0 = auto)
+      g_dec_split_in = value;
+      return SSD200_OK;
+    case 7:  // wide-batch decode: out_proj split-K factor (0 = auto)
+      g_dec_split_out = value;
+      return SSD200_OK;
+    case 8:  // programmatic dependent launch between the decode kernels (1 on, 0 off)
+      g_dec_pdl = value != 0;
       return SSD200_OK;
     case 4:  // output kernel: split heads into groups until >= value x SMs CTAs exist
       REQUIRE(value >= 1 && value <= 64, SSD200_EINVAL, "option 4 out of range");

@@ -584,4 +584,442 @@ __global__ __launch_bounds__(128) void dec_ssm(DecSsmArgs s) {
   if (threadIdx.x == 0) s.ssq[(size_t)b * s.H * s.PS + hs] = red[0] + red[1] + red[2] + red[3];
 }
 
+// ---------------------------------------------------------------------------
+// Wide-batch decode (bf16 mode, B > DEC_MAX_B): the SSM state dominates the
+// step's bytes (1.3B, B = 64: 13.2 GB of f32 state read + written vs 2.7 GB of
+// weights), so the layer's middle is one streaming kernel.
+//
+// dec_ssm_stream: a persistent TMA pipeline over the (row, head) state tiles
+// (P x N f32 = 32 KB, contiguous in the cache).  One CTA per SM takes a
+// contiguous range of tiles.  A producer warp keeps S-1 tiles in flight with
+// cp.async.bulk — per tile: the state tile, the raw in_proj x / z / B / C
+// slices of every split-K partial, and the conv windows of the tile's x and
+// B / C channels — writes each updated tile back with a bulk store (in place)
+// and refills its stage.  Eight consumer warps, per tile:
+//   conv taps + SiLU for the tile's x channels and its row's B / C channels
+//     (decode.py:103-108; the x windows are rolled here, each is owned by one
+//     tile; the shared B / C windows are rolled by dec_out_finish, after every
+//     tile has read them),
+//   h <- e^{a dt} h + dt x B ; y = C.h + D x ; u = y silu(z)      decode.py:111-133
+// all from shared memory.  dt = clip(softplus(dt_raw + dt_bias)) of all the
+// CTA's tiles is computed once up front.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(static_cast<uint32_t>(__cvta_generic_to_shared(src))), "r"(bytes)
+               : "memory");
+}
+
+struct DecStreamArgs {
+  int B, H, P, G, N, d_inner, conv_dim;
+  const float *proj;  // (nsplit, B, ldp) raw in_proj partials [z | x | B | C | dt_raw]
+  long ldp, sstride;
+  int nsplit;
+  const float *conv_in;  // (B, conv_dim, 3)
+  float *conv_out;       // x windows rolled here (may alias conv_in)
+  const float *conv_w, *conv_b, *dt_bias, *a, *D;
+  float dt_lo, dt_hi;
+  const float *ssm_in;
+  float *ssm_out;  // may alias ssm_in
+  bf16 *u;         // (B, d_inner)
+  float *ssq;      // (B, H)
+  int stages;
+  uint32_t stage_bytes;
+};
+constexpr int DSS_MAX_STAGES = 8;
+constexpr int DSS_MAX_TILES = 512;  // tiles per CTA (dt table)
+
+// byte offsets inside a stage (nsplit raw partials of x, z, B, C; conv windows)
+struct DssLayout {
+  uint32_t xr, zr, br, cr, xw, bw, cw, total;
+  __host__ __device__ DssLayout(int P, int N, int ns) {
+    xr = (uint32_t)P * N * 4;
+    zr = xr + ns * P * 4;
+    br = zr + ns * P * 4;
+    cr = br + ns * N * 4;
+    xw = cr + ns * N * 4;
+    bw = xw + P * 12;
+    cw = bw + N * 12;
+    total = (cw + N * 12 + 127) & ~127u;
+  }
+};
+
+template <int NQ, int RPW>
+__global__ __launch_bounds__(288, 1) void dec_ssm_stream(DecStreamArgs a) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  __shared__ __align__(8) uint64_t full[DSS_MAX_STAGES], done[DSS_MAX_STAGES];
+  __shared__ float red[DSS_MAX_STAGES][8];
+  __shared__ float2 hdr[DSS_MAX_TILES];                   // (dt, e^{a dt}) per local tile
+  __shared__ __align__(16) float actb[2][2 * 64];       // [x P | z P] per tile, double buffered
+  __shared__ __align__(16) float bcact[2][2 * 256];     // [B N | C N] per (row, group), double buffered
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int P = a.P, N = a.N, N4 = N >> 2, H = a.H, ns = a.nsplit;
+  const int ntiles = a.B * H;
+  const int t0 = (int)((long)ntiles * blockIdx.x / gridDim.x);
+  const int t1 = (int)((long)ntiles * (blockIdx.x + 1) / gridDim.x);
+  const int cnt = t1 - t0;
+  const int S = a.stages;
+  const DssLayout L(P, N, ns);
+  const uint32_t tile_bytes = (uint32_t)P * N * 4;
+  // B / C (and their conv windows) only travel with the first tile of each (row, group)
+  const uint32_t in_bytes = tile_bytes + (uint32_t)ns * 2 * P * 4 + P * 12;
+  const uint32_t bc_bytes = (uint32_t)ns * 2 * N * 4 + 2 * N * 12;
+  const int hpg = H / a.G;
+  auto bc_key = [&](int li) { const int t = t0 + li; return (t / H) * a.G + (t % H) / hpg; };
+  auto new_bc = [&](int li) { return li == 0 || bc_key(li) != bc_key(li - 1); };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init_s(&full[s], 1);
+      mbar_init_s(&done[s], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // the state tile is independent of this step's earlier kernels (last written
+  // by this layer's previous step, which every PDL predecessor has transitively
+  // completed), so it is requested before griddepcontrol.wait ...
+  auto issue_state = [&](int li) {
+    uint64_t *bar = &full[li % S];
+    mbar_expect_s(bar, in_bytes + (new_bc(li) ? bc_bytes : 0u));
+    bulk_g2s(dsm + (size_t)(li % S) * a.stage_bytes, a.ssm_in + (size_t)(t0 + li) * P * N,
+             tile_bytes, bar);
+  };
+  // ... the in_proj partials and conv windows after it
+  auto issue_rest = [&](int li) {
+    const int t = t0 + li, b = t / H, h = t % H, g = h / (H / a.G);
+    uint8_t *st = dsm + (size_t)(li % S) * a.stage_bytes;
+    uint64_t *bar = &full[li % S];
+    const bool nbc = new_bc(li);
+    for (int j = 0; j < ns; ++j) {
+      const float *pr = a.proj + j * a.sstride + (size_t)b * a.ldp;
+      bulk_g2s(st + L.xr + j * P * 4, pr + a.d_inner + h * P, P * 4, bar);
+      bulk_g2s(st + L.zr + j * P * 4, pr + h * P, P * 4, bar);
+      if (nbc) {
+        bulk_g2s(st + L.br + j * N * 4, pr + 2 * a.d_inner + g * N, N * 4, bar);
+        bulk_g2s(st + L.cr + j * N * 4, pr + 2 * a.d_inner + a.G * N + g * N, N * 4, bar);
+      }
+    }
+    const float *cwin = a.conv_in + (size_t)b * a.conv_dim * 3;
+    bulk_g2s(st + L.xw, cwin + (size_t)h * P * 3, P * 12, bar);
+    if (nbc) {
+      bulk_g2s(st + L.bw, cwin + (size_t)(a.d_inner + g * N) * 3, N * 12, bar);
+      bulk_g2s(st + L.cw, cwin + (size_t)(a.d_inner + a.G * N + g * N) * 3, N * 12, bar);
+    }
+  };
+  if (warp == 8) {
+    // ---------------- producer warp: loads, write-back, refills
+    if (lane == 0) {
+      for (int li = 0; li < S && li < cnt; ++li) issue_state(li);
+      griddep_wait();  // the in_proj partials
+      griddep_launch();
+      for (int li = 0; li < S && li < cnt; ++li) issue_rest(li);
+      for (int li = 0; li < cnt; ++li) {
+        const int s = li % S;
+        mbar_wait_s(&done[s], (uint32_t)(li / S) & 1u);  // the 8 warps finished tile li
+        float tsum = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) tsum += red[s][w];  // fixed order: deterministic
+        a.ssq[t0 + li] = tsum;
+        bulk_s2g(a.ssm_out + (size_t)(t0 + li) * P * N, dsm + (size_t)s * a.stage_bytes,
+                 tile_bytes);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (li + S < cnt) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // stage s read out
+          issue_state(li + S);
+          issue_rest(li + S);
+        }
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    return;
+  }
+  // ---------------- consumers: dt of every local tile first (decode.py:111-114)
+  griddep_wait();
+  for (int i = threadIdx.x; i < cnt; i += 256) {
+    const int t = t0 + i, b = t / H, h = t % H;
+    float raw = 0.f;
+    for (int j = 0; j < ns; ++j)
+      raw += a.proj[j * a.sstride + (size_t)b * a.ldp + a.d_inner + a.conv_dim + h];
+    const float dt = clamp_(softplus(raw + a.dt_bias[h]), a.dt_lo, a.dt_hi);
+    hdr[i] = make_float2(dt, expf(a.a[h] * dt));
+  }
+  named_barrier_sync(1, 256);
+  int bce = 1;
+  for (int li = 0; li < cnt; ++li) {
+    const int s = li % S;
+    uint8_t *st = dsm + (size_t)s * a.stage_bytes;
+    mbar_wait_s(&full[s], (uint32_t)(li / S) & 1u);
+    const int t = t0 + li, b = t / H, h = t % H, g = h / hpg;
+    float *ab = actb[li & 1];
+    const bool nbc = new_bc(li);
+    bce ^= nbc ? 1 : 0;
+    float *bca = bcact[bce];
+    // conv taps (oldest first) + SiLU of the tile's x channels (and of its row's B / C
+    // channels when the (row, group) changes); z summed over the split-K partials
+    for (int j = threadIdx.x; j < (nbc ? 2 * P + 2 * N : 2 * P); j += 256) {
+      const float *rawp;
+      int ch, jj;
+      if (j < P) {
+        rawp = reinterpret_cast<const float *>(st + L.xr);
+        jj = j;
+        ch = h * P + j;
+      } else if (j < 2 * P) {
+        const float *zr = reinterpret_cast<const float *>(st + L.zr);
+        float v = 0.f;
+        for (int q = 0; q < ns; ++q) v += zr[q * P + (j - P)];
+        ab[j] = v;
+        continue;
+      } else if (j < 2 * P + N) {
+        rawp = reinterpret_cast<const float *>(st + L.br);
+        jj = j - 2 * P;
+        ch = a.d_inner + g * N + jj;
+      } else {
+        rawp = reinterpret_cast<const float *>(st + L.cr);
+        jj = j - 2 * P - N;
+        ch = a.d_inner + a.G * N + g * N + jj;
+      }
+      const int nn = j < P ? P : N;
+      float v = 0.f;
+      for (int q = 0; q < ns; ++q) v += rawp[q * nn + jj];
+      const float *win = reinterpret_cast<const float *>(
+          st + (j < P ? L.xw : (j < 2 * P + N ? L.bw : L.cw))) + jj * 3;
+      const float4 cwt = __ldg(reinterpret_cast<const float4 *>(a.conv_w) + ch);
+      const float w0 = win[0], w1 = win[1], w2 = win[2];
+      const float act = silu(w0 * cwt.x + w1 * cwt.y + w2 * cwt.z + v * cwt.w + __ldg(a.conv_b + ch));
+      if (j < P)
+        ab[j] = act;
+      else
+        bca[j - 2 * P] = act;
+      if (j < P) {  // this tile owns the x windows: roll them (roll_and_insert, decode.py:65-69)
+        float *co = a.conv_out + ((size_t)b * a.conv_dim + ch) * 3;
+        co[0] = w1;
+        co[1] = w2;
+        co[2] = v;
+      }
+    }
+    named_barrier_sync(1, 256);
+    float4 *hs = reinterpret_cast<float4 *>(st);
+    const float *xs = ab;
+    const float *zs = ab + P;
+    const float4 *bs = reinterpret_cast<const float4 *>(bca);
+    const float4 *cs = reinterpret_cast<const float4 *>(bca + N);
+    const float dt = hdr[li].x, decay = hdr[li].y, Dh = __ldg(a.D + h);
+    float4 bq[NQ], cq[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      if (lane + 32 * q < N4) {
+        bq[q] = bs[lane + 32 * q];
+        cq[q] = cs[lane + 32 * q];
+      }
+    // RPW rows per warp, all loads / FMAs of the rows independent (ILP)
+    float acc[RPW];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const int p = warp * RPW + r;
+      const float dx = dt * xs[p];
+      float t = 0.f;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int n4 = lane + 32 * q;
+        if (n4 < N4) {
+          float4 v = hs[p * N4 + n4];
+          v.x = decay * v.x + dx * bq[q].x;
+          v.y = decay * v.y + dx * bq[q].y;
+          v.z = decay * v.z + dx * bq[q].z;
+          v.w = decay * v.w + dx * bq[q].w;
+          hs[p * N4 + n4] = v;
+          t = fmaf(cq[q].x, v.x, t);
+          t = fmaf(cq[q].y, v.y, t);
+          t = fmaf(cq[q].z, v.z, t);
+          t = fmaf(cq[q].w, v.w, t);
+        }
+      }
+      acc[r] = t;
+    }
+    // y_p = C . h_p: reduce the RPW row sums over the 32 lanes
+    float yv;
+    int prow;
+    bool owner;
+    if constexpr (RPW == 8) {
+      // transposing butterfly: 4 + 2 + 1 + 1 + 1 shuffles for all 8 rows; afterwards
+      // lanes 4r'..4r'+3 (r' = bit-reversed lane>>2) hold row r's total
+      const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
+#pragma unroll
+      for (int i2 = 0; i2 < 4; ++i2) {
+        const float send = u16 ? acc[i2] : acc[i2 + 4];
+        const float keep = u16 ? acc[i2 + 4] : acc[i2];
+        acc[i2] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+#pragma unroll
+      for (int i2 = 0; i2 < 2; ++i2) {
+        const float send = u8 ? acc[i2] : acc[i2 + 2];
+        const float keep = u8 ? acc[i2 + 2] : acc[i2];
+        acc[i2] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
+      {
+        const float send = u4 ? acc[0] : acc[1];
+        const float keep = u4 ? acc[1] : acc[0];
+        acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
+      acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 2);
+      acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+      yv = acc[0];
+      prow = warp * 8 + (u16 ? 4 : 0) + (u8 ? 2 : 0) + (u4 ? 1 : 0);
+      owner = (lane & 3) == 0;
+    } else {
+      yv = 0.f;
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) {
+        const float t = warp_sum(acc[r]);
+        if (lane == r) yv = t;
+      }
+      prow = warp * RPW + lane;
+      owner = lane < RPW;
+    }
+    float uu = 0.f;
+    if (owner) {
+      const float xv = xs[prow];
+      const float y = yv + Dh * xv;  // decode.py:132
+      const float uv = y * silu(zs[prow]);
+      a.u[(size_t)b * a.d_inner + h * P + prow] = __float2bfloat16_rn(uv);
+      uu = uv * uv;
+    }
+    uu = warp_sum(uu);
+    if (lane == 0) red[s][warp] = uu;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> bulk store
+    __syncwarp();
+    if (lane == 0) mbar_arrive_s(&done[s]);
+  }
+}
+
+// hidden += rsqrt(sum_h ssq[b, h] / d_inner + eps) * sum_s part[s, b, :]
+// (gated RMSNorm row scale after the out_proj, norm_w folded into W_out;
+// residual in f32 + bf16 shadow) — model.py:166-173.  grid (chunks, B); the
+// blocks past d_model roll the row's shared B / C conv windows (read by every
+// tile of dec_ssm_stream, so rolled only now): roll_and_insert, decode.py:65-69.
+struct DecFinishArgs {
+  const float *part;  // (nsplit_out, B, d_model)
+  int nsplit;
+  long sstride;
+  const float *ssq;   // (B, H)
+  int H;
+  float inv_d, eps;
+  float *hidden;
+  bf16 *lp;
+  int d_model;
+  // B / C windows
+  const float *proj;  // (nsplit_in, B, ldp)
+  long ldp, psstride;
+  int pnsplit, d_inner, conv_dim;
+  const float *conv_in;
+  float *conv_out;
+};
+__global__ __launch_bounds__(256) void dec_out_finish(DecFinishArgs a) {
+  __shared__ float sc;
+  griddep_wait();
+  griddep_launch();
+  const int b = blockIdx.y;
+  const int nb_h = (a.d_model + 255) / 256;
+  if ((int)blockIdx.x >= nb_h) {
+    const int c = a.d_inner + ((int)blockIdx.x - nb_h) * 256 + threadIdx.x;  // B / C channel
+    if (c >= a.conv_dim) return;
+    float v = 0.f;
+    for (int j = 0; j < a.pnsplit; ++j) v += a.proj[j * a.psstride + (long)b * a.ldp + a.d_inner + c];
+    const float *ci = a.conv_in + ((long)b * a.conv_dim + c) * 3;
+    float *co = a.conv_out + ((long)b * a.conv_dim + c) * 3;
+    const float w1 = ci[1], w2 = ci[2];
+    co[0] = w1;
+    co[1] = w2;
+    co[2] = v;
+    return;
+  }
+  if (threadIdx.x < 32) {
+    float t = 0.f;
+    for (int h = threadIdx.x; h < a.H; h += 32) t += a.ssq[(long)b * a.H + h];
+    t = warp_sum(t);  // fixed shuffle tree: deterministic
+    if (threadIdx.x == 0) sc = 1.f / sqrtf(t * a.inv_d + a.eps);
+  }
+  __syncthreads();
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= a.d_model) return;
+  float acc = 0.f;
+  for (int j = 0; j < a.nsplit; ++j) acc += a.part[j * a.sstride + (long)b * a.d_model + n];
+  const long i = (long)b * a.d_model + n;
+  const float v = a.hidden[i] + sc * acc;
+  a.hidden[i] = v;
+  a.lp[i] = __float2bfloat16_rn(v);
+}
+
+// greedy pick over wide logits (decode.py:72-74, ties -> lowest id): grid
+// (chunks, rows) partial maxima, then one warp per row over the partials
+__global__ __launch_bounds__(256) void argmax_part(const float *__restrict__ lg, long ld, int V,
+                                                   int chunk, float *__restrict__ pv,
+                                                   int *__restrict__ pi) {
+  __shared__ float sv[8];
+  __shared__ int si[8];
+  griddep_wait();
+  griddep_launch();
+  const int r = blockIdx.y, c0 = blockIdx.x * chunk;
+  const int c1 = min(V, c0 + chunk);
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+    const float v = lg[(long)r * ld + c];
+    if (v > bv) {  // ascending per thread: strict > keeps the lowest id
+      bv = v;
+      bi = c;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sv[warp] = bv;
+    si[warp] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w2 = 1; w2 < (int)(blockDim.x >> 5); ++w2)
+      if (sv[w2] > bv || (sv[w2] == bv && si[w2] < bi)) {
+        bv = sv[w2];
+        bi = si[w2];
+      }
+    pv[(long)r * gridDim.x + blockIdx.x] = bv;
+    pi[(long)r * gridDim.x + blockIdx.x] = bi;
+  }
+}
+
+__global__ void argmax_final(const float *__restrict__ pv, const int *__restrict__ pi, int nparts,
+                             int64_t *__restrict__ out) {
+  griddep_wait();
+  const int r = blockIdx.x, lane = threadIdx.x;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = lane; i < nparts; i += 32) {
+    const float v = pv[(long)r * nparts + i];
+    const int j = pi[(long)r * nparts + i];
+    if (v > bv || (v == bv && j < bi)) {
+      bv = v;
+      bi = j;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) out[r] = bi == 0x7fffffff ? 0 : bi;
+}
+
 }  // namespace ssd200

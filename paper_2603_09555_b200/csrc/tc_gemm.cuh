@@ -60,6 +60,11 @@ struct TcEpilogue {
   const float *conv_w;  // (conv_dim, 4)
   const float *conv_b;  // (conv_dim)
   float *conv_tail;     // (M / T, conv_dim, 3)
+  // F32 only: split-K.  ksplit > 1 cuts the K blocks into ksplit ranges (extra
+  // tiles for small-M GEMMs, decode batches); range s writes its partial
+  // product to C + s * split_stride, the consumer sums them in a fixed order.
+  int ksplit;
+  long split_stride;
 };
 
 template <int EPI> struct TcRows {
@@ -87,14 +92,14 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 
 template <int EPI>
 __device__ __forceinline__ void tc_store_chunk(const TcEpilogue &ep, uint32_t (&r)[32], int m,
-                                               int n0, int N, float rowscale) {
+                                               int n0, int N, float rowscale, size_t coff = 0) {
   if (EPI == TC_EPI_RESID_NORM) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * rowscale);
   }
   const bool full = (n0 + 32 <= N);
   if (EPI == TC_EPI_F32) {
-    float *dst = reinterpret_cast<float *>(ep.C) + (size_t)m * ep.ldc + n0;
+    float *dst = reinterpret_cast<float *>(ep.C) + coff + (size_t)m * ep.ldc + n0;
     if (full && ((ep.ldc & 3) == 0)) {
 #pragma unroll
       for (int j = 0; j < 32; j += 4)
@@ -193,7 +198,9 @@ __global__ void __launch_bounds__(320, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int RSTRIDE = TcRows<EPI>::STRIDE, HALO = TcRows<EPI>::HALO;
   const int num_n = (N + BN - 1) / BN;
-  const int num_tiles = ((M + RSTRIDE - 1) / RSTRIDE) * num_n;
+  const int num_mn = ((M + RSTRIDE - 1) / RSTRIDE) * num_n;
+  const int ksplit = (EPI == TC_EPI_F32 && ep.ksplit > 1) ? ep.ksplit : 1;
+  const int num_tiles = num_mn * ksplit;
   const int num_kb = (K + BK - 1) / BK;
   __shared__ float xch[2][2][4][3][32];  // INPROJ_CONV: [half][buf][quarter][row][col]
 
@@ -223,8 +230,10 @@ __global__ void __launch_bounds__(320, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m_blk = tile / num_n, n_blk = tile % num_n;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int mn = tile % num_mn, ks = tile / num_mn;
+        const int m_blk = mn / num_n, n_blk = mn % num_n;
+        const int kb0 = ks * num_kb / ksplit, kb1 = (ks + 1) * num_kb / ksplit;
+        for (int kb = kb0; kb < kb1; ++kb) {
           sm100::mbar_wait(&empty[s], ph ^ 1);
           sm100::mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
           sm100::tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * BK,
@@ -249,7 +258,9 @@ __global__ void __launch_bounds__(320, 1)
         sm100::mbar_wait(&tempty[as], aph ^ 1);
         sm100::tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int ks = tile / num_mn;
+        const int kb0 = ks * num_kb / ksplit, kb1 = (ks + 1) * num_kb / ksplit;
+        for (int kb = kb0; kb < kb1; ++kb) {
           sm100::mbar_wait(&full[s], ph);
           sm100::tc_fence_after();
           const uint32_t a0 = sm100::smem_u32(sA + s * Cfg::A_BYTES);
@@ -258,7 +269,7 @@ __global__ void __launch_bounds__(320, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = sm100::sw128_desc(a0 + k * 32, 16, 1024);
             const uint64_t bd = sm100::sw128_desc(b0 + k * 32, 16, 1024);
-            sm100::mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            sm100::mma_bf16(d_tmem, ad, bd, idesc, (kb != kb0) || (k != 0));
           }
           sm100::mma_commit(&empty[s]);
           if (++s == STAGES) {
@@ -277,7 +288,9 @@ __global__ void __launch_bounds__(320, 1)
     const bool vec_ok = (ep.ldc & 7) == 0;
     int local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-      const int m_blk = tile / num_n, n_blk = tile % num_n;
+      const int mn = tile % num_mn;
+      const size_t coff = (size_t)(tile / num_mn) * (size_t)ep.split_stride;
+      const int m_blk = mn / num_n, n_blk = mn % num_n;
       const int as = local & 1;
       const uint32_t aph = (local >> 1) & 1;
       const int i_row = q * 32 + lane;                 // tile row == TMEM lane
@@ -443,7 +456,7 @@ __global__ void __launch_bounds__(320, 1)
           }
           __syncwarp();
         } else if (m < M) {
-          tc_store_chunk<EPI>(ep, r, m, n0, N, rowscale);
+          tc_store_chunk<EPI>(ep, r, m, n0, N, rowscale, coff);
         }
 #pragma unroll
         for (int j = 0; j < 32; ++j) hv[j] = hn[j];

@@ -391,3 +391,32 @@ def test_bf16_head_sharded_prefill_matches_unsharded(world):
         for i in range(cfg.n_layers):
             a, b = run.ssm[i], cache.ssm_all[i][:, hs].float()
             assert (torch.linalg.norm(a - b) / torch.linalg.norm(b)).item() <= BF16_BOUND
+
+
+@pytest.mark.parametrize("B", [9, 16])
+def test_bf16_wide_batch_decode_state_vs_oracle(B):
+    """Wide-batch decode (B > 8: tensor-core in_proj, fused SSM update + gate +
+    sum u^2, out_proj with the norm in its epilogue): one step's logits and the
+    updated SSM / conv cache against the oracle on bf16-rounded weights, and
+    the in-place graph loop against the functional step."""
+    import paper_2603_09555_b200 as m
+
+    cfg = _bf16_cfg()
+    host = m.random_init_host(cfg, 41)
+    params = m.from_reference(host, cfg)
+    toks = np.random.default_rng(42).integers(0, cfg.vocab_size, size=(B, 30))
+    _, cache = m.prefill(params, toks[:, :29], cfg, logits=None)
+    before = cache.ssm_all.clone()
+    sl, new = m.decode_step(params, cache, toks[:, 29], cfg)
+    assert torch.equal(cache.ssm_all, before)  # the input cache is not mutated
+    rl, rs, rc = orc.prefill(orc.round_weights_bf16(host), toks, cfg.with_policy(compute="f32"))
+    rel = np.linalg.norm(_np(sl) - rl[:, -1]) / np.linalg.norm(rl[:, -1])
+    assert rel <= BF16_BOUND, rel
+    rs = np.stack(rs)
+    assert np.linalg.norm(_np(new.ssm_all) - rs) / np.linalg.norm(rs) <= BF16_BOUND
+    rc = np.stack(rc)
+    assert np.linalg.norm(_np(new.conv_all) - rc) / np.linalg.norm(rc) <= BF16_BOUND
+    a = m.generate(params, toks[:, :29], 6, cfg=cfg, use_graph=True, keep_logits=True)
+    b = m.generate(params, toks[:, :29], 6, cfg=cfg, use_graph=False, keep_logits=True)
+    assert torch.equal(a.tokens, b.tokens)
+    assert torch.equal(a.per_step_logits, b.per_step_logits)
