@@ -30,6 +30,7 @@ thread_local int g_force_fused_conv = 0;  // option 1: 1 = fused-conv in_proj ep
 thread_local bool g_force_chunkscan = false;   // tests: exercise the fused state+pass scan
 thread_local bool g_chunkscan_mc = true;       // option 3: B-tile multicast in the chunk scan
 thread_local int g_out_waves = 1;              // option 4: target CTAs (x SMs) of the output kernel
+thread_local int g_stream_stages = 0, g_stream_cps = 0, g_stream_cw = 8;  // options 11 / 12 / 13
 thread_local bool g_dec_pdl = true;            // option 8: PDL between the decode kernels
 thread_local int g_dec_split_in = 0, g_dec_split_out = 0;  // options 6 / 7: wide-decode split-K (0 auto)
 thread_local bool g_use_pdl = false;           // option 5: programmatic dependent launch (measured neutral on the prefill chain; off)
@@ -823,7 +824,7 @@ inline DecSplits dec_splits(const ssd200_dims_t *d, int B) {
 }
 
 inline bool dec_big_eligible(const ssd200_dims_t *d) {
-  return (d->head_dim == 8 || d->head_dim == 16 || d->head_dim == 32 || d->head_dim == 64) &&
+  return (d->head_dim == 16 || d->head_dim == 32 || d->head_dim == 64) &&
          d->d_state % 4 == 0 &&
          d->d_state <= 256 && d->n_heads % d->n_groups == 0 && d->d_inner % 4 == 0 &&
          d->n_heads % 4 == 0 && d->conv_kernel == 4 &&
@@ -1007,29 +1008,40 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   sa.ssq = o.ssq;
   const DssLayout lay(d->head_dim, d->d_state, sp.in);
   sa.stage_bytes = lay.total;
-  int stages = (int)((200u * 1024u) / lay.total);
+  // CTAs per SM: two independent pipelines per SM stream faster once every CTA
+  // has enough tiles to amortise its pipeline fill (measured: B = 256 at 1.3B
+  // 12.1 -> 10.9 ms/step; B <= 64 slightly slower)
+  const int ntiles_all = B * d->n_heads;
+  const int cps = g_stream_cps == 1 ? 1
+                  : g_stream_cps == 2 ? 2
+                  : (ntiles_all >= 48 * num_sms() ? 2 : 1);
+  int stages = (int)((cps == 2 ? 105u * 1024u : 214u * 1024u) / lay.total);
+  if (g_stream_stages > 0 && g_stream_stages < stages) stages = g_stream_stages;
   sa.stages = stages > DSS_MAX_STAGES ? DSS_MAX_STAGES : stages;
   REQUIRE(sa.stages >= 2, SSD200_EUNSUPPORTED, "decode state tile too large for the smem ring");
   const size_t smem = (size_t)sa.stages * lay.total;
   cudaError_t e;
   const int ntiles = B * d->n_heads;
-  const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  const int grid = ntiles < cps * num_sms() ? ntiles : cps * num_sms();
   REQUIRE((ntiles + grid - 1) / grid <= DSS_MAX_TILES, SSD200_EUNSUPPORTED,
           "decode: %d state tiles per CTA exceed %d", (ntiles + grid - 1) / grid, DSS_MAX_TILES);
-  const int nq = d->d_state <= 128 ? 1 : 2, rpw = d->head_dim / 8;
+  const int cw = g_stream_cw == 16 ? 16 : 8;  // consumer warps
+  const int nq = d->d_state <= 128 ? 1 : 2, rpw = d->head_dim / cw;
   e = cudaErrorInvalidValue;
-#define DSS_CASE(NQ, RPW)                                                                      \
-  if (nq == NQ && rpw == RPW) {                                                                \
+#define DSS_CASE(NQ, RPW, CW)                                                                  \
+  if (nq == NQ && rpw == RPW && cw == CW) {                                                    \
     static bool attr = false;                                                                  \
     if (!attr) {                                                                               \
-      cudaFuncSetAttribute(dec_ssm_stream<NQ, RPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           210 * 1024);                                                        \
+      cudaFuncSetAttribute(dec_ssm_stream<NQ, RPW, CW>,                                        \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 214 * 1024);           \
       attr = true;                                                                             \
     }                                                                                          \
-    e = launch_pdl(dec_ssm_stream<NQ, RPW>, dim3(grid), dim3(288), smem, st, sa);              \
+    e = launch_pdl(dec_ssm_stream<NQ, RPW, CW>, dim3(grid), dim3(CW * 32 + 32), smem, st, sa); \
   }
-  DSS_CASE(1, 1) DSS_CASE(1, 2) DSS_CASE(1, 4) DSS_CASE(1, 8)
-  DSS_CASE(2, 1) DSS_CASE(2, 2) DSS_CASE(2, 4) DSS_CASE(2, 8)
+  DSS_CASE(1, 1, 8) DSS_CASE(1, 2, 8) DSS_CASE(1, 4, 8) DSS_CASE(1, 8, 8)
+  DSS_CASE(2, 1, 8) DSS_CASE(2, 2, 8) DSS_CASE(2, 4, 8) DSS_CASE(2, 8, 8)
+  DSS_CASE(1, 1, 16) DSS_CASE(1, 2, 16) DSS_CASE(1, 4, 16)
+  DSS_CASE(2, 1, 16) DSS_CASE(2, 2, 16) DSS_CASE(2, 4, 16)
 #undef DSS_CASE
   REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_ssm_stream: %s", cudaGetErrorString(e));
   LAUNCH_CHECK("dec_ssm_stream");
@@ -1664,6 +1676,15 @@ int ssd200_set_option(int option, int value) {
       return SSD200_OK;
     case 7:  // wide-batch decode: out_proj split-K factor (0 = auto)
       g_dec_split_out = value;
+      return SSD200_OK;
+    case 11:  // wide-batch decode stream: ring stages (0 = as many as fit)
+      g_stream_stages = value;
+      return SSD200_OK;
+    case 13:  // wide-batch decode stream: consumer warps (8 or 16)
+      g_stream_cw = value;
+      return SSD200_OK;
+    case 12:  // wide-batch decode stream: CTAs per SM (1 or 2; 0 = by tile count)
+      g_stream_cps = value;
       return SSD200_OK;
     case 8:  // programmatic dependent launch between the decode kernels (1 on, 0 off)
       g_dec_pdl = value != 0;

@@ -644,13 +644,14 @@ struct DssLayout {
   }
 };
 
-template <int NQ, int RPW>
-__global__ __launch_bounds__(288, 1) void dec_ssm_stream(DecStreamArgs a) {
+// CW consumer warps (RPW = P / CW rows each) + 1 producer warp
+template <int NQ, int RPW, int CW>
+__global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(DecStreamArgs a) {
+  constexpr int CT = CW * 32;
   extern __shared__ __align__(128) uint8_t dsm[];
   __shared__ __align__(8) uint64_t full[DSS_MAX_STAGES], done[DSS_MAX_STAGES];
-  __shared__ float red[DSS_MAX_STAGES][8];
+  __shared__ float red[DSS_MAX_STAGES][CW];
   __shared__ float2 hdr[DSS_MAX_TILES];                   // (dt, e^{a dt}) per local tile
-  __shared__ __align__(16) float actb[2][2 * 64];       // [x P | z P] per tile, double buffered
   __shared__ __align__(16) float bcact[2][2 * 256];     // [B N | C N] per (row, group), double buffered
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int P = a.P, N = a.N, N4 = N >> 2, H = a.H, ns = a.nsplit;
@@ -670,7 +671,7 @@ __global__ __launch_bounds__(288, 1) void dec_ssm_stream(DecStreamArgs a) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init_s(&full[s], 1);
-      mbar_init_s(&done[s], 8);
+      mbar_init_s(&done[s], CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -706,7 +707,7 @@ __global__ __launch_bounds__(288, 1) void dec_ssm_stream(DecStreamArgs a) {
       bulk_g2s(st + L.cw, cwin + (size_t)(a.d_inner + a.G * N + g * N) * 3, N * 12, bar);
     }
   };
-  if (warp == 8) {
+  if (warp == CW) {
     // ---------------- producer warp: loads, write-back, refills
     if (lane == 0) {
       for (int li = 0; li < S && li < cnt; ++li) issue_state(li);
@@ -715,27 +716,22 @@ __global__ __launch_bounds__(288, 1) void dec_ssm_stream(DecStreamArgs a) {
       for (int li = 0; li < S && li < cnt; ++li) issue_rest(li);
       for (int li = 0; li < cnt; ++li) {
         const int s = li % S;
-        mbar_wait_s(&done[s], (uint32_t)(li / S) & 1u);  // the 8 warps finished tile li
+        mbar_wait_s(&done[s], (uint32_t)(li / S) & 1u);  // the consumer warps finished tile li
         float tsum = 0.f;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) tsum += red[s][w];  // fixed order: deterministic
+        for (int w = 0; w < CW; ++w) tsum += red[s][w];  // fixed order: deterministic
         a.ssq[t0 + li] = tsum;
-        bulk_s2g(a.ssm_out + (size_t)(t0 + li) * P * N, dsm + (size_t)s * a.stage_bytes,
-                 tile_bytes);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        if (li + S < cnt) {
-          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // stage s read out
+        if (li + S < cnt) {  // stage s is free: the consumers stored the tile from registers
           issue_state(li + S);
           issue_rest(li + S);
         }
       }
-      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     return;
   }
   // ---------------- consumers: dt of every local tile first (decode.py:111-114)
   griddep_wait();
-  for (int i = threadIdx.x; i < cnt; i += 256) {
+  for (int i = threadIdx.x; i < cnt; i += CT) {
     const int t = t0 + i, b = t / H, h = t % H;
     float raw = 0.f;
     for (int j = 0; j < ns; ++j)
@@ -743,64 +739,60 @@ __global__ __launch_bounds__(288, 1) void dec_ssm_stream(DecStreamArgs a) {
     const float dt = clamp_(softplus(raw + a.dt_bias[h]), a.dt_lo, a.dt_hi);
     hdr[i] = make_float2(dt, expf(a.a[h] * dt));
   }
-  named_barrier_sync(1, 256);
+  named_barrier_sync(1, CT);
   int bce = 1;
   for (int li = 0; li < cnt; ++li) {
     const int s = li % S;
     uint8_t *st = dsm + (size_t)s * a.stage_bytes;
     mbar_wait_s(&full[s], (uint32_t)(li / S) & 1u);
     const int t = t0 + li, b = t / H, h = t % H, g = h / hpg;
-    float *ab = actb[li & 1];
     const bool nbc = new_bc(li);
     bce ^= nbc ? 1 : 0;
     float *bca = bcact[bce];
-    // conv taps (oldest first) + SiLU of the tile's x channels (and of its row's B / C
-    // channels when the (row, group) changes); z summed over the split-K partials
-    for (int j = threadIdx.x; j < (nbc ? 2 * P + 2 * N : 2 * P); j += 256) {
-      const float *rawp;
-      int ch, jj;
-      if (j < P) {
-        rawp = reinterpret_cast<const float *>(st + L.xr);
-        jj = j;
-        ch = h * P + j;
-      } else if (j < 2 * P) {
-        const float *zr = reinterpret_cast<const float *>(st + L.zr);
+    if (nbc) {
+      // the row's B / C channels (shared by every head of the group): conv taps
+      // (oldest first) + SiLU, once per (row, group) per CTA
+      for (int j = threadIdx.x; j < 2 * N; j += CT) {
+        const bool isc = j >= N;
+        const int jj = isc ? j - N : j;
+        const int ch = a.d_inner + (isc ? a.G * N : 0) + g * N + jj;
+        const float *rawp = reinterpret_cast<const float *>(st + (isc ? L.cr : L.br));
         float v = 0.f;
-        for (int q = 0; q < ns; ++q) v += zr[q * P + (j - P)];
-        ab[j] = v;
-        continue;
-      } else if (j < 2 * P + N) {
-        rawp = reinterpret_cast<const float *>(st + L.br);
-        jj = j - 2 * P;
-        ch = a.d_inner + g * N + jj;
-      } else {
-        rawp = reinterpret_cast<const float *>(st + L.cr);
-        jj = j - 2 * P - N;
-        ch = a.d_inner + a.G * N + g * N + jj;
+        for (int q = 0; q < ns; ++q) v += rawp[q * N + jj];
+        const float *win = reinterpret_cast<const float *>(st + (isc ? L.cw : L.bw)) + jj * 3;
+        const float4 cwt = __ldg(reinterpret_cast<const float4 *>(a.conv_w) + ch);
+        bca[j] = silu(win[0] * cwt.x + win[1] * cwt.y + win[2] * cwt.z + v * cwt.w +
+                      __ldg(a.conv_b + ch));
       }
-      const int nn = j < P ? P : N;
+      named_barrier_sync(1, CT);
+    }
+    // this warp's rows need only their own x and z: lanes 0..RPW-1 run the x conv
+    // (and roll the x windows, which this tile owns: roll_and_insert, decode.py:65-69),
+    // lanes 16..16+RPW-1 sum z over the split-K partials
+    float mine = 0.f;
+    if (lane < RPW) {
+      const int p = warp * RPW + lane, ch = h * P + p;
+      const float *rawp = reinterpret_cast<const float *>(st + L.xr);
       float v = 0.f;
-      for (int q = 0; q < ns; ++q) v += rawp[q * nn + jj];
-      const float *win = reinterpret_cast<const float *>(
-          st + (j < P ? L.xw : (j < 2 * P + N ? L.bw : L.cw))) + jj * 3;
+      for (int q = 0; q < ns; ++q) v += rawp[q * P + p];
+      const float *win = reinterpret_cast<const float *>(st + L.xw) + p * 3;
       const float4 cwt = __ldg(reinterpret_cast<const float4 *>(a.conv_w) + ch);
       const float w0 = win[0], w1 = win[1], w2 = win[2];
-      const float act = silu(w0 * cwt.x + w1 * cwt.y + w2 * cwt.z + v * cwt.w + __ldg(a.conv_b + ch));
-      if (j < P)
-        ab[j] = act;
-      else
-        bca[j - 2 * P] = act;
-      if (j < P) {  // this tile owns the x windows: roll them (roll_and_insert, decode.py:65-69)
-        float *co = a.conv_out + ((size_t)b * a.conv_dim + ch) * 3;
-        co[0] = w1;
-        co[1] = w2;
-        co[2] = v;
-      }
+      mine = silu(w0 * cwt.x + w1 * cwt.y + w2 * cwt.z + v * cwt.w + __ldg(a.conv_b + ch));
+      float *co = a.conv_out + ((size_t)b * a.conv_dim + ch) * 3;
+      co[0] = w1;
+      co[1] = w2;
+      co[2] = v;
+    } else if (lane >= 16 && lane < 16 + RPW) {
+      const float *zr = reinterpret_cast<const float *>(st + L.zr);
+      const int p = warp * RPW + lane - 16;
+      for (int q = 0; q < ns; ++q) mine += zr[q * P + p];
     }
-    named_barrier_sync(1, 256);
-    float4 *hs = reinterpret_cast<float4 *>(st);
-    const float *xs = ab;
-    const float *zs = ab + P;
+    float xrow[RPW];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) xrow[r] = __shfl_sync(0xffffffffu, mine, r);
+    const float4 *hs = reinterpret_cast<const float4 *>(st);
+    float4 *ho = reinterpret_cast<float4 *>(a.ssm_out + (size_t)t * P * N);
     const float4 *bs = reinterpret_cast<const float4 *>(bca);
     const float4 *cs = reinterpret_cast<const float4 *>(bca + N);
     const float dt = hdr[li].x, decay = hdr[li].y, Dh = __ldg(a.D + h);
@@ -816,7 +808,7 @@ __global__ __launch_bounds__(288, 1) void dec_ssm_stream(DecStreamArgs a) {
 #pragma unroll
     for (int r = 0; r < RPW; ++r) {
       const int p = warp * RPW + r;
-      const float dx = dt * xs[p];
+      const float dx = dt * xrow[r];
       float t = 0.f;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
@@ -827,7 +819,7 @@ __global__ __launch_bounds__(288, 1) void dec_ssm_stream(DecStreamArgs a) {
           v.y = decay * v.y + dx * bq[q].y;
           v.z = decay * v.z + dx * bq[q].z;
           v.w = decay * v.w + dx * bq[q].w;
-          hs[p * N4 + n4] = v;
+          __stcs(ho + p * N4 + n4, v);  // streaming store straight from registers
           t = fmaf(cq[q].x, v.x, t);
           t = fmaf(cq[q].y, v.y, t);
           t = fmaf(cq[q].z, v.z, t);
@@ -840,53 +832,43 @@ __global__ __launch_bounds__(288, 1) void dec_ssm_stream(DecStreamArgs a) {
     float yv;
     int prow;
     bool owner;
-    if constexpr (RPW == 8) {
-      // transposing butterfly: 4 + 2 + 1 + 1 + 1 shuffles for all 8 rows; afterwards
-      // lanes 4r'..4r'+3 (r' = bit-reversed lane>>2) hold row r's total
-      const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
+    if constexpr (RPW > 1) {
+      // transposing butterfly: log2(RPW) levels halve the row set per lane (RPW - 1
+      // shuffles in all), then plain xor levels; afterwards every lane of an aligned
+      // group of 32 / RPW lanes holds the total of row warp * RPW + rsel
+      int rsel = 0;
 #pragma unroll
-      for (int i2 = 0; i2 < 4; ++i2) {
-        const float send = u16 ? acc[i2] : acc[i2 + 4];
-        const float keep = u16 ? acc[i2 + 4] : acc[i2];
-        acc[i2] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      for (int hf = RPW / 2, o = 16; hf >= 1; hf >>= 1, o >>= 1) {
+        const bool up = lane & o;
+#pragma unroll
+        for (int i2 = 0; i2 < hf; ++i2) {
+          const float send = up ? acc[i2] : acc[i2 + hf];
+          const float keep = up ? acc[i2 + hf] : acc[i2];
+          acc[i2] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+        if (up) rsel += hf;
       }
 #pragma unroll
-      for (int i2 = 0; i2 < 2; ++i2) {
-        const float send = u8 ? acc[i2] : acc[i2 + 2];
-        const float keep = u8 ? acc[i2 + 2] : acc[i2];
-        acc[i2] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-      }
-      {
-        const float send = u4 ? acc[0] : acc[1];
-        const float keep = u4 ? acc[1] : acc[0];
-        acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-      }
-      acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 2);
-      acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+      for (int o = 16 / RPW; o > 0; o >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], o);
       yv = acc[0];
-      prow = warp * 8 + (u16 ? 4 : 0) + (u8 ? 2 : 0) + (u4 ? 1 : 0);
-      owner = (lane & 3) == 0;
+      prow = warp * RPW + rsel;
+      owner = (lane & (32 / RPW - 1)) == 0;
     } else {
-      yv = 0.f;
-#pragma unroll
-      for (int r = 0; r < RPW; ++r) {
-        const float t = warp_sum(acc[r]);
-        if (lane == r) yv = t;
-      }
-      prow = warp * RPW + lane;
-      owner = lane < RPW;
+      yv = warp_sum(acc[0]);
+      prow = warp;
+      owner = lane == 0;
     }
     float uu = 0.f;
+    const float xv = __shfl_sync(0xffffffffu, mine, prow - warp * RPW);
+    const float zv = __shfl_sync(0xffffffffu, mine, 16 + prow - warp * RPW);
     if (owner) {
-      const float xv = xs[prow];
       const float y = yv + Dh * xv;  // decode.py:132
-      const float uv = y * silu(zs[prow]);
+      const float uv = y * silu(zv);
       a.u[(size_t)b * a.d_inner + h * P + prow] = __float2bfloat16_rn(uv);
       uu = uv * uv;
     }
     uu = warp_sum(uu);
     if (lane == 0) red[s][warp] = uu;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> bulk store
     __syncwarp();
     if (lane == 0) mbar_arrive_s(&done[s]);
   }
