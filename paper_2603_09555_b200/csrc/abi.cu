@@ -31,6 +31,8 @@ thread_local bool g_force_chunkscan = false;   // tests: exercise the fused stat
 thread_local bool g_chunkscan_mc = true;       // option 3: B-tile multicast in the chunk scan
 thread_local int g_out_waves = 1;              // option 4: target CTAs (x SMs) of the output kernel
 thread_local int g_stream_stages = 0, g_stream_cps = 0, g_stream_cw = 8;  // options 11 / 12 / 13
+thread_local int g_wide_min = 2;               // option 14: smallest batch on the wide-batch decode path (measured: the per-layer path beats the fused step from B = 2)
+thread_local int g_mega_pf = 0;                // option 9: fused decode step L2 prefetch lookahead (stages)
 thread_local bool g_dec_pdl = true;            // option 8: PDL between the decode kernels
 thread_local int g_dec_split_in = 0, g_dec_split_out = 0;  // options 6 / 7: wide-decode split-K (0 auto)
 thread_local bool g_use_pdl = false;           // option 5: programmatic dependent launch (measured neutral on the prefill chain; off)
@@ -836,7 +838,7 @@ bool carve_decode(const ssd200_dims_t *d, int B, void *ws, size_t cap, DecodeWs<
                   size_t *need) {
   Widths w = widths(d);
   Carve cv(ws, cap);
-  const bool big = std::is_same<T, float>::value && d->dtype == SSD200_BF16 && B > DEC_MAX_B &&
+  const bool big = std::is_same<T, float>::value && d->dtype == SSD200_BF16 && B >= g_wide_min &&
                    dec_big_eligible(d);
   const DecSplits sp = big ? dec_splits(d, B) : DecSplits{1, 1};
   o.u = cv.take<T>((size_t)sp.in * B * w.d_in_proj);
@@ -1092,6 +1094,11 @@ int decode_layer_impl(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidden
   const bool lp = d->dtype == SSD200_BF16;
   const int k = d->conv_kernel;
   if constexpr (std::is_same<T, float>::value) {
+    if (lp && B >= g_wide_min && dec_big_eligible(d)) {
+      REQUIRE(hidden_lp, SSD200_EINVAL, "bf16 mode needs the hidden_lp shadow");
+      return decode_layer_big(d, w, hidden, hidden_lp, ssm_in, ssm_out, conv_in, conv_out, B, o,
+                              st);
+    }
     if (dec_fast_eligible(d, B) && hidden_lp) {
       static bool attrs = false;
       if (!attrs) {
@@ -1103,11 +1110,6 @@ int decode_layer_impl(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidden
       }
       return decode_layer_fast(d, w, hidden, hidden_lp, ssm_in, ssm_out, conv_in, conv_out, B, o,
                                st);
-    }
-    if (lp && B > DEC_MAX_B && dec_big_eligible(d)) {
-      REQUIRE(hidden_lp, SSD200_EINVAL, "bf16 mode needs the hidden_lp shadow");
-      return decode_layer_big(d, w, hidden, hidden_lp, ssm_in, ssm_out, conv_in, conv_out, B, o,
-                              st);
     }
   }
   // in_proj
@@ -1517,7 +1519,7 @@ int ssd200_gemm_bf16(const void *A, const void *B, void *C, int M, int N, int K,
 
 // ---------------------------------------------------------------- fused step
 static bool mega_eligible(const ssd200_dims_t *d, int B) {
-  return d->dtype == SSD200_BF16 && B >= 1 && B <= DEC_MAX_B && d->d_model % 256 == 0 &&
+  return d->dtype == SSD200_BF16 && B >= 1 && B <= DEC_MAX_B && (B < g_wide_min || !dec_big_eligible(d)) && d->d_model % 256 == 0 &&
          d->d_inner % 256 == 0 && d->d_state <= 256 && d->d_state % 4 == 0 &&
          d->head_dim % 4 == 0 && d->conv_kernel >= 1 && d->conv_kernel <= 16 &&
          (size_t)2 * d->d_inner * 2 <= MEGA_STAGE && (size_t)2 * d->d_model * 2 <= MEGA_STAGE;
@@ -1603,6 +1605,7 @@ int ssd200_decode_step(const ssd200_dims_t *d, const ssd200_layer_t *layers_dev,
   a.L = n_layers;
   a.V = vocab;
   a.stages = S;
+  a.pf_ahead = g_mega_pf;
   a.d_model = d->d_model;
   a.d_inner = d->d_inner;
   a.conv_dim = (int)w.conv_dim;
@@ -1685,6 +1688,14 @@ int ssd200_set_option(int option, int value) {
       return SSD200_OK;
     case 12:  // wide-batch decode stream: CTAs per SM (1 or 2; 0 = by tile count)
       g_stream_cps = value;
+      return SSD200_OK;
+    case 14:  // smallest batch that takes the wide-batch decode path (default 2)
+      REQUIRE(value >= 1, SSD200_EINVAL, "option 14 out of range");
+      g_wide_min = value;
+      return SSD200_OK;
+    case 9:  // fused decode step: L2 prefetch lookahead in ring stages (0 = off)
+      REQUIRE(value >= 0 && value <= 64, SSD200_EINVAL, "option 9 out of range");
+      g_mega_pf = value;
       return SSD200_OK;
     case 8:  // programmatic dependent launch between the decode kernels (1 on, 0 off)
       g_dec_pdl = value != 0;

@@ -38,7 +38,7 @@ constexpr int MEGA_MAX_NK = 64;   // own d_inner channels per CTA
 constexpr int MEGA_MAX_DT = 16;   // heads touched by one CTA's channels
 
 struct MegaArgs {
-  int B, L, V, stages;
+  int B, L, V, stages, pf_ahead;
   int d_model, d_inner, conv_dim, d_in_proj, H, P, G, N, k, PS;
   float eps, dt_lo, dt_hi;
   const ssd200_layer_t *layers;  // device array [L]
@@ -168,8 +168,10 @@ __global__ void __launch_bounds__(MEGA_THREADS, 1) decode_mega(MegaArgs a) {
     // ------------------------------------------------ producer: the weight stream
     // Segment j of the step: 2l = this CTA's W_in rows of layer l, 2l+1 = its
     // W_out share, 2L = its share of E; rows are bulk-copied into the ring.
-    // (L2 prefetching ahead of the ring was measured to slow the step down:
-    // it competes with the copies and lengthens every synchronisation.)
+    // With pf_ahead > 0 a second cursor runs pf_ahead stages ahead of the copies
+    // and prefetches those stages into L2, so HBM keeps streaming while the ring
+    // is full during the grid-wide synchronisations (bounded: prefetching a
+    // whole layer ahead was measured to slow the step down).
     if (lane == 0) {
       int s = 0, pstage = 0;
       uint32_t ph = 0;
@@ -191,11 +193,43 @@ __global__ void __launch_bounds__(MEGA_THREADS, 1) decode_mega(MegaArgs a) {
       auto seg_row = [&](int j, int i) {
         return j == 2 * a.L ? r0_e + i : (j & 1) ? r0_out + i : own.row(i, a);
       };
+      // L2 prefetch cursor (segment pj, first row pi0), pq = its stage index
+      int pj = 0, pi0 = 0, pq = 0, q = 0;
+      auto pf_next = [&]() {
+        while (pj < nseg && pi0 >= seg_n(pj)) {
+          ++pj;
+          pi0 = 0;
+        }
+        if (pj >= nseg) return false;
+        const int K = seg_k(pj), nr = min(mega_rows(K), seg_n(pj) - pi0);
+        const bf16 *W = seg_w(pj);
+        for (int r = 0; r < nr;) {
+          const int row0 = seg_row(pj, pi0 + r);
+          int run = 1;
+          while (r + run < nr && seg_row(pj, pi0 + r + run) == row0 + run) ++run;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(W + (size_t)row0 * K),
+                       "r"((uint32_t)run * K * 2)
+                       : "memory");
+          r += run;
+        }
+        pi0 += nr;
+        ++pq;
+        return true;
+      };
       for (int j = 0; j < nseg; ++j) {
         const bf16 *W = seg_w(j);
         const int K = seg_k(j), nrows = seg_n(j), per = mega_rows(K);
         for (int i0 = 0; i0 < nrows; i0 += per) {
           const int nr = min(per, nrows - i0);
+          if (a.pf_ahead > 0) {
+            if (pq <= q) {  // keep the prefetch cursor past this stage
+              while (pq <= q && pf_next()) {
+              }
+            }
+            while (pq <= q + a.pf_ahead && pf_next()) {
+            }
+          }
+          ++q;
           mbar_wait_s(&empty[s], ph ^ 1);
           if (a.trace && blockIdx.x == 0 && pstage < 512) a.trace[6000 + pstage] = gtimer();
           ++pstage;

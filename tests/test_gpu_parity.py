@@ -286,28 +286,43 @@ def test_bf16_generate_graph_is_deterministic():
 @pytest.mark.parametrize("B", [1, 3, 8])
 def test_bf16_fused_step_matches_per_layer(B):
     """The persistent single-kernel decode step (ssd200_decode_step) against
-    the per-layer kernel sequence: same tokens, logits within fp32 rounding,
-    same in-place cache."""
+    the per-layer kernel sequences (streaming-GEMV layer, and the wide-batch
+    layer that is the default from B = 2: option 14): same tokens, logits
+    within fp32 rounding, same in-place cache."""
     import paper_2603_09555_b200 as m
+    from paper_2603_09555_b200 import _abi
 
     cfg = _bf16_cfg(n_layers=3)
     params = m.from_reference(m.random_init_host(cfg, 21), cfg)
     prompt = np.random.default_rng(22).integers(0, cfg.vocab_size, size=(B, 33))
     _, c0 = m.prefill(params, prompt, cfg, logits=None)
-    ca, cb = c0.copy(), c0.copy()
-    da = m.GreedyDecoder(params, cfg, ca, 12, keep_logits=True, use_graph=False, fused=True)
-    db = m.GreedyDecoder(params, cfg, cb, 12, keep_logits=True, use_graph=False, fused=False)
     first = torch.as_tensor(prompt[:, -1], device="cuda")
-    for d in (da, db):
-        d.tok.copy_(first)
-        d.step_idx.fill_(1)
-        for _ in range(10):
-            d.step()
-    assert torch.equal(da.tokens, db.tokens)
-    la, lb = da.kept[:, 1:11], db.kept[:, 1:11]
-    assert ((la - lb).norm() / lb.norm()).item() <= 1e-5
-    assert ((ca.ssm_all - cb.ssm_all).norm() / cb.ssm_all.norm()).item() <= 1e-5
-    assert torch.equal(ca.conv_all, cb.conv_all)
+    runs = []
+    try:
+        for wide_min, fused in ((9, True), (9, False), (2, False)):
+            _abi.lib().ssd200_set_option(14, wide_min)
+            c = c0.copy()
+            d = m.GreedyDecoder(params, cfg, c, 12, keep_logits=True, use_graph=False, fused=fused)
+            d.tok.copy_(first)
+            d.step_idx.fill_(1)
+            for _ in range(10):
+                d.step()
+            runs.append((d, c))
+    finally:
+        _abi.lib().ssd200_set_option(14, 2)
+    da, ca = runs[0]
+    # the streaming-GEMV layer does the fused step's arithmetic in the same order;
+    # the wide-batch layer's tensor-core GEMMs sum in another order, so a bf16
+    # rounding of an activation can flip: 1e-3, still 10x inside BF16_BOUND
+    for (db, cb), tol in zip(runs[1:], (1e-5, 1e-3)):
+        assert torch.equal(da.tokens, db.tokens)
+        la, lb = da.kept[:, 1:11], db.kept[:, 1:11]
+        assert ((la - lb).norm() / lb.norm()).item() <= tol
+        assert ((ca.ssm_all - cb.ssm_all).norm() / cb.ssm_all.norm()).item() <= tol
+        if tol == 1e-5:
+            assert torch.equal(ca.conv_all, cb.conv_all)
+        else:
+            assert ((ca.conv_all - cb.conv_all).norm() / cb.conv_all.norm()).item() <= tol
 
 
 @pytest.mark.parametrize("B,T", [(1, 1), (2, 2), (3, 5), (2, 125), (1, 253), (2, 600)])
