@@ -16,6 +16,7 @@
 #include "decode_mega.cuh"
 #include "ssd_tc.cuh"
 #include "tc_gemm.cuh"
+#include "decode_gemm.cuh"
 
 using namespace ssd200;
 
@@ -31,6 +32,7 @@ thread_local bool g_force_chunkscan = false;   // tests: exercise the fused stat
 thread_local bool g_chunkscan_mc = true;       // option 3: B-tile multicast in the chunk scan
 thread_local int g_out_waves = 1;              // option 4: target CTAs (x SMs) of the output kernel
 thread_local int g_stream_stages = 0, g_stream_cps = 0, g_stream_cw = 8;  // options 11 / 12 / 13
+thread_local bool g_dec_swap = true;           // option 15: swapped-operand decode GEMM (else tc_gemm)
 thread_local int g_wide_min = 2;               // option 14: smallest batch on the wide-batch decode path (measured: the per-layer path beats the fused step from B = 2)
 thread_local int g_mega_pf = 0;                // option 9: fused decode step L2 prefetch lookahead (stages)
 thread_local bool g_dec_pdl = true;            // option 8: PDL between the decode kernels
@@ -816,7 +818,7 @@ inline DecSplits dec_splits(const ssd200_dims_t *d, int B) {
     if (s > kb / 4) s = kb / 4;
     return (int)(s < 1 ? 1 : s);
   };
-  const long mt = (B + 127) / 128;
+  const long mt = B <= 256 ? 1 : (B + 127) / 128;  // dec_gemm_swap: one tile covers the batch
   DecSplits r;
   r.in = pick(mt * ((w.d_in_proj + 127) / 128), d->d_model);
   r.out = pick(mt * ((d->d_model + 127) / 128), d->d_inner);
@@ -961,6 +963,50 @@ int decode_layer_fast(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hi
   return launch_dec_stream<DEC_EPI_OUT>(o2, st);
 }
 
+// part[s, b, n] = sum_{k in range s} W[n, k] X[b, k] for decode batches: the
+// weight-streaming swapped-operand GEMM (decode_gemm.cuh) for B <= 256, else tc_gemm
+template <int BNB>
+int launch_dec_gemm_bnb(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long ldo,
+                        int ksplit, long split_stride, cudaStream_t st) {
+  using Cfg = DgCfg<BNB>;
+  CUtensorMap tw, tx;
+  int rc = make_map_2d(&tw, W, N, K, K, 128);
+  if (rc) return rc;
+  rc = make_map_2d(&tx, X, B, K, K, BNB);
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dec_gemm_swap<BNB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Cfg::SMEM);
+    attr = true;
+  }
+  DgArgs a{N, K, B, ksplit, out, ldo, split_stride};
+  const int grid = ((N + 127) / 128) * ksplit;
+  cudaError_t e = launch_pdl(dec_gemm_swap<BNB>, dim3(grid), dim3(192), Cfg::SMEM, st, tw, tx, a);
+  REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_gemm_swap: %s", cudaGetErrorString(e));
+  LAUNCH_CHECK("dec_gemm_swap");
+  return SSD200_OK;
+}
+
+int dec_gemm(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long ldo, int ksplit,
+             long split_stride, cudaStream_t st) {
+  REQUIRE(ksplit >= 1 && ksplit <= (K + 63) / 64, SSD200_EINVAL, "dec_gemm: bad split");
+  if (B <= 256 && g_dec_swap) {
+    if (B <= 16) return launch_dec_gemm_bnb<16>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
+    if (B <= 32) return launch_dec_gemm_bnb<32>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
+    if (B <= 64) return launch_dec_gemm_bnb<64>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
+    if (B <= 128)
+      return launch_dec_gemm_bnb<128>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
+    return launch_dec_gemm_bnb<256>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
+  }
+  TcEpilogue ep{};
+  ep.C = out;
+  ep.ldc = ldo;
+  ep.ksplit = ksplit;
+  ep.split_stride = split_stride;
+  return tc_gemm<TC_EPI_F32>(X, K, W, K, B, N, K, ep, st, true);
+}
+
 // wide-batch bf16 decode layer (B > DEC_MAX_B), 4 PDL-chained launches:
 //   tc_gemm F32 split-K in_proj -> dec_ssm_stream (TMA-pipelined conv + state
 //   update + gate + sum u^2) -> tc_gemm F32 split-K out_proj -> dec_out_finish
@@ -974,13 +1020,8 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   const DecSplits sp = dec_splits(d, B);
   const long s_in = (long)B * wd.d_in_proj, s_out = (long)B * d->d_model;
   {
-    TcEpilogue ep{};
-    ep.C = o.u;
-    ep.ldc = wd.d_in_proj;
-    ep.ksplit = sp.in;
-    ep.split_stride = s_in;
-    int rc = tc_gemm<TC_EPI_F32>(hidden_lp, d->d_model, static_cast<const bf16 *>(w->W_in),
-                                 d->d_model, B, (int)wd.d_in_proj, d->d_model, ep, st, true);
+    int rc = dec_gemm(static_cast<const bf16 *>(w->W_in), (int)wd.d_in_proj, d->d_model, hidden_lp,
+                      B, o.u, wd.d_in_proj, sp.in, s_in, st);
     if (rc) return rc;
   }
   DecStreamArgs sa{};
@@ -1048,13 +1089,8 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_ssm_stream: %s", cudaGetErrorString(e));
   LAUNCH_CHECK("dec_ssm_stream");
 
-  TcEpilogue er{};
-  er.C = o.part;
-  er.ldc = d->d_model;
-  er.ksplit = sp.out;
-  er.split_stride = s_out;
-  int rc = tc_gemm<TC_EPI_F32>(o.normed_lp, d->d_inner, static_cast<const bf16 *>(w->W_out),
-                               d->d_inner, B, d->d_model, d->d_inner, er, st, true);
+  int rc = dec_gemm(static_cast<const bf16 *>(w->W_out), d->d_model, d->d_inner, o.normed_lp, B,
+                    o.part, d->d_model, sp.out, s_out, st);
   if (rc) return rc;
   DecFinishArgs fa{};
   fa.part = o.part;
@@ -1231,7 +1267,7 @@ int head_bf16(const ssd200_dims_t *d, int V, const float *hidden, long hrs, cons
               const bf16 *E, float *logits, int64_t *amax, int rows, void *ws, size_t ws_bytes,
               cudaStream_t st) {
   Carve cv(ws, ws_bytes);
-  if (rows <= DEC_MAX_B && d->d_model % 256 == 0) {
+  if (rows <= DEC_MAX_B && d->d_model % 256 == 0 && !(g_dec_swap && d->d_model % 8 == 0)) {
     // fused final RMSNorm + tied-head GEMV + per-CTA argmax partials (decode.cuh)
     const int grid = num_sms();  // upper bound of launch_dec_stream's grid
     float *pv = cv.take<float>((size_t)grid * rows);
@@ -1270,7 +1306,11 @@ int head_bf16(const ssd200_dims_t *d, int V, const float *hidden, long hrs, cons
   rmsnorm_rows<float, bf16><<<rows, 256, 0, st>>>(hidden, hrs, fw, normed, d->d_model,
                                                   d->d_model, (float)d->norm_eps);
   LAUNCH_CHECK("rmsnorm_rows");
-  if (rows <= GEMV_MAX_ROWS) {
+  if (rows <= 256 && g_dec_swap && d->d_model % 8 == 0) {
+    // decode batches: the embedding streamed once as the UMMA M side (decode_gemm.cuh)
+    int rc = dec_gemm(E, V, d->d_model, normed, rows, lg, V, 1, 0, st);
+    if (rc) return rc;
+  } else if (rows <= GEMV_MAX_ROWS) {
     gemv_nk<float, bf16, bf16, EPI_STORE>
         <<<dim3(blocks_for(V, 32), blocks_for(rows, 4)), 256, 0, st>>>(
             normed, d->d_model, E, d->d_model, lg, V, nullptr, rows, V, d->d_model);
@@ -1688,6 +1728,9 @@ int ssd200_set_option(int option, int value) {
       return SSD200_OK;
     case 12:  // wide-batch decode stream: CTAs per SM (1 or 2; 0 = by tile count)
       g_stream_cps = value;
+      return SSD200_OK;
+    case 15:  // wide-batch decode GEMMs: swapped-operand weight-streaming kernel (1) or tc_gemm (0)
+      g_dec_swap = value != 0;
       return SSD200_OK;
     case 14:  // smallest batch that takes the wide-batch decode path (default 2)
       REQUIRE(value >= 1, SSD200_EINVAL, "option 14 out of range");
