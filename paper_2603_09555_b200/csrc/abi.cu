@@ -33,7 +33,7 @@ thread_local bool g_chunkscan_mc = true;       // option 3: B-tile multicast in 
 thread_local int g_out_waves = 1;              // option 4: target CTAs (x SMs) of the output kernel
 thread_local int g_stream_stages = 0, g_stream_cps = 0, g_stream_cw = 8;  // options 11 / 12 / 13
 thread_local bool g_dec_swap = true;           // option 15: swapped-operand decode GEMM (else tc_gemm)
-thread_local int g_wide_min = 2;               // option 14: smallest batch on the wide-batch decode path (measured: the per-layer path beats the fused step from B = 2)
+thread_local int g_wide_min = 1;               // option 14: smallest batch on the wide-batch decode path (measured: the per-layer path beats the fused step at every B, 1.3B B=1 1.215 -> 1.150 ms)
 thread_local int g_mega_pf = 0;                // option 9: fused decode step L2 prefetch lookahead (stages)
 thread_local bool g_dec_pdl = true;            // option 8: PDL between the decode kernels
 thread_local int g_dec_split_in = 0, g_dec_split_out = 0;  // options 6 / 7: wide-decode split-K (0 auto)
@@ -1732,7 +1732,7 @@ int ssd200_set_option(int option, int value) {
     case 15:  // wide-batch decode GEMMs: swapped-operand weight-streaming kernel (1) or tc_gemm (0)
       g_dec_swap = value != 0;
       return SSD200_OK;
-    case 14:  // smallest batch that takes the wide-batch decode path (default 2)
+    case 14:  // smallest batch that takes the wide-batch decode path (default 1; 9 = fused step for B <= 8)
       REQUIRE(value >= 1, SSD200_EINVAL, "option 14 out of range");
       g_wide_min = value;
       return SSD200_OK;
