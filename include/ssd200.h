@@ -109,6 +109,20 @@ int ssd200_resid_norm_finish(int d_model, int d_inner_full, double eps, void *hi
                              void *hidden_lp, const float *partial, long partial_ld, long rows,
                              ssd200_stream_t stream);
 
+/* ---- head-group-sharded decode_step layer (bf16) ----------
+ * As ssd200_prefill_layer_partial for one token per row: d / w describe THIS
+ * rank's shard (local heads a multiple of 4); the rank's cache slices
+ * (ssm (batch, H_local, P, N), conv (batch, conv_dim_local, k-1)) are updated
+ * (in place when aliased); hidden is NOT updated: partial[b, 0:d_model] =
+ * u_local . W_out'_local and partial[b, d_model] = sum u_local^2.  The caller
+ * sums partial over the ranks (one all-reduce) and applies
+ * ssd200_resid_norm_finish.  Workspace: ssd200_decode_layer_workspace(d, batch). */
+int ssd200_decode_layer_partial(const ssd200_dims_t *d, const ssd200_layer_t *w,
+                                const void *hidden_lp, float *partial, long partial_ld,
+                                const void *ssm_in, void *ssm_out, const void *conv_in,
+                                void *conv_out, int batch, void *workspace,
+                                size_t workspace_bytes, ssd200_stream_t stream);
+
 /* ---- one decode_step layer (decode.py:99-140) ----------------------------
  * ssm_out/conv_out may alias ssm_in/conv_in (in-place update for generate). */
 size_t ssd200_decode_layer_workspace(const ssd200_dims_t *d, int batch);

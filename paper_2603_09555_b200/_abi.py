@@ -76,6 +76,12 @@ SIGNATURES = [
          c_void_p, c_int, c_int, c_void_p, c_size_t, c_void_p],
     ),
     (
+        "ssd200_decode_layer_partial",
+        c_int,
+        [ctypes.POINTER(Dims), ctypes.POINTER(Layer), c_void_p, c_void_p, ctypes.c_long, c_void_p,
+         c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_size_t, c_void_p],
+    ),
+    (
         "ssd200_resid_norm_finish",
         c_int,
         [c_int, c_int, c_double, c_void_p, c_void_p, c_void_p, ctypes.c_long, ctypes.c_long, c_void_p],

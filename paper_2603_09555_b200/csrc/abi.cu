@@ -837,11 +837,11 @@ inline bool dec_big_eligible(const ssd200_dims_t *d) {
 
 template <typename T>
 bool carve_decode(const ssd200_dims_t *d, int B, void *ws, size_t cap, DecodeWs<T> &o,
-                  size_t *need) {
+                  size_t *need, bool force_big = false) {
   Widths w = widths(d);
   Carve cv(ws, cap);
-  const bool big = std::is_same<T, float>::value && d->dtype == SSD200_BF16 && B >= g_wide_min &&
-                   dec_big_eligible(d);
+  const bool big = std::is_same<T, float>::value && d->dtype == SSD200_BF16 &&
+                   (B >= g_wide_min || force_big) && dec_big_eligible(d);
   const DecSplits sp = big ? dec_splits(d, B) : DecSplits{1, 1};
   o.u = cv.take<T>((size_t)sp.in * B * w.d_in_proj);
   o.part = big ? cv.take<float>((size_t)sp.out * B * d->d_model) : nullptr;
@@ -1013,9 +1013,13 @@ int dec_gemm(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long
 //   (norm row scale + residual, B / C conv windows rolled).
 // Split-K keeps every SM streaming weights at B = 16..128, where the
 // (row tile x column tile) grid alone covers a fraction of the SMs.
+// pout != nullptr: head-group-sharded mode: hidden is not
+// updated; pout[b, :d_model] = the local out_proj partial, pout[b, d_model] =
+// the local sum of u^2, for the caller's all-reduce + ssd200_resid_norm_finish.
 int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hidden,
                      bf16 *hidden_lp, const float *ssm_in, float *ssm_out, const float *conv_in,
-                     float *conv_out, int B, DecodeWs<float> &o, cudaStream_t st) {
+                     float *conv_out, int B, DecodeWs<float> &o, cudaStream_t st,
+                     float *pout = nullptr, long pld = 0) {
   Widths wd = widths(d);
   const DecSplits sp = dec_splits(d, B);
   const long s_in = (long)B * wd.d_in_proj, s_out = (long)B * d->d_model;
@@ -1111,6 +1115,8 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   fa.conv_dim = (int)wd.conv_dim;
   fa.conv_in = conv_in;
   fa.conv_out = conv_out;
+  fa.pout = pout;
+  fa.pld = pld;
   const int gbx = (d->d_model + 255) / 256 + (int)((wd.conv_dim - d->d_inner + 255) / 256);
   e = launch_pdl(dec_out_finish, dim3(gbx, B), dim3(256), 0, st, fa);
   REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_out_finish: %s", cudaGetErrorString(e));
@@ -1487,10 +1493,35 @@ size_t ssd200_decode_layer_workspace(const ssd200_dims_t *d, int batch) {
     DecodeWs<double> o;
     carve_decode<double>(d, batch, nullptr, 0, o, &need);
   } else {
-    DecodeWs<float> o;
-    carve_decode<float>(d, batch, nullptr, 0, o, &need);
+    DecodeWs<float> o;  // the wide-batch carve is a superset (also covers the partial entry)
+    carve_decode<float>(d, batch, nullptr, 0, o, &need, true);
   }
   return need;
+}
+
+int ssd200_decode_layer_partial(const ssd200_dims_t *d, const ssd200_layer_t *w,
+                                const void *hidden_lp, float *partial, long partial_ld,
+                                const void *ssm_in, void *ssm_out, const void *conv_in,
+                                void *conv_out, int batch, void *workspace,
+                                size_t workspace_bytes, ssd200_stream_t stream) {
+  int rc = check_dims(d);
+  if (rc) return rc;
+  REQUIRE(d->dtype == SSD200_BF16 && dec_big_eligible(d), SSD200_EUNSUPPORTED,
+          "head-sharded decode needs bf16, conv_kernel 4, head_dim 16/32/64, local heads a "
+          "multiple of 4");
+  REQUIRE(batch >= 1 && batch <= 256, SSD200_EINVAL, "batch must be in [1, 256]");
+  REQUIRE(hidden_lp && partial && ssm_in && ssm_out && conv_in && conv_out, SSD200_EINVAL,
+          "null pointer");
+  REQUIRE(partial_ld >= d->d_model + 1 && partial_ld % 4 == 0, SSD200_EINVAL,
+          "partial_ld must be a multiple of 4 and >= d_model + 1");
+  DecodeWs<float> o;
+  size_t need = 0;
+  REQUIRE(carve_decode<float>(d, batch, workspace, workspace_bytes, o, &need, true),
+          SSD200_EWORKSPACE, "decode workspace %zu < %zu", workspace_bytes, need);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return decode_layer_big(d, w, nullptr, (bf16 *)hidden_lp, (const float *)ssm_in,
+                          (float *)ssm_out, (const float *)conv_in, (float *)conv_out, batch, o,
+                          st, partial, partial_ld);
 }
 
 int ssd200_decode_layer(const ssd200_dims_t *d, const ssd200_layer_t *w, void *hidden,

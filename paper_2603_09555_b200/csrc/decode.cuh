@@ -895,6 +895,9 @@ struct DecFinishArgs {
   int pnsplit, d_inner, conv_dim;
   const float *conv_in;
   float *conv_out;
+  // head-group-sharded mode: pout[b, :d_model] = partial, pout[b, d_model] = sum u^2
+  float *pout;
+  long pld;
 };
 __global__ __launch_bounds__(256) void dec_out_finish(DecFinishArgs a) {
   __shared__ float sc;
@@ -919,13 +922,20 @@ __global__ __launch_bounds__(256) void dec_out_finish(DecFinishArgs a) {
     float t = 0.f;
     for (int h = threadIdx.x; h < a.H; h += 32) t += a.ssq[(long)b * a.H + h];
     t = warp_sum(t);  // fixed shuffle tree: deterministic
-    if (threadIdx.x == 0) sc = 1.f / sqrtf(t * a.inv_d + a.eps);
+    if (threadIdx.x == 0) {
+      sc = 1.f / sqrtf(t * a.inv_d + a.eps);
+      if (a.pout && blockIdx.x == 0) a.pout[(long)b * a.pld + a.d_model] = t;
+    }
   }
   __syncthreads();
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= a.d_model) return;
   float acc = 0.f;
   for (int j = 0; j < a.nsplit; ++j) acc += a.part[j * a.sstride + (long)b * a.d_model + n];
+  if (a.pout) {
+    a.pout[(long)b * a.pld + n] = acc;
+    return;
+  }
   const long i = (long)b * a.d_model + n;
   const float v = a.hidden[i] + sc * acc;
   a.hidden[i] = v;

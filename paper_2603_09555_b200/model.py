@@ -122,6 +122,8 @@ class _Runner:
         return self._ws
 
     def embed(self, tok: torch.Tensor):
+        if tok.dtype != torch.int64 or not tok.is_contiguous():  # the C-ABI reads dense int64
+            tok = tok.to(torch.int64).contiguous()
         rows = tok.numel()
         cfg = self.cfg
         hidden = torch.empty((rows, cfg.d_model), dtype=self.sdt, device=self.dev)

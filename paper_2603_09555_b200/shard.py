@@ -256,10 +256,10 @@ class HeadShardedPrefill:
             "ssd200_resid_norm_finish",
         )
 
-    def logits(self) -> torch.Tensor:
+    def logits(self, argmax: torch.Tensor | None = None) -> torch.Tensor:
         cfg = self.cfg
         out = torch.empty((self.B, cfg.vocab_size), dtype=torch.float32, device=self.r.dev)
-        self.r.head(self.hidden, self.T * cfg.d_model, self.B, logits=out,
+        self.r.head(self.hidden, self.T * cfg.d_model, self.B, logits=out, argmax=argmax,
                     base_offset=(self.T - 1) * cfg.d_model)
         return out
 
@@ -279,3 +279,105 @@ def prefill_head_sharded(shard_params, tokens, cfg: ModelConfig, group=None):
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
         run.finish()
     return run.logits(), run.ssm
+
+
+# ------------------------------------------------------------------ head-group-sharded decode
+
+
+class HeadShardedDecoder:
+    """One rank's side of head-group-sharded greedy decoding (decode.py:77-194):
+    the rank keeps its heads' slice of the cache (SSM states (n_layers, B,
+    H_local, P, N), conv windows over its x channels + the replicated B / C
+    channels) and, per token, per layer, runs ``ssd200_decode_layer_partial``
+    into ``buf`` = ``[partial (B, d_model) | sum u^2]``; the caller sums ``buf``
+    over the ranks (one all-reduce per layer, as in prefill) and calls
+    ``finish()``; the final norm + tied head + argmax are replicated.
+
+    Build it from a finished ``HeadShardedPrefill`` (its states become the
+    cache) or from explicit cache tensors."""
+
+    def __init__(self, shard_params, cfg: ModelConfig, ssm: torch.Tensor, conv: torch.Tensor):
+        from .model import _Runner, layer_struct
+
+        self.cfg, self.params = cfg, shard_params
+        self.r = r = _Runner(shard_params, cfg)
+        local = shard_params.local
+        self.dims_l = _local_dims_struct(cfg, local)
+        self.layers = [layer_struct(lp) for lp in shard_params.layers]
+        self.ssm, self.conv = ssm, conv  # updated in place
+        self.B = ssm.shape[1]
+        self.ld = (cfg.d_model + 4) // 4 * 4
+        self.buf = torch.empty((self.B, self.ld), dtype=torch.float32, device=r.dev)
+        self.ws = r.workspace(r.lib.ssd200_decode_layer_workspace(self.dims_l, self.B))
+        self.hidden = self.lp = None
+
+    @classmethod
+    def from_prefill(cls, run: "HeadShardedPrefill"):
+        return cls(run.params, run.cfg, run.ssm, run.conv)
+
+    def begin(self, tok: torch.Tensor):
+        """Embed this step's tokens (B,) — replicated on every rank."""
+        self.hidden, self.lp = self.r.embed(tok.reshape(-1))
+
+    def partial(self, i: int) -> torch.Tensor:
+        from . import _abi
+
+        r = self.r
+        _abi.check(
+            r.lib.ssd200_decode_layer_partial(
+                self.dims_l, self.layers[i], self.lp.data_ptr(), self.buf.data_ptr(), self.ld,
+                self.ssm[i].data_ptr(), self.ssm[i].data_ptr(), self.conv[i].data_ptr(),
+                self.conv[i].data_ptr(), self.B, self.ws.data_ptr(), self.ws.numel(), r.stream,
+            ),
+            "ssd200_decode_layer_partial",
+        )
+        return self.buf
+
+    def finish(self):
+        from . import _abi
+
+        cfg, r = self.cfg, self.r
+        _abi.check(
+            r.lib.ssd200_resid_norm_finish(
+                cfg.d_model, cfg.d_inner, float(cfg.norm_eps), self.hidden.data_ptr(),
+                self.lp.data_ptr(), self.buf.data_ptr(), self.ld, self.B, r.stream,
+            ),
+            "ssd200_resid_norm_finish",
+        )
+
+    def logits_and_pick(self):
+        """Replicated final RMSNorm + tied head + greedy pick (ties -> lowest id)."""
+        cfg = self.cfg
+        out = torch.empty((self.B, cfg.vocab_size), dtype=torch.float32, device=self.r.dev)
+        pick = torch.empty((self.B,), dtype=torch.int64, device=self.r.dev)
+        self.r.head(self.hidden, cfg.d_model, self.B, logits=out, argmax=pick)
+        return out, pick
+
+
+def generate_head_sharded(shard_params, prompt, gen_len: int, cfg: ModelConfig, group=None):
+    """Head-group-sharded cached ``generate`` (decode.py:147-194) for this rank:
+    a head-sharded prefill of the prompt, then gen_len - 1 decode steps; per
+    layer of every step ONE all-reduce (sum) of ``[partial | sum u^2]``.
+    Returns the (B, gen_len) greedy tokens (replicated on every rank)."""
+    import torch.distributed as dist
+
+    if gen_len < 1:
+        raise ValueError("gen_len must be >= 1")
+    run = HeadShardedPrefill(shard_params, prompt, cfg)
+    for i in range(cfg.n_layers):
+        buf = run.partial(i)
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+        run.finish()
+    tok = torch.empty((run.B,), dtype=torch.int64, device=run.r.dev)
+    run.logits(argmax=tok)  # greedy pick, ties -> lowest id (decode.py:72-74)
+    tokens = [tok]
+    dec = HeadShardedDecoder.from_prefill(run)
+    for _ in range(gen_len - 1):
+        dec.begin(tok)
+        for i in range(cfg.n_layers):
+            buf = dec.partial(i)
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+            dec.finish()
+        _, tok = dec.logits_and_pick()
+        tokens.append(tok)
+    return torch.stack(tokens, dim=1)

@@ -408,6 +408,53 @@ def test_bf16_head_sharded_prefill_matches_unsharded(world):
             assert (torch.linalg.norm(a - b) / torch.linalg.norm(b)).item() <= BF16_BOUND
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_bf16_head_sharded_decode_matches_unsharded(world):
+    """Head-group-sharded decode: simulated ranks run their heads
+    of every layer (ssd200_decode_layer_partial), the [partial | sum u^2]
+    buffers are summed (the all-reduce) and finished on every rank.  Fed the
+    unsharded run's tokens, each step's logits match the unsharded bf16
+    decode within the bf16 bound, and the greedy picks agree."""
+    import paper_2603_09555_b200 as m
+    from paper_2603_09555_b200 import shard
+
+    d_model = 256 * world  # 8 heads of 64 per rank (the sharded prefill needs multiples of 8)
+    cfg = m.ModelConfig(vocab_size=1024, d_model=d_model, n_layers=2, norm_eps=1e-5).with_policy(
+        compute="bf16")
+    host = m.random_init_host(cfg, 23)
+    rng = np.random.default_rng(5)
+    for lp in host.layers:
+        lp.norm_w = (1.0 + 0.2 * rng.standard_normal(cfg.d_inner)).astype(np.float32)
+    prompt = rng.integers(0, cfg.vocab_size, size=(3, 40))
+    G = 6
+    ref = m.generate(m.from_reference(host, cfg), prompt, G, cfg=cfg, keep_logits=True)
+    runs = [shard.HeadShardedPrefill(shard.upload_shard(host, cfg, r, world), prompt, cfg)
+            for r in range(world)]
+    for i in range(cfg.n_layers):
+        total = sum(run.partial(i).clone() for run in runs)
+        for run in runs:
+            run.buf.copy_(total)
+            run.finish()
+    decs = [shard.HeadShardedDecoder.from_prefill(run) for run in runs]
+    for g in range(1, G):
+        tok = ref.tokens[:, g - 1]
+        for dec in decs:
+            dec.begin(tok)
+        for i in range(cfg.n_layers):
+            total = sum(dec.partial(i).clone() for dec in decs)  # the all-reduce
+            for dec in decs:
+                dec.buf.copy_(total)
+                dec.finish()
+        outs = [dec.logits_and_pick() for dec in decs]
+        for lg, pk in outs[1:]:
+            assert torch.equal(lg, outs[0][0]) and torch.equal(pk, outs[0][1])  # replicated
+        got, pick = outs[0]
+        want = ref.per_step_logits[:, g]
+        rel = (torch.linalg.norm(got - want) / torch.linalg.norm(want)).item()
+        assert rel <= BF16_BOUND, (g, rel)
+        assert torch.equal(pick, ref.tokens[:, g]), g
+
+
 @pytest.mark.parametrize("B", [9, 16])
 def test_bf16_wide_batch_decode_state_vs_oracle(B):
     """Wide-batch decode (B > 8: tensor-core in_proj, fused SSM update + gate +

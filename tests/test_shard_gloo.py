@@ -161,3 +161,68 @@ def _head_block_worker(rank, world):
 
 def test_head_sharded_block_gloo():
     _run(_head_block_worker, 2)
+
+
+def _head_sharded_decode_layer(lay, hidden, ssm, conv, cfg):
+    """One rank's part of a head-sharded decode layer (decode.py:99-140 on its
+    heads): returns (partial, sum u^2, new ssm slice, new conv slice)."""
+    d = lay.dims
+    P, N, G = cfg.head_dim, cfg.d_state, cfg.n_groups
+    nb = hidden.shape[0]
+    proj = hidden @ lay.W_in
+    z = proj[:, : d.d_inner]
+    col = proj[:, d.d_inner: d.d_inner + d.conv_dim]
+    dt_raw = proj[:, d.d_inner + d.conv_dim:]
+    window = np.concatenate([conv, col[:, :, None]], axis=2)  # roll_and_insert, decode.py:65-69
+    act = orc.silu(np.einsum("bck,ck->bc", window, lay.conv_w) + lay.conv_b)
+    x = act[:, : d.d_inner].reshape(nb, d.n_heads, P)
+    rep = d.n_heads // G
+    Bh = np.repeat(act[:, d.d_inner: d.d_inner + G * N].reshape(nb, G, N), rep, 1)
+    Ch = np.repeat(act[:, d.d_inner + G * N:].reshape(nb, G, N), rep, 1)
+    dt = orc.step_sizes(dt_raw[:, None, :], lay.dt_bias, cfg.dt_limits, hidden.dtype)[:, 0, :]
+    a = orc.decay_scalar(lay.A_log, hidden.dtype)
+    h = np.exp(a * dt)[:, :, None, None] * ssm + dt[:, :, None, None] * x[..., None] * Bh[:, :, None]
+    y = np.einsum("bhn,bhpn->bhp", Ch, h) + lay.D[None, :, None] * x
+    u = y.reshape(nb, d.d_inner) * orc.silu(z)
+    return u @ (lay.norm_w[:, None] * lay.W_out), np.sum(u * u, axis=-1), h, window[:, :, 1:]
+
+
+def _head_decode_worker(rank, world):
+    """Head-sharded decode step: each rank updates only its heads'
+    cache slice and contributes [partial | sum u^2] to ONE all-reduce per layer;
+    the logits equal the unsharded oracle decode_step."""
+    cfg = small_config(d_model=32, head_dim=8, chunk_size=8).with_policy(compute="f64")
+    host = random_init_host(cfg, 6)
+    rng = np.random.default_rng(2)
+    for layer in host.layers:
+        layer.norm_w = 1.0 + 0.3 * rng.standard_normal(cfg.d_inner)
+    B, P = 3, cfg.head_dim
+    tok = rng.integers(0, cfg.vocab_size, size=B)
+    conv_dim = cfg.d_inner + 2 * cfg.n_groups * cfg.d_state
+    ssm = [rng.standard_normal((B, cfg.n_heads, P, cfg.d_state)) for _ in host.layers]
+    conv = [rng.standard_normal((B, conv_dim, cfg.conv_kernel - 1)) for _ in host.layers]
+    hidden = np.asarray(host.embedding, dtype=np.float64)[tok]
+    for i, layer in enumerate(host.layers):
+        lay = shard.shard_layer_by_heads(layer, cfg, rank, world)
+        hs = lay.heads
+        ch = slice(hs.start * P, hs.stop * P)
+        conv_l = np.concatenate([conv[i][:, ch], conv[i][:, cfg.d_inner:]], axis=1)
+        partial, ssq, h_new, c_new = _head_sharded_decode_layer(lay, hidden, ssm[i][:, hs],
+                                                                conv_l, cfg)
+        buf = torch.from_numpy(np.concatenate([partial, ssq[:, None]], axis=-1).copy())
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM)
+        buf = buf.numpy()
+        hidden = hidden + buf[:, :-1] / np.sqrt(buf[:, -1] / cfg.d_inner + cfg.norm_eps)[:, None]
+        _, ref_ssm, ref_conv = orc.decode_step(host, ssm, conv, tok, cfg)
+        assert np.max(np.abs(h_new - ref_ssm[i][:, hs])) < 1e-12 or i > 0
+        if i == 0:
+            assert np.max(np.abs(c_new[:, : ch.stop - ch.start] - ref_conv[0][:, ch])) == 0
+    emb = np.asarray(host.embedding, dtype=np.float64)
+    logits = orc.rms_norm(hidden, host.final_norm_w, cfg.norm_eps) @ emb.T
+    ref, _, _ = orc.decode_step(host, ssm, conv, tok, cfg)
+    err = np.max(np.abs(logits - ref)) / np.max(np.abs(ref))
+    assert err < 1e-12, err
+
+
+def test_head_sharded_decode_gloo():
+    _run(_head_decode_worker, 2)
