@@ -482,3 +482,18 @@ def test_bf16_wide_batch_decode_state_vs_oracle(B):
     b = m.generate(params, toks[:, :29], 6, cfg=cfg, use_graph=False, keep_logits=True)
     assert torch.equal(a.tokens, b.tokens)
     assert torch.equal(a.per_step_logits, b.per_step_logits)
+
+
+def test_bf16_decode_batch_invariance_bitwise():
+    """bf16 decode rows do not depend on the batch they run in (the decode GEMMs'
+    split-K factors depend only on the widths for B <= 256): the basis of batch
+    sharding for decode."""
+    import paper_2603_09555_b200 as m
+
+    cfg = _bf16_cfg()
+    params = m.from_reference(m.random_init_host(cfg, 51), cfg)
+    toks = np.random.default_rng(52).integers(0, cfg.vocab_size, size=(6, 24))
+    full = m.generate(params, toks, 5, cfg=cfg, keep_logits=True)
+    part = m.generate(params, toks[2:4], 5, cfg=cfg, keep_logits=True)
+    assert torch.equal(full.tokens[2:4], part.tokens)
+    assert torch.equal(full.per_step_logits[2:4, 1:], part.per_step_logits[:, 1:])
