@@ -8,6 +8,18 @@ in and out.  Every FLOP runs in hand-written CUDA (libssd200.so, C ABI in
 include/ssd200.h); there is no CPU fallback.
 """
 
+from .bundle import (
+    BundleError,
+    FormatVersionError,
+    MissingTensorError,
+    PayloadError,
+    TensorShapeError,
+    load_bundle,
+    load_bundle_host,
+    save_bundle,
+    tensor_names,
+    tensor_shape,
+)
 from .cache import GenerationResult, Mamba2Cache
 from .config import MODEL_SIZES, ElemPolicy, ModelConfig, named_config
 from .cost import (
@@ -38,6 +50,16 @@ from .ssd import ChunkPlan, SsdInputs, SsdOutputs, plan_chunks, ssd_forward
 __version__ = "0.1.0"
 
 __all__ = [
+    "BundleError",
+    "FormatVersionError",
+    "MissingTensorError",
+    "PayloadError",
+    "TensorShapeError",
+    "load_bundle",
+    "load_bundle_host",
+    "save_bundle",
+    "tensor_names",
+    "tensor_shape",
     "ChunkPlan",
     "DeviceSpec",
     "ElemPolicy",

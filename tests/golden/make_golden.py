@@ -14,6 +14,10 @@ Fixtures written next to this script:
                     (seed 0), generate(gen_len=65) tokens + logits.
   weights_digest.npz per-tensor float64 sums of random_init weights, pinning
                     the Philox draw order of our re-implementation.
+  ref_bundle/       manifest.json + data.bin written by the reference's
+                    save_bundle (bundle.py:134-168) for random_init(small
+                    config with d_model 16, 1 layer, seed 9): pins the bundle
+                    format byte for byte.
 """
 
 from __future__ import annotations
@@ -182,8 +186,13 @@ def gen_digest():
     np.savez_compressed(os.path.join(HERE, "weights_digest.npz"), **out)
 
 
+def gen_bundle():
+    cfg = small_config(d_model=16, n_layers=1, vocab_size=32)
+    se.save_bundle(se.random_init(cfg, 9), cfg, os.path.join(HERE, "ref_bundle"))
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["ssd", "small", "digest", "c1"]
+    which = sys.argv[1:] or ["ssd", "small", "digest", "c1", "bundle"]
     if "ssd" in which:
         gen_ssd_cases()
     if "small" in which:
@@ -192,4 +201,6 @@ if __name__ == "__main__":
         gen_digest()
     if "c1" in which:
         gen_c1()
+    if "bundle" in which:
+        gen_bundle()
     print("golden fixtures written to", HERE)
