@@ -32,6 +32,8 @@ thread_local bool g_force_chunkscan = false;   // tests: exercise the fused stat
 thread_local bool g_chunkscan_mc = true;       // option 3: B-tile multicast in the chunk scan
 thread_local int g_out_waves = 1;              // option 4: target CTAs (x SMs) of the output kernel
 thread_local int g_stream_stages = 0, g_stream_cps = 0, g_stream_cw = 8;  // options 11 / 12 / 13
+thread_local int g_dec_gemm_small = -1;        // option 17: decode GEMM ~96 KB ring (two CTAs per SM); -1 auto
+thread_local int g_dec_skip = 0;               // option 16: profiling only — skip decode kernels (bit mask)
 thread_local bool g_dec_swap = true;           // option 15: swapped-operand decode GEMM (else tc_gemm)
 thread_local int g_wide_min = 1;               // option 14: smallest batch on the wide-batch decode path (measured: the per-layer path beats the fused step at every B, 1.3B B=1 1.215 -> 1.150 ms)
 thread_local int g_mega_pf = 0;                // option 9: fused decode step L2 prefetch lookahead (stages)
@@ -821,6 +823,11 @@ inline DecSplits dec_splits(const ssd200_dims_t *d, int B) {
   const long mt = B <= 256 ? 1 : (B + 127) / 128;  // dec_gemm_swap: one tile covers the batch
   DecSplits r;
   r.in = pick(mt * ((w.d_in_proj + 127) / 128), d->d_model);
+  if (B <= 64 && g_dec_gemm_small != 0) {  // two CTAs per SM: twice the units
+    const int s2 = 2 * ((int)num_sms() / (int)((w.d_in_proj + 127) / 128));
+    const int cap = (d->d_model + 63) / 64 / 4;
+    r.in = s2 < 1 ? 1 : (s2 > cap ? cap : s2);
+  }
   r.out = pick(mt * ((d->d_model + 127) / 128), d->d_inner);
   if (g_dec_split_in > 0 && g_dec_split_in <= (d->d_model + 63) / 64) r.in = g_dec_split_in;
   if (g_dec_split_out > 0 && g_dec_split_out <= (d->d_inner + 63) / 64) r.out = g_dec_split_out;
@@ -965,10 +972,10 @@ int decode_layer_fast(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hi
 
 // part[s, b, n] = sum_{k in range s} W[n, k] X[b, k] for decode batches: the
 // weight-streaming swapped-operand GEMM (decode_gemm.cuh) for B <= 256, else tc_gemm
-template <int BNB>
-int launch_dec_gemm_bnb(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long ldo,
+template <int BNB, bool SMALL>
+int launch_dec_gemm_cfg(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long ldo,
                         int ksplit, long split_stride, cudaStream_t st) {
-  using Cfg = DgCfg<BNB>;
+  using Cfg = DgCfg<BNB, SMALL>;
   CUtensorMap tw, tx;
   int rc = make_map_2d(&tw, W, N, K, K, 128);
   if (rc) return rc;
@@ -976,16 +983,27 @@ int launch_dec_gemm_bnb(const bf16 *W, int N, int K, const bf16 *X, int B, float
   if (rc) return rc;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(dec_gemm_swap<BNB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(dec_gemm_swap<BNB, SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Cfg::SMEM);
     attr = true;
   }
   DgArgs a{N, K, B, ksplit, out, ldo, split_stride};
   const int grid = ((N + 127) / 128) * ksplit;
-  cudaError_t e = launch_pdl(dec_gemm_swap<BNB>, dim3(grid), dim3(192), Cfg::SMEM, st, tw, tx, a);
+  cudaError_t e =
+      launch_pdl(dec_gemm_swap<BNB, SMALL>, dim3(grid), dim3(192), Cfg::SMEM, st, tw, tx, a);
   REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_gemm_swap: %s", cudaGetErrorString(e));
   LAUNCH_CHECK("dec_gemm_swap");
   return SSD200_OK;
+}
+template <int BNB>
+int launch_dec_gemm_bnb(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long ldo,
+                        int ksplit, long split_stride, cudaStream_t st) {
+  // the small ring (two CTAs per SM) measured faster up to B = 64 (B = 1: 1.18 -> 1.06 ms
+  // with the in_proj split 4), slower at B = 256
+  const bool small = g_dec_gemm_small < 0 ? B <= 64 : g_dec_gemm_small != 0;
+  return small
+             ? launch_dec_gemm_cfg<BNB, true>(W, N, K, X, B, out, ldo, ksplit, split_stride, st)
+             : launch_dec_gemm_cfg<BNB, false>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
 }
 
 int dec_gemm(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long ldo, int ksplit,
@@ -1023,7 +1041,7 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   Widths wd = widths(d);
   const DecSplits sp = dec_splits(d, B);
   const long s_in = (long)B * wd.d_in_proj, s_out = (long)B * d->d_model;
-  {
+  if (!(g_dec_skip & 1)) {
     int rc = dec_gemm(static_cast<const bf16 *>(w->W_in), (int)wd.d_in_proj, d->d_model, hidden_lp,
                       B, o.u, wd.d_in_proj, sp.in, s_in, st);
     if (rc) return rc;
@@ -1085,6 +1103,7 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
     }                                                                                          \
     e = launch_pdl(dec_ssm_stream<NQ, RPW, CW>, dim3(grid), dim3(CW * 32 + 32), smem, st, sa); \
   }
+  if (g_dec_skip & 2) e = cudaSuccess; else
   DSS_CASE(1, 1, 8) DSS_CASE(1, 2, 8) DSS_CASE(1, 4, 8) DSS_CASE(1, 8, 8)
   DSS_CASE(2, 1, 8) DSS_CASE(2, 2, 8) DSS_CASE(2, 4, 8) DSS_CASE(2, 8, 8)
   DSS_CASE(1, 1, 16) DSS_CASE(1, 2, 16) DSS_CASE(1, 4, 16)
@@ -1093,7 +1112,7 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_ssm_stream: %s", cudaGetErrorString(e));
   LAUNCH_CHECK("dec_ssm_stream");
 
-  int rc = dec_gemm(static_cast<const bf16 *>(w->W_out), d->d_model, d->d_inner, o.normed_lp, B,
+  int rc = (g_dec_skip & 4) ? 0 : dec_gemm(static_cast<const bf16 *>(w->W_out), d->d_model, d->d_inner, o.normed_lp, B,
                     o.part, d->d_model, sp.out, s_out, st);
   if (rc) return rc;
   DecFinishArgs fa{};
@@ -1118,7 +1137,7 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   fa.pout = pout;
   fa.pld = pld;
   const int gbx = (d->d_model + 255) / 256 + (int)((wd.conv_dim - d->d_inner + 255) / 256);
-  e = launch_pdl(dec_out_finish, dim3(gbx, B), dim3(256), 0, st, fa);
+  e = (g_dec_skip & 8) ? cudaSuccess : launch_pdl(dec_out_finish, dim3(gbx, B), dim3(256), 0, st, fa);
   REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_out_finish: %s", cudaGetErrorString(e));
   LAUNCH_CHECK("dec_out_finish");
   return SSD200_OK;
@@ -1759,6 +1778,12 @@ int ssd200_set_option(int option, int value) {
       return SSD200_OK;
     case 12:  // wide-batch decode stream: CTAs per SM (1 or 2; 0 = by tile count)
       g_stream_cps = value;
+      return SSD200_OK;
+    case 17:  // decode GEMMs: ~96 KB smem ring so consecutive kernels share SMs (1), 192 KB (0), auto (-1)
+      g_dec_gemm_small = value != 0;
+      return SSD200_OK;
+    case 16:  // profiling only: skip wide-decode kernels (1 in_proj, 2 stream, 4 out_proj, 8 finish)
+      g_dec_skip = value;
       return SSD200_OK;
     case 15:  // wide-batch decode GEMMs: swapped-operand weight-streaming kernel (1) or tc_gemm (0)
       g_dec_swap = value != 0;

@@ -21,13 +21,15 @@
 
 namespace ssd200 {
 
-template <int BNB> struct DgCfg {
+// SMALL: a ~96 KB ring so that two CTAs (this GEMM's and the next kernel's)
+// can share an SM and the next one's weight prefetch overlaps this one's tail
+template <int BNB, bool SMALL = false> struct DgCfg {
   static constexpr int BM = 128, BK = 64;
   static constexpr uint32_t A_BYTES = BM * BK * 2;   // 16 KB weight tile
   static constexpr uint32_t B_BYTES = BNB * BK * 2;  // activation tile
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (int)((192u * 1024u) / STAGE_BYTES) > 8 ? 8
-                                : (int)((192u * 1024u) / STAGE_BYTES);
+  static constexpr uint32_t BUDGET = SMALL ? 96u * 1024u : 192u * 1024u;
+  static constexpr int STAGES = (int)(BUDGET / STAGE_BYTES) > 8 ? 8 : (int)(BUDGET / STAGE_BYTES);
   static constexpr int TMEM_COLS = BNB < 32 ? 32 : BNB;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
 };
@@ -39,11 +41,11 @@ struct DgArgs {
   long ldo, split_stride;
 };
 
-template <int BNB>
+template <int BNB, bool SMALL = false>
 __global__ void __launch_bounds__(192, 1)
     dec_gemm_swap(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                   DgArgs a) {
-  using Cfg = DgCfg<BNB>;
+  using Cfg = DgCfg<BNB, SMALL>;
   constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
