@@ -184,7 +184,16 @@ int ssd200_debug_trace(void *device_buffer);
  * B tile across 4-CTA clusters by TMA multicast in that kernel (1, default)
  * or load it per CTA (0); option 4 = output-kernel CTA target in multiples of
  * the SM count (head-group split, default 1); option 5 = programmatic
- * dependent launch between the prefill kernels (0 default, 1 on). */
+ * dependent launch between the prefill kernels (0 default, 1 on).
+ * Decode (bf16): options 6 / 7 = in_proj / out_proj split-K factor (0 auto);
+ * 8 = PDL between the decode kernels (1 default); 9 = fused step's L2
+ * prefetch lookahead in ring stages (0 default); 11 / 12 / 13 = state-stream
+ * ring stages (0 = as many as fit) / CTAs per SM (0 auto, 1, 2) / consumer
+ * warps (8 default, 16); 14 = smallest batch on the per-layer wide path (1
+ * default; 9 = fused persistent step for B <= 8); 15 = swapped-operand decode
+ * GEMMs (1 default) or tc_gemm (0); 16 = profiling only: skip decode kernels
+ * (bit mask 1 in_proj, 2 stream, 4 out_proj, 8 finish); 17 = decode-GEMM
+ * ~96 KB ring, two CTAs per SM (-1 auto: B <= 64, 0, 1). */
 int ssd200_set_option(int option, int value);
 
 #ifdef __cplusplus
