@@ -231,8 +231,9 @@ int tc_gemm(const bf16 *A, long lda, const bf16 *B, long ldb, int M, int N, int 
   if (EPI == TC_EPI_F32 && ep.ksplit > 1)  // split-K: always 128-wide tiles (most tiles)
     return launch_tc_gemm_bn<128, EPI>(A, lda, B, ldb, M, N, K, ep, st, pdl);
   // 128-wide tiles when 256-wide ones would leave SMs idle (few row tiles: decode batches)
+  // (prefill at B = 1 / short T: the out_proj's 256-wide tiles covered 64 of 148 SMs)
   const long tiles256 = (long)((M + 127) / 128) * ((N + 255) / 256);
-  if (N <= 128 || (EPI == TC_EPI_F32 && tiles256 < num_sms()))
+  if (N <= 128 || (EPI != TC_EPI_INPROJ_CONV && tiles256 < num_sms()))
     return launch_tc_gemm_bn<128, EPI>(A, lda, B, ldb, M, N, K, ep, st, pdl);
   return launch_tc_gemm_bn<256, EPI>(A, lda, B, ldb, M, N, K, ep, st, pdl);
 }
