@@ -520,3 +520,13 @@ def test_bf16_prefill_production_width_vs_oracle(B, T):
     rs = np.stack(ref_ssm)
     rel_s = np.linalg.norm(_np(cache.ssm_all) - rs) / np.linalg.norm(rs)
     assert rel_s <= BF16_BOUND, rel_s
+
+
+def test_verify_suites_pass():
+    """The reference's verify suites (verify.py:22) ported to the GPU path."""
+    from paper_2603_09555_b200 import verify
+
+    results = verify.run_verify()
+    assert [r.suite for r in results] == list(verify.SUITES)
+    bad = [r.to_dict() for r in results if not r.passed]
+    assert not bad, bad
