@@ -828,7 +828,8 @@ inline DecSplits dec_splits(const ssd200_dims_t *d, int B) {
   r.in = pick(mt * ((w.d_in_proj + 127) / 128), d->d_model);
   if (B <= 64 && g_dec_gemm_small != 0) {  // two CTAs per SM: twice the units
     const int s2 = 2 * ((int)num_sms() / (int)((w.d_in_proj + 127) / 128));
-    const int cap = (d->d_model + 63) / 64 / 4;
+    int cap = (d->d_model + 63) / 64 / 4;
+    if (cap < 1) cap = 1;
     r.in = s2 < 1 ? 1 : (s2 > cap ? cap : s2);
   }
   r.out = pick(mt * ((d->d_model + 127) / 128), d->d_inner);
