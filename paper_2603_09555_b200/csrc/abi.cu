@@ -1107,11 +1107,14 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
     }                                                                                          \
     e = launch_pdl(dec_ssm_stream<NQ, RPW, CW>, dim3(grid), dim3(CW * 32 + 32), smem, st, sa); \
   }
-  if (g_dec_skip & 2) e = cudaSuccess; else
-  DSS_CASE(1, 1, 8) DSS_CASE(1, 2, 8) DSS_CASE(1, 4, 8) DSS_CASE(1, 8, 8)
-  DSS_CASE(2, 1, 8) DSS_CASE(2, 2, 8) DSS_CASE(2, 4, 8) DSS_CASE(2, 8, 8)
-  DSS_CASE(1, 1, 16) DSS_CASE(1, 2, 16) DSS_CASE(1, 4, 16)
-  DSS_CASE(2, 1, 16) DSS_CASE(2, 2, 16) DSS_CASE(2, 4, 16)
+  if (g_dec_skip & 2) {
+    e = cudaSuccess;
+  } else {
+    DSS_CASE(1, 1, 8) DSS_CASE(1, 2, 8) DSS_CASE(1, 4, 8) DSS_CASE(1, 8, 8)
+    DSS_CASE(2, 1, 8) DSS_CASE(2, 2, 8) DSS_CASE(2, 4, 8) DSS_CASE(2, 8, 8)
+    DSS_CASE(1, 1, 16) DSS_CASE(1, 2, 16) DSS_CASE(1, 4, 16)
+    DSS_CASE(2, 1, 16) DSS_CASE(2, 2, 16) DSS_CASE(2, 4, 16)
+  }
 #undef DSS_CASE
   REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_ssm_stream: %s", cudaGetErrorString(e));
   LAUNCH_CHECK("dec_ssm_stream");
