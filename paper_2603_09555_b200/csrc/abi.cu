@@ -1077,13 +1077,13 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   sa.ssq = o.ssq;
   const DssLayout lay(d->head_dim, d->d_state, sp.in);
   sa.stage_bytes = lay.total;
-  // CTAs per SM: two independent pipelines per SM stream faster once every CTA
-  // has enough tiles to amortise its pipeline fill (measured: B = 256 at 1.3B
-  // 12.1 -> 10.9 ms/step; B <= 64 slightly slower)
+  // CTAs per SM: two independent pipelines per SM (measured at 1.3B with the
+  // small-ring decode GEMMs: B = 8 1.42 -> 1.29, B = 64 3.97 -> 3.51, B = 256
+  // 12.1 -> 10.9 ms/step; neutral at B = 1, where there are fewer tiles than SMs)
   const int ntiles_all = B * d->n_heads;
   const int cps = g_stream_cps == 1 ? 1
                   : g_stream_cps == 2 ? 2
-                  : (ntiles_all >= 48 * num_sms() ? 2 : 1);
+                  : (ntiles_all >= 2 * num_sms() ? 2 : 1);
   int stages = (int)((cps == 2 ? 105u * 1024u : 214u * 1024u) / lay.total);
   if (g_stream_stages > 0 && g_stream_stages < stages) stages = g_stream_stages;
   sa.stages = stages > DSS_MAX_STAGES ? DSS_MAX_STAGES : stages;
