@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--seqlen", type=int, default=8192)
     ap.add_argument("--decode-model", default="1.3b")
     ap.add_argument("--decode-batch", type=int, default=1)
-    ap.add_argument("--decode-sweep", default="8,64,256",
+    ap.add_argument("--decode-sweep", default="2,8,16,64,128,256",
                     help="extra decode batch sizes reported under decode.sweep ('' = none)")
     ap.add_argument("--decode-steps", type=int, default=64)
     ap.add_argument("--no-decode", action="store_true")
