@@ -35,6 +35,7 @@ thread_local int g_stream_stages = 0, g_stream_cps = 0, g_stream_cw = 8;  // opt
 thread_local int g_dec_gemm_small = -1;        // option 17: decode GEMM ~96 KB ring (two CTAs per SM); -1 auto
 thread_local int g_dec_skip = 0;               // option 16: profiling only — skip decode kernels (bit mask)
 thread_local bool g_dec_swap = true;           // option 15: swapped-operand decode GEMM (else tc_gemm)
+thread_local bool g_gemm_pair = true;          // option 20: CTA-pair (cta_group::2) prefill GEMMs (370M prefill +3.6%, 2.7B +11%)
 thread_local int g_wide_min = 1;               // option 14: smallest batch on the wide-batch decode path (measured: the per-layer path beats the fused step at every B, 1.3B B=1 1.215 -> 1.150 ms)
 thread_local int g_mega_pf = 0;                // option 9: fused decode step L2 prefetch lookahead (stages)
 thread_local bool g_dec_pdl = true;            // option 8: PDL between the decode kernels
@@ -219,6 +220,44 @@ int launch_tc_gemm_bn(const bf16 *A, long lda, const bf16 *B, long ldb, int M, i
   return SSD200_OK;
 }
 
+// CTA-pair variant (cluster of 2, cta_group::2, 256-row tiles)
+template <int BN, int EPI>
+int launch_tc_gemm_pair(const bf16 *A, long lda, const bf16 *B, long ldb, int M, int N, int K,
+                        const TcEpilogue &ep, cudaStream_t st, bool pdl) {
+  using Cfg = TcCfg<BN, true>;
+  CUtensorMap ta, tb;
+  int rc = make_map_2d(&ta, A, M, K, lda, Cfg::BM);
+  if (rc) return rc;
+  rc = make_map_2d(&tb, B, N, K, ldb, BN / 2);
+  if (rc) return rc;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(tc_gemm_kernel<BN, EPI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Cfg::SMEM);
+    attr_set = true;
+  }
+  const int tiles = ((M + 255) / 256) * ((N + BN - 1) / BN);
+  const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(320);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = (pdl || g_use_pdl) ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, EPI, true>, ta, tb, M, N, K, ep);
+  REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "tc_gemm_kernel (pair): %s", cudaGetErrorString(e));
+  LAUNCH_CHECK("tc_gemm_kernel (pair)");
+  return SSD200_OK;
+}
+
 // D (M,N) = A (M,K) . B (N,K)^T, bf16 operands, fused epilogue.
 template <int EPI>
 int tc_gemm(const bf16 *A, long lda, const bf16 *B, long ldb, int M, int N, int K,
@@ -230,6 +269,12 @@ int tc_gemm(const bf16 *A, long lda, const bf16 *B, long ldb, int M, int N, int 
           "tc_gemm: split-K needs the F32 epilogue and at least one K block per split");
   if (EPI == TC_EPI_F32 && ep.ksplit > 1)  // split-K: always 128-wide tiles (most tiles)
     return launch_tc_gemm_bn<128, EPI>(A, lda, B, ldb, M, N, K, ep, st, pdl);
+  if constexpr (EPI != TC_EPI_INPROJ_CONV) {
+    // CTA pairs when 256 x 256 tiles still cover the SMs several times
+    const long tiles_pair = (long)((M + 255) / 256) * ((N + 255) / 256);
+    if (g_gemm_pair && N > 128 && tiles_pair >= 2L * num_sms())
+      return launch_tc_gemm_pair<256, EPI>(A, lda, B, ldb, M, N, K, ep, st, pdl);
+  }
   // 128-wide tiles when 256-wide ones would leave SMs idle (few row tiles: decode batches)
   // (prefill at B = 1 / short T: the out_proj's 256-wide tiles covered 64 of 148 SMs)
   const long tiles256 = (long)((M + 127) / 128) * ((N + 255) / 256);
@@ -1794,6 +1839,9 @@ int ssd200_set_option(int option, int value) {
       return SSD200_OK;
     case 15:  // wide-batch decode GEMMs: swapped-operand weight-streaming kernel (1) or tc_gemm (0)
       g_dec_swap = value != 0;
+      return SSD200_OK;
+    case 20:  // prefill GEMMs: CTA pairs (cluster of 2, cta_group::2, 256 x 256 tiles) (1) or single CTAs (0)
+      g_gemm_pair = value != 0;
       return SSD200_OK;
     case 14:  // smallest batch that takes the wide-batch decode path (default 1; 9 = fused step for B <= 8)
       REQUIRE(value >= 1, SSD200_EINVAL, "option 14 out of range");

@@ -72,11 +72,15 @@ template <int EPI> struct TcRows {
   static constexpr int HALO = 128 - STRIDE;
 };
 
-template <int BN> struct TcCfg {
+// PAIR: a CTA pair (cluster of 2, cta_group::2) computes a 256 x BN tile; each
+// CTA stages its 128 rows of A and half (BN / 2 rows) of B, the leader issues
+// M = 256 MMAs that read both CTAs' shared memory, each CTA's TMEM holds its
+// 128 x BN accumulator rows.  Halves the shared-memory traffic per MMA.
+template <int BN, bool PAIR = false> struct TcCfg {
   static constexpr int BM = 128, BK = 64;
-  static constexpr int STAGES = BN >= 256 ? 4 : 6;
   static constexpr uint32_t A_BYTES = BM * BK * 2;
-  static constexpr uint32_t B_BYTES = BN * BK * 2;
+  static constexpr uint32_t B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;
+  static constexpr int STAGES = (A_BYTES + B_BYTES) > 32768 ? 4 : 6;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
   // per epilogue warp: a 32-row x 16-word transpose buffer (padded) so that
@@ -176,11 +180,12 @@ __device__ __forceinline__ void tc_store_chunk(const TcEpilogue &ep, uint32_t (&
   }
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool PAIR = false>
 __global__ void __launch_bounds__(320, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int M, int N, int K, TcEpilogue ep) {
-  using Cfg = TcCfg<BN>;
+  using Cfg = TcCfg<BN, PAIR>;
+  static_assert(!PAIR || (EPI != TC_EPI_INPROJ_CONV), "pair mode: no halo tiles");
   constexpr int BM = Cfg::BM, BK = Cfg::BK, STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned, derived from smem_raw by an offset so that the compiler
@@ -197,8 +202,13 @@ __global__ void __launch_bounds__(320, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int RSTRIDE = TcRows<EPI>::STRIDE, HALO = TcRows<EPI>::HALO;
+  // pair mode: tiles are 256 rows per cluster; rank r owns rows [128 r, 128 r + 128)
+  const uint32_t rank = PAIR ? sm100::cluster_rank() : 0u;
+  const int cta0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int nct = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  constexpr int TROWS = PAIR ? 256 : RSTRIDE;
   const int num_n = (N + BN - 1) / BN;
-  const int num_mn = ((M + RSTRIDE - 1) / RSTRIDE) * num_n;
+  const int num_mn = ((M + TROWS - 1) / TROWS) * num_n;
   const int ksplit = (EPI == TC_EPI_F32 && ep.ksplit > 1) ? ep.ksplit : 1;
   const int num_tiles = num_mn * ksplit;
   const int num_kb = (K + BK - 1) / BK;
@@ -213,13 +223,19 @@ __global__ void __launch_bounds__(320, 1)
     }
     for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(&tfull[s], 1);
-      sm100::mbar_init(&tempty[s], 8);
+      sm100::mbar_init(&tempty[s], PAIR ? 16 : 8);  // pair: both CTAs' epilogue warps
     }
     sm100::fence_barrier_init();
   }
-  if (warp == 1) sm100::tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (PAIR)
+      sm100::tmem_alloc_pair<Cfg::TMEM_COLS>(tmem_slot);
+    else
+      sm100::tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  }
   sm100::tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) sm100::cluster_sync();  // both CTAs' barriers live before any remote arrive
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_launch();  // the next kernel's CTAs may take SMs as ours retire
@@ -229,16 +245,26 @@ __global__ void __launch_bounds__(320, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = cta0; tile < num_tiles; tile += nct) {
         const int mn = tile % num_mn, ks = tile / num_mn;
         const int m_blk = mn / num_n, n_blk = mn % num_n;
         const int kb0 = ks * num_kb / ksplit, kb1 = (ks + 1) * num_kb / ksplit;
         for (int kb = kb0; kb < kb1; ++kb) {
           sm100::mbar_wait(&empty[s], ph ^ 1);
+          if constexpr (PAIR) {
+            // both CTAs' bytes complete on the leader's full barrier
+            const uint32_t fb = sm100::mapa_u32(sm100::smem_u32(&full[s]), 0);
+            if (rank == 0) sm100::mbar_arrive_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
+            sm100::tma_load_2d_pair(sA + s * Cfg::A_BYTES, &tmA, fb, kb * BK,
+                                    m_blk * 256 + (int)rank * 128);
+            sm100::tma_load_2d_pair(sB + s * Cfg::B_BYTES, &tmB, fb, kb * BK,
+                                    n_blk * BN + (int)rank * (BN / 2));
+          } else {
           sm100::mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
           sm100::tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * BK,
                              m_blk * RSTRIDE - HALO);
           sm100::tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, &full[s], kb * BK, n_blk * BN);
+          }
           if (++s == STAGES) {
             s = 0;
             ph ^= 1;
@@ -247,12 +273,12 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = sm100::idesc_bf16(BM, BN, false, false);
+    if (lane == 0 && rank == 0) {  // pair mode: the leader issues for both CTAs
+      constexpr uint32_t idesc = sm100::idesc_bf16(PAIR ? 256 : BM, BN, false, false);
       int s = 0;
       uint32_t ph = 0;
       int local = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      for (int tile = cta0; tile < num_tiles; tile += nct, ++local) {
         const int as = local & 1;
         const uint32_t aph = (local >> 1) & 1;
         sm100::mbar_wait(&tempty[as], aph ^ 1);
@@ -269,15 +295,24 @@ __global__ void __launch_bounds__(320, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = sm100::sw128_desc(a0 + k * 32, 16, 1024);
             const uint64_t bd = sm100::sw128_desc(b0 + k * 32, 16, 1024);
-            sm100::mma_bf16(d_tmem, ad, bd, idesc, (kb != kb0) || (k != 0));
+            if constexpr (PAIR)
+              sm100::mma_bf16_pair(d_tmem, ad, bd, idesc, (kb != kb0) || (k != 0));
+            else
+              sm100::mma_bf16(d_tmem, ad, bd, idesc, (kb != kb0) || (k != 0));
           }
-          sm100::mma_commit(&empty[s]);
+          if constexpr (PAIR)
+            sm100::mma_commit_pair(&empty[s], 3);
+          else
+            sm100::mma_commit(&empty[s]);
           if (++s == STAGES) {
             s = 0;
             ph ^= 1;
           }
         }
-        sm100::mma_commit(&tfull[as]);
+        if constexpr (PAIR)
+          sm100::mma_commit_pair(&tfull[as], 3);
+        else
+          sm100::mma_commit(&tfull[as]);
       }
     }
   } else {
@@ -287,14 +322,15 @@ __global__ void __launch_bounds__(320, 1)
     constexpr bool RESID = (EPI == TC_EPI_RESID || EPI == TC_EPI_RESID_NORM);
     const bool vec_ok = (ep.ldc & 7) == 0;
     int local = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+    for (int tile = cta0; tile < num_tiles; tile += nct, ++local) {
       const int mn = tile % num_mn;
       const size_t coff = (size_t)(tile / num_mn) * (size_t)ep.split_stride;
       const int m_blk = mn / num_n, n_blk = mn % num_n;
       const int as = local & 1;
       const uint32_t aph = (local >> 1) & 1;
       const int i_row = q * 32 + lane;                 // tile row == TMEM lane
-      const int m = m_blk * RSTRIDE - HALO + i_row;    // global row (HALO = 0: m_blk*128+i)
+      const int row0 = PAIR ? m_blk * 256 + (int)rank * 128 : m_blk * RSTRIDE - HALO;
+      const int m = row0 + i_row;                      // global row (HALO = 0: m_blk*128+i)
       const bool out_row = i_row >= HALO && m < M;
       // row-only inputs before the wait: the norm scale and the first residual chunk
       float rowscale = 1.f;
@@ -306,7 +342,7 @@ __global__ void __launch_bounds__(320, 1)
       // transposed view of a 32 x 32 chunk: lanes 0-15 / 16-31 take rows 2i / 2i+1,
       // column (lane & 15) of each 16-column half -> row-contiguous global accesses
       uint32_t *xpb = sX + (warp - 2) * (32 * 17);
-      const int m_w = m_blk * RSTRIDE - HALO + q * 32;  // global row of this warp's lane 0
+      const int m_w = row0 + q * 32;  // global row of this warp's lane 0
       const int tc = lane & 15, tr = lane >> 4;
       float hv[32];  // residual, transposed layout: [half h][pair i] -> hv[16 h + i]
       auto fetch = [&](int cc, float(&dst)[32]) {
@@ -465,14 +501,23 @@ __global__ void __launch_bounds__(320, 1)
         asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
       sm100::tc_fence_before();
       __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(&tempty[as]);
+      if (lane == 0) {
+        if constexpr (PAIR)  // the leader's MMA waits for both CTAs' epilogues
+          sm100::mbar_arrive_cluster(sm100::mapa_u32(sm100::smem_u32(&tempty[as]), 0));
+        else
+          sm100::mbar_arrive(&tempty[as]);
+      }
     }
   }
   __syncthreads();
+  if constexpr (PAIR) sm100::cluster_sync();  // the peer's MMAs / arrivals are done
   if (warp == 1) {
     __syncwarp();
     sm100::tc_fence_after();
-    sm100::tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+    if constexpr (PAIR)
+      sm100::tmem_dealloc_pair<Cfg::TMEM_COLS>(tmem_base);
+    else
+      sm100::tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
   }
 }
 

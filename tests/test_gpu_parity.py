@@ -530,3 +530,28 @@ def test_verify_suites_pass():
     assert [r.suite for r in results] == list(verify.SUITES)
     bad = [r.to_dict() for r in results if not r.passed]
     assert not bad, bad
+
+
+@pytest.mark.parametrize("B,T", [(4, 4096)])
+def test_bf16_prefill_cta_pair_gemms_match(B, T):
+    """CTA-pair (cta_group::2) GEMMs for in_proj / out_proj (option 20) against
+    the single-CTA GEMMs on a production-width layer at a size where both
+    take 256 x 256 pair tiles; the single-CTA path is the one pinned to the
+    oracle above."""
+    import paper_2603_09555_b200 as m
+    from paper_2603_09555_b200 import _abi
+
+    cfg = _bf16_cfg(vocab_size=2048, d_model=1024, n_layers=2)
+    params = m.from_reference(m.random_init_host(cfg, 71), cfg)
+    toks = np.random.default_rng(72).integers(0, cfg.vocab_size, size=(B, T))
+    outs = []
+    try:
+        for pair in (0, 1):
+            _abi.lib().ssd200_set_option(20, pair)
+            lg, cache = m.prefill(params, toks, cfg, logits="last")
+            outs.append((lg, cache.ssm_all.clone()))
+    finally:
+        _abi.lib().ssd200_set_option(20, 1)
+    (la, sa), (lb, sb) = outs
+    assert ((la - lb).norm() / la.norm()).item() <= 1e-3
+    assert ((sa - sb).norm() / sa.norm()).item() <= 1e-3
