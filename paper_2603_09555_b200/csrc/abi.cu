@@ -741,7 +741,7 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
               SSD200_ELAUNCH, "conv_tail launch");
       LAUNCH_CHECK("conv_tail");
     }
-    if (k == 4 && n_split % 8 == 0 && d->d_inner % 8 == 0) {
+    if (k == 4 && n_split % 8 == 0 && d->d_inner % 8 == 0 && wd.conv_dim % 4 == 0) {
       // TMA-tiled streaming conv (ssd_tc.cuh)
       CUtensorMap tmx;
       rc = make_map_2d_plain(&tmx, u + d->d_inner, rows, wd.conv_dim, n_split, CONV_COLS,

@@ -62,12 +62,12 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int ch) {
 // Causal depthwise conv (k = 4) + SiLU over the xBC columns, numerics.py:169-189.
 // One CTA = 256 channels x 64 tokens: one TMA load brings the [64+3, 256]
 // bf16 tile (3-row history halo; rows before the buffer start are zero-filled)
-// into smem; thread (pair p, half h) slides the window down channels
-// (2p, 2p+1) over rows [32h, 32h+32), restarting it at sequence starts.
+// into smem; thread (quad q, quarter h) slides the window down channels
+// 4q .. 4q+3 over rows [16h, 16h+16), restarting it at sequence starts.
 constexpr int CONV_ROWS = 64, CONV_COLS = 256;
 
 __global__ void __launch_bounds__(256) conv_silu_tma(const __grid_constant__ CUtensorMap tm_xbc,
-                                                     const float *__restrict__ w,
+                                                     const float *__restrict__ w_,
                                                      const float *__restrict__ bias,
                                                      bf16 *__restrict__ out, long ld_out, int T,
                                                      int C, long rows) {
@@ -86,45 +86,70 @@ __global__ void __launch_bounds__(256) conv_silu_tma(const __grid_constant__ CUt
     sm100::mbar_arrive_expect_tx(&bar, (CONV_ROWS + 3) * CONV_COLS * 2);
     sm100::tma_load_2d(&tile[0][0], &tm_xbc, &bar, c0, (int)(r0 - 3));
   }
-  const int pair = threadIdx.x & 127, half = threadIdx.x >> 7;
-  const int c = c0 + 2 * pair;
-  float w0[4], w1[4], b0 = 0.f, b1 = 0.f;
-  if (c + 1 < C) {
-    const float4 a = reinterpret_cast<const float4 *>(w)[c];
-    const float4 bb = reinterpret_cast<const float4 *>(w)[c + 1];
-    w0[0] = a.x; w0[1] = a.y; w0[2] = a.z; w0[3] = a.w;
-    w1[0] = bb.x; w1[1] = bb.y; w1[2] = bb.z; w1[3] = bb.w;
-    b0 = bias[c];
-    b1 = bias[c + 1];
+  // thread (quad qd, quarter qr): channels 4 qd .. 4 qd + 3 over rows [16 qr, 16 qr + 16)
+  const int qd = threadIdx.x & 63, qr = threadIdx.x >> 6;
+  const int c = c0 + 4 * qd;
+  float w[4][4], bs[4] = {0.f, 0.f, 0.f, 0.f};
+  const bool ok = c + 3 < C;
+  if (ok) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 a = reinterpret_cast<const float4 *>(w_)[c + j];
+      w[j][0] = a.x;
+      w[j][1] = a.y;
+      w[j][2] = a.z;
+      w[j][3] = a.w;
+      bs[j] = bias[c + j];
+    }
   }
   sm100::mbar_wait(&bar, 0);
-  if (c + 1 >= C) return;
-  const int i0 = half * 32;  // first output row of this thread (tile row i0 + 3)
+  if (!ok) return;
+  auto ld4 = [&](int row, float (&v)[4]) {
+    const uint2 u = *reinterpret_cast<const uint2 *>(&tile[row][4 * qd]);
+    const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.x));
+    const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.y));
+    v[0] = lo.x;
+    v[1] = lo.y;
+    v[2] = hi.x;
+    v[3] = hi.y;
+  };
+  const int i0 = qr * 16;  // first output row of this thread (tile row i0 + 3)
   long r = r0 + i0;
   int t = (int)(r % T);
   // window: x[t-3], x[t-2], x[t-1] from the tile rows i0, i0+1, i0+2 (masked at sequence start)
-  float2 h3 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&tile[i0][2 * pair]));
-  float2 h2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&tile[i0 + 1][2 * pair]));
-  float2 h1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&tile[i0 + 2][2 * pair]));
-  if (t < 3) h3 = make_float2(0.f, 0.f);
-  if (t < 2) h2 = make_float2(0.f, 0.f);
-  if (t < 1) h1 = make_float2(0.f, 0.f);
+  float h3[4], h2[4], h1[4];
+  ld4(i0, h3);
+  ld4(i0 + 1, h2);
+  ld4(i0 + 2, h1);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (t < 3) h3[j] = 0.f;
+    if (t < 2) h2[j] = 0.f;
+    if (t < 1) h1[j] = 0.f;
+  }
 #pragma unroll 4
-  for (int i = 0; i < 32; ++i, ++r, ++t) {
+  for (int i = 0; i < 16; ++i, ++r, ++t) {
     if (r >= rows) break;
     if (t == T) {  // next sequence: zero history
       t = 0;
-      h1 = h2 = h3 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) h1[j] = h2[j] = h3[j] = 0.f;
     }
-    const float2 x = __bfloat1622float2(
-        *reinterpret_cast<const __nv_bfloat162 *>(&tile[i0 + i + 3][2 * pair]));
-    const float a0 = w0[0] * h3.x + w0[1] * h2.x + w0[2] * h1.x + w0[3] * x.x + b0;
-    const float a1 = w1[0] * h3.y + w1[1] * h2.y + w1[2] * h1.y + w1[3] * x.y + b1;
-    *reinterpret_cast<__nv_bfloat162 *>(out + r * ld_out + c) =
-        __floats2bfloat162_rn(silu_fast(a0), silu_fast(a1));
-    h3 = h2;
-    h2 = h1;
-    h1 = x;
+    float x[4], o[4];
+    ld4(i0 + i + 3, x);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      o[j] = silu_fast(w[j][0] * h3[j] + w[j][1] * h2[j] + w[j][2] * h1[j] + w[j][3] * x[j] + bs[j]);
+      h3[j] = h2[j];
+      h2[j] = h1[j];
+      h1[j] = x[j];
+    }
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(o[0], o[1]);
+    const __nv_bfloat162 hi = __floats2bfloat162_rn(o[2], o[3]);
+    uint2 pk;
+    pk.x = *reinterpret_cast<const uint32_t *>(&lo);
+    pk.y = *reinterpret_cast<const uint32_t *>(&hi);
+    *reinterpret_cast<uint2 *>(out + r * ld_out + c) = pk;
   }
 }
 
