@@ -578,7 +578,7 @@ def run_decode_workload(args, rank, world, local):
     # e2e through the public API with host buffers
     host_prompt = torch.randint(0, cfg.vocab_size, (B, 16)).pin_memory()
     gen = 64
-    m.generate(params, host_prompt.to(dev, non_blocking=True), 4, cfg=cfg)  # warm
+    m.generate(params, host_prompt.to(dev, non_blocking=True), gen, cfg=cfg)  # warm: captures
     torch.cuda.synchronize()
     barrier(world)
     s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -613,7 +613,9 @@ def run_decode_workload(args, rank, world, local):
             "e2e": {"value": B * world * (gen - 1) / (e2e_ms / 1e3), "unit": "tok/s",
                     "h2d_bytes_per_step": int(host_prompt.numel() * 8),
                     "d2h_bytes_per_step": int(toks.numel() * 8),
-                    "note": "public generate(): 16-token prefill + graph capture + 63 decode steps"},
+                    "note": "public generate(): prompt H2D + 16-token prefill + 63 decode steps + "
+                            "tokens D2H; the decode graph captured by a warm-up call is reused "
+                            "when the cache is <= 2 GB (decode._GRAPH_CACHE), else re-captured"},
             "roofline": {"kernel": "decode token step (one CUDA graph: 48 x [in_proj, state stream, "
                                    "out_proj, finish] + head)",
                          "bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",

@@ -154,6 +154,36 @@ class GreedyDecoder:
             self._body()
 
 
+# captured decode graphs kept across generate() calls (a capture costs ~100x a token step);
+# keyed by the parameters' identity, config, batch and length; only modest caches are kept
+_GRAPH_CACHE: dict = {}
+_GRAPH_CACHE_MAX = 2
+_GRAPH_CACHE_MAX_BYTES = 2 << 30
+
+
+def _decoder_for(params: ModelParams, cfg: ModelConfig, cache: Mamba2Cache, gen_len: int,
+                 keep_logits: bool, use_graph: bool) -> "GreedyDecoder":
+    nbytes = cache.ssm_all.numel() * cache.ssm_all.element_size() + \
+        cache.conv_all.numel() * cache.conv_all.element_size()
+    if not use_graph or nbytes > _GRAPH_CACHE_MAX_BYTES:
+        return GreedyDecoder(params, cfg, cache, gen_len, keep_logits=keep_logits,
+                             use_graph=use_graph)
+    key = (id(params), cfg, cache.batch, gen_len, keep_logits, str(params.device))
+    hit = _GRAPH_CACHE.get(key)
+    if hit is not None and hit[0] is params:
+        dec = hit[1]
+        dec.cache.ssm_all.copy_(cache.ssm_all)  # the graph's buffers take this prefill's state
+        dec.cache.conv_all.copy_(cache.conv_all)
+        dec.tokens.zero_()
+        return dec
+    dec = GreedyDecoder(params, cfg, cache.copy(), gen_len, keep_logits=keep_logits,
+                        use_graph=True)
+    if len(_GRAPH_CACHE) >= _GRAPH_CACHE_MAX:
+        _GRAPH_CACHE.pop(next(iter(_GRAPH_CACHE)))
+    _GRAPH_CACHE[key] = (params, dec)
+    return dec
+
+
 def generate(params: ModelParams, prompt, gen_len: int, mode: str = "cached",
              cfg: ModelConfig | None = None, keep_logits: bool = False,
              use_graph: bool = True) -> GenerationResult:
@@ -190,7 +220,7 @@ def generate(params: ModelParams, prompt, gen_len: int, mode: str = "cached",
 
     pick = torch.empty((B,), dtype=torch.int64, device=dev)
     last, cache = prefill(params, ptok, cfg, logits="last", argmax_out=pick)
-    dec = GreedyDecoder(params, cfg, cache, gen_len, keep_logits=keep_logits, use_graph=use_graph)
+    dec = _decoder_for(params, cfg, cache, gen_len, keep_logits, use_graph)
     dec.tok.copy_(pick)
     dec.tokens[:, 0] = pick
     if dec.kept is not None:
@@ -198,4 +228,6 @@ def generate(params: ModelParams, prompt, gen_len: int, mode: str = "cached",
     dec.step_idx.fill_(1)
     for _ in range(gen_len - 1):
         dec.step()
-    return GenerationResult(tokens=dec.tokens, steps=gen_len, per_step_logits=dec.kept)
+    # the decoder may be reused by the next call: hand back copies
+    return GenerationResult(tokens=dec.tokens.clone(), steps=gen_len,
+                            per_step_logits=None if dec.kept is None else dec.kept.clone())

@@ -555,3 +555,22 @@ def test_bf16_prefill_cta_pair_gemms_match(B, T):
     (la, sa), (lb, sb) = outs
     assert ((la - lb).norm() / la.norm()).item() <= 1e-3
     assert ((sa - sb).norm() / sa.norm()).item() <= 1e-3
+
+
+def test_generate_graph_cache_reuse_is_exact():
+    """generate() keeps captured decode graphs across calls (decode._GRAPH_CACHE):
+    a second call with another prompt through the cached graph must equal an
+    uncached (eager) run, and the first call's results must not be overwritten."""
+    import paper_2603_09555_b200 as m
+
+    cfg = _bf16_cfg()
+    params = m.from_reference(m.random_init_host(cfg, 81), cfg)
+    rng = np.random.default_rng(82)
+    p1 = rng.integers(0, cfg.vocab_size, size=(2, 20))
+    p2 = rng.integers(0, cfg.vocab_size, size=(2, 20))
+    a = m.generate(params, p1, 9, cfg=cfg, keep_logits=True)
+    b = m.generate(params, p2, 9, cfg=cfg, keep_logits=True)  # cache hit
+    ea = m.generate(params, p1, 9, cfg=cfg, keep_logits=True, use_graph=False)
+    eb = m.generate(params, p2, 9, cfg=cfg, keep_logits=True, use_graph=False)
+    assert torch.equal(a.tokens, ea.tokens) and torch.equal(a.per_step_logits, ea.per_step_logits)
+    assert torch.equal(b.tokens, eb.tokens) and torch.equal(b.per_step_logits, eb.per_step_logits)
