@@ -344,19 +344,41 @@ __global__ void __launch_bounds__(320, 1)
       uint32_t *xpb = sX + (warp - 2) * (32 * 17);
       const int m_w = row0 + q * 32;  // global row of this warp's lane 0
       const int tc = lane & 15, tr = lane >> 4;
-      float hv[32];  // residual, transposed layout: [half h][pair i] -> hv[16 h + i]
+      float hv[32];  // residual chunk, transposed layout (see fetch)
+      // RESID with 16-byte aligned rows (rvec): in each 16-column half h, lane l takes rows
+      // 8 i + (l >> 2) and columns 4 (l & 3) .. + 3 -> hv[16 h + 4 i + j] (float4 loads /
+      // stores); otherwise the scalar layout [half h][pair i] -> hv[16 h + i]
+      const bool rvec = RESID && (ep.ldc & 3) == 0 && (N & 3) == 0;
+      const int vr = lane >> 2, vc = 4 * (lane & 3);
       auto fetch = [&](int cc, float(&dst)[32]) {
         const int n0 = n_blk * BN + cc;
         if (RESID && cc < BN && n0 < N) {
+          if (rvec) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int mr = m_w + 2 * i + tr, n = n0 + 16 * h + tc;
-              dst[16 * h + i] = (mr < M && n < N)
-                                    ? reinterpret_cast<const float *>(ep.C)[(size_t)mr * ep.ldc + n]
-                                    : 0.f;
-            }
+              for (int i = 0; i < 4; ++i) {
+                const int mr = m_w + 8 * i + vr, n = n0 + 16 * h + vc;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (mr < M && n < N)
+                  v = *reinterpret_cast<const float4 *>(
+                      reinterpret_cast<const float *>(ep.C) + (size_t)mr * ep.ldc + n);
+                dst[16 * h + 4 * i + 0] = v.x;
+                dst[16 * h + 4 * i + 1] = v.y;
+                dst[16 * h + 4 * i + 2] = v.z;
+                dst[16 * h + 4 * i + 3] = v.w;
+              }
+          } else {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const int mr = m_w + 2 * i + tr, n = n0 + 16 * h + tc;
+                dst[16 * h + i] = (mr < M && n < N)
+                                      ? reinterpret_cast<const float *>(ep.C)[(size_t)mr * ep.ldc + n]
+                                      : 0.f;
+              }
+          }
         }
       };
       fetch(half * 32, hv);
@@ -459,6 +481,32 @@ __global__ void __launch_bounds__(320, 1)
         } else if constexpr (RESID) {
           // hidden += acc * rowscale: f32 + bf16 shadow, stored row-contiguously
           float *C = reinterpret_cast<float *>(ep.C);
+          if (rvec) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                xpb[lane * 17 + j] = __float_as_uint(__uint_as_float(r[16 * h + j]) * rowscale);
+              __syncwarp();
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int rr = 8 * i + vr, mr = m_w + rr, n = n0 + 16 * h + vc;
+                if (mr < M && n < N) {
+                  float4 o;
+                  o.x = hv[16 * h + 4 * i + 0] + __uint_as_float(xpb[rr * 17 + vc + 0]);
+                  o.y = hv[16 * h + 4 * i + 1] + __uint_as_float(xpb[rr * 17 + vc + 1]);
+                  o.z = hv[16 * h + 4 * i + 2] + __uint_as_float(xpb[rr * 17 + vc + 2]);
+                  o.w = hv[16 * h + 4 * i + 3] + __uint_as_float(xpb[rr * 17 + vc + 3]);
+                  *reinterpret_cast<float4 *>(C + (size_t)mr * ep.ldc + n) = o;
+                  uint2 pk;
+                  pk.x = pack_bf16x2(o.x, o.y);
+                  pk.y = pack_bf16x2(o.z, o.w);
+                  *reinterpret_cast<uint2 *>(ep.C_lp + (size_t)mr * ep.ldc + n) = pk;
+                }
+              }
+              __syncwarp();
+            }
+          } else
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
 #pragma unroll
