@@ -525,18 +525,24 @@ __global__ void __launch_bounds__(320, 1)
             __syncwarp();
           }
         } else if (EPI == TC_EPI_INPROJ && n0 + 32 <= ep.n_split && vec_ok) {
-          // bf16 z / xBC columns, stored row-contiguously (16 bf16 pairs per row)
+          // bf16 z / xBC columns, stored row-contiguously: 16 bf16 pairs (64 B) per row,
+          // lane l stores 16 B of row 8 i + (l >> 2)
           bf16 *C = reinterpret_cast<bf16 *>(ep.C);
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             xpb[lane * 17 + j] = pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
           __syncwarp();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int mr = m_w + 2 * i + tr;
-            if (mr < M)
-              reinterpret_cast<uint32_t *>(C + (size_t)mr * ep.ldc + n0)[tc] =
-                  xpb[(2 * i + tr) * 17 + tc];
+          for (int i = 0; i < 4; ++i) {
+            const int rr = 8 * i + vr, mr = m_w + rr;
+            if (mr < M) {
+              uint4 v;
+              v.x = xpb[rr * 17 + vc + 0];
+              v.y = xpb[rr * 17 + vc + 1];
+              v.z = xpb[rr * 17 + vc + 2];
+              v.w = xpb[rr * 17 + vc + 3];
+              *reinterpret_cast<uint4 *>(C + (size_t)mr * ep.ldc + n0 + 2 * vc) = v;
+            }
           }
           __syncwarp();
         } else if (m < M) {
