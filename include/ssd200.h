@@ -184,7 +184,8 @@ int ssd200_debug_trace(void *device_buffer);
  * B tile across 4-CTA clusters by TMA multicast in that kernel (1, default)
  * or load it per CTA (0); option 4 = output-kernel CTA target in multiples of
  * the SM count (head-group split, default 1); option 5 = programmatic
- * dependent launch between the prefill kernels (0 default, 1 on).
+ * dependent launch between the prefill kernels (1 default, 0 off); option 20 =
+ * CTA-pair (cta_group::2) prefill GEMMs (1 default, 0 off).
  * Decode (bf16): options 6 / 7 = in_proj / out_proj split-K factor (0 auto);
  * 8 = PDL between the decode kernels (1 default); 9 = fused step's L2
  * prefetch lookahead in ring stages (0 default); 11 / 12 / 13 = state-stream
