@@ -36,6 +36,7 @@ thread_local int g_dec_gemm_small = -1;        // option 17: decode GEMM ~96 KB 
 thread_local int g_dec_skip = 0;               // option 16: profiling only — skip decode kernels (bit mask)
 thread_local bool g_dec_swap = true;           // option 15: swapped-operand decode GEMM (else tc_gemm)
 thread_local bool g_gemm_pair = true;          // option 20: CTA-pair (cta_group::2) prefill GEMMs (370M prefill +3.6%, 2.7B +11%)
+thread_local int g_pair_min_tiles = 0;         // option 21: fewest 256x256 tiles for CTA-pair GEMMs (0 = 64)
 thread_local int g_wide_min = 1;               // option 14: smallest batch on the wide-batch decode path (measured: the per-layer path beats the fused step at every B, 1.3B B=1 1.215 -> 1.150 ms)
 thread_local int g_mega_pf = 0;                // option 9: fused decode step L2 prefetch lookahead (stages)
 thread_local bool g_dec_pdl = true;            // option 8: PDL between the decode kernels
@@ -272,7 +273,10 @@ int tc_gemm(const bf16 *A, long lda, const bf16 *B, long ldb, int M, int N, int 
   if constexpr (EPI != TC_EPI_INPROJ_CONV) {
     // CTA pairs when 256 x 256 tiles still cover the SMs several times
     const long tiles_pair = (long)((M + 255) / 256) * ((N + 255) / 256);
-    if (g_gemm_pair && N > 128 && tiles_pair >= 2L * num_sms())
+    // measured: pairs win from 64 tiles (370M B=1 T=4K 559K -> 616K tok/s, B=2 T=2K
+    // 655K -> 685K); at 32 tiles (B=1 T=2K out_proj) the 128-wide single tiles win
+    const long min_pair = g_pair_min_tiles > 0 ? g_pair_min_tiles : 64;
+    if (g_gemm_pair && N > 128 && tiles_pair >= min_pair)
       return launch_tc_gemm_pair<256, EPI>(A, lda, B, ldb, M, N, K, ep, st, pdl);
   }
   // 128-wide tiles when 256-wide ones would leave SMs idle (few row tiles: decode batches)
@@ -1842,6 +1846,9 @@ int ssd200_set_option(int option, int value) {
       return SSD200_OK;
     case 20:  // prefill GEMMs: CTA pairs (cluster of 2, cta_group::2, 256 x 256 tiles) (1) or single CTAs (0)
       g_gemm_pair = value != 0;
+      return SSD200_OK;
+    case 21:  // CTA-pair GEMMs from this many 256 x 256 tiles (0 = 64)
+      g_pair_min_tiles = value;
       return SSD200_OK;
     case 14:  // smallest batch that takes the wide-batch decode path (default 1; 9 = fused step for B <= 8)
       REQUIRE(value >= 1, SSD200_EINVAL, "option 14 out of range");
