@@ -729,7 +729,31 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
     }
     return;
   }
-  // ---------------- consumers: dt of every local tile first (decode.py:111-114)
+  // ---------------- consumers
+  // the layer's parameters do not depend on the predecessor: pull the first tile's
+  // conv taps / biases and the per-head scalars into L1 while the in_proj drains
+  if (cnt > 0) {
+    const int h0 = t0 % H, g0 = h0 / hpg;
+    auto pf = [](const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); };
+    if (threadIdx.x < 2 * N) {
+      const int j = threadIdx.x, isc = j >= N;
+      const int ch = a.d_inner + (isc ? a.G * N : 0) + g0 * N + (isc ? j - N : j);
+      pf(a.conv_w + (size_t)ch * 4);
+      pf(a.conv_b + ch);
+    }
+    if (lane < RPW) {
+      const int ch = h0 * P + warp * RPW + lane;
+      pf(a.conv_w + (size_t)ch * 4);
+      pf(a.conv_b + ch);
+    }
+    if (threadIdx.x < cnt && threadIdx.x < CT) {
+      const int h = (t0 + threadIdx.x) % H;
+      pf(a.dt_bias + h);
+      pf(a.a + h);
+      pf(a.D + h);
+    }
+  }
+  // dt of every local tile first (decode.py:111-114)
   griddep_wait();
   for (int i = threadIdx.x; i < cnt; i += CT) {
     const int t = t0 + i, b = t / H, h = t % H;
