@@ -925,10 +925,15 @@ struct DecFinishArgs {
 };
 __global__ __launch_bounds__(256) void dec_out_finish(DecFinishArgs a) {
   __shared__ float sc;
-  griddep_wait();
-  griddep_launch();
   const int b = blockIdx.y;
   const int nb_h = (a.d_model + 255) / 256;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = (int)blockIdx.x < nb_h && n < a.d_model;
+  const long i = (long)b * a.d_model + n;
+  // the residual was written a layer ago (every PDL predecessor has completed it)
+  const float hold = (live && !a.pout) ? a.hidden[i] : 0.f;
+  griddep_wait();
+  griddep_launch();
   if ((int)blockIdx.x >= nb_h) {
     const int c = a.d_inner + ((int)blockIdx.x - nb_h) * 256 + threadIdx.x;  // B / C channel
     if (c >= a.conv_dim) return;
@@ -942,6 +947,10 @@ __global__ __launch_bounds__(256) void dec_out_finish(DecFinishArgs a) {
     co[2] = v;
     return;
   }
+  // the split-K partials are requested before the row's norm reduction
+  float acc = 0.f;
+  if (live)
+    for (int j = 0; j < a.nsplit; ++j) acc += a.part[j * a.sstride + (long)b * a.d_model + n];
   if (threadIdx.x < 32) {
     float t = 0.f;
     for (int h = threadIdx.x; h < a.H; h += 32) t += a.ssq[(long)b * a.H + h];
@@ -952,16 +961,12 @@ __global__ __launch_bounds__(256) void dec_out_finish(DecFinishArgs a) {
     }
   }
   __syncthreads();
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= a.d_model) return;
-  float acc = 0.f;
-  for (int j = 0; j < a.nsplit; ++j) acc += a.part[j * a.sstride + (long)b * a.d_model + n];
+  if (!live) return;
   if (a.pout) {
     a.pout[(long)b * a.pld + n] = acc;
     return;
   }
-  const long i = (long)b * a.d_model + n;
-  const float v = a.hidden[i] + sc * acc;
+  const float v = hold + sc * acc;
   a.hidden[i] = v;
   a.lp[i] = __float2bfloat16_rn(v);
 }
