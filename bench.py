@@ -615,7 +615,7 @@ def run_decode_workload(args, rank, world, local):
                     "d2h_bytes_per_step": int(toks.numel() * 8),
                     "note": "public generate(): prompt H2D + 16-token prefill + 63 decode steps + "
                             "tokens D2H; the decode graph captured by a warm-up call is reused "
-                            "when the cache is <= 2 GB (decode._GRAPH_CACHE), else re-captured"},
+                            "when the cache is <= 8 GB (decode._GRAPH_CACHE), else re-captured"},
             "roofline": {"kernel": "decode token step (one CUDA graph: 48 x [in_proj, state stream, "
                                    "out_proj, finish] + head)",
                          "bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",

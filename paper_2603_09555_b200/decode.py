@@ -158,7 +158,12 @@ class GreedyDecoder:
 # keyed by the parameters' identity, config, batch and length; only modest caches are kept
 _GRAPH_CACHE: dict = {}
 _GRAPH_CACHE_MAX = 2
-_GRAPH_CACHE_MAX_BYTES = 2 << 30
+_GRAPH_CACHE_MAX_BYTES = 8 << 30  # per entry: the decoder keeps its own copy of the cache
+
+
+def clear_graph_cache() -> None:
+    """Drop the decode graphs (and their cache buffers) kept by generate()."""
+    _GRAPH_CACHE.clear()
 
 
 def _decoder_for(params: ModelParams, cfg: ModelConfig, cache: Mamba2Cache, gen_len: int,
