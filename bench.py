@@ -1,7 +1,7 @@
 """Benchmark of the Mamba-2 SSD hot path on B200 (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload prefill|decode] [--model 370m] [--batch B] [--seqlen T]
+                    [--workload prefill|decode|serve] [--model 370m] [--batch B] [--seqlen T]
 
 Headline (BASELINE.json configs[1]): Mamba-2 370M bf16 chunked-SSD prefill,
 per-GPU batch B x T tokens, one step = one full prefill (embed, 48 blocks,
@@ -53,11 +53,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--workload", default="prefill", choices=("prefill", "decode"))
+    ap.add_argument("--workload", default="prefill", choices=("prefill", "decode", "serve"))
     ap.add_argument("--model", default="370m")
     ap.add_argument("--batch", type=int, default=4, help="per-GPU batch")
     ap.add_argument("--seqlen", type=int, default=8192)
     ap.add_argument("--decode-model", default="1.3b")
+    ap.add_argument("--serve-model", default="780m")
+    ap.add_argument("--serve-batch", type=int, default=64, help="GLOBAL batch (split over ranks)")
+    ap.add_argument("--serve-prompt", type=int, default=4096)
+    ap.add_argument("--serve-gen", type=int, default=512)
     ap.add_argument("--decode-batch", type=int, default=1)
     ap.add_argument("--decode-sweep", default="2,8,16,64,128,256",
                     help="extra decode batch sizes reported under decode.sweep ('' = none)")
@@ -533,10 +537,9 @@ def run_decode(args, local, B=None, params=None):
         "hbm_gbs": gbs,
         "hbm_frac": gbs / pk["hbm_gbs"],
         "bytes_per_step": nbytes,
-        "note": ("CUDA-graph step: one persistent kernel (embed + 48 layers + head + argmax)"
-                 if B <= 8 else
-                 "CUDA-graph step: per layer tensor-core in_proj, conv, fused SSM update + gate, "
-                 "out_proj with norm + residual epilogue; head + argmax"),
+        "note": ("CUDA-graph step: per layer a swapped-operand tensor-core in_proj, the TMA state "
+                 "stream (conv + SSM update + gate + sum u^2), out_proj, norm + residual finish; "
+                 "head + argmax"),
     }
 
 
@@ -628,6 +631,126 @@ def run_decode_workload(args, rank, world, local):
         print(json.dumps(line), flush=True)
 
 
+def run_serve_workload(args, rank, world, local):
+    """``--workload serve`` (BASELINE configs[4], C5): Mamba-2 780M serving, a
+    global batch of 64 prompts of 4K tokens, each prefilled and then extended
+    by 512 greedy tokens through the public ``generate`` (decode.py:147-194):
+    one chunked-SSD prefill, then CUDA-graph token steps with the cache in
+    place.  Rows are sharded over ranks (strong scaling: the global batch is
+    fixed, no data-path collective).  One step = one whole serving batch.
+    ``value`` = (prompt + generated) tokens/s over all ranks with the prompts
+    resident in HBM; ``e2e`` = the same call from pinned host prompts with the
+    generated tokens copied back.  ``roofline`` = the decode phase (the
+    larger share), measured in a separate pass of CUDA-graph token steps
+    against the HBM peak; ``phases_ms_per_step`` splits prefill / decode."""
+    import torch
+
+    import paper_2603_09555_b200 as m
+    from paper_2603_09555_b200 import _abi
+
+    lib = _abi.lib()
+    cfg = m.named_config(args.serve_model, compute="bf16")
+    dev = f"cuda:{local}"
+    if args.serve_batch % world:
+        raise ValueError("--serve-batch must divide by the number of GPUs")
+    B, P, G = args.serve_batch // world, args.serve_prompt, args.serve_gen
+    K, W = args.steps, args.warmup
+    params = m.synthetic_init(cfg, seed=11, device=dev)
+    gen_t = torch.Generator().manual_seed(1000 + rank)
+    host_prompt = torch.randint(0, cfg.vocab_size, (B, P), generator=gen_t).pin_memory()
+    dev_prompt = host_prompt.to(dev)
+
+    def serve(prompt):
+        return m.generate(params, prompt, G, cfg=cfg)
+
+    for _ in range(W):
+        serve(dev_prompt)  # warm-up: the first call captures the decode graph
+    torch.cuda.synchronize()
+    # prefill share of the step, timed alone on the same prompts
+    pf_ms = []
+    for _ in range(2):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        m.prefill(params, dev_prompt, cfg, logits="last")
+        e.record()
+        torch.cuda.synchronize()
+        pf_ms.append(s.elapsed_time(e))
+    prefill_ms = max_over_ranks(min(pf_ms), world)
+    with ClockSampler(local) as clk:
+        barrier(world)
+        torch.cuda.synchronize()
+        n0 = lib.ssd200_launch_count()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(K):
+            res = serve(dev_prompt)
+        e.record()
+        torch.cuda.synchronize()
+        barrier(world)
+        host_launches = lib.ssd200_launch_count() - n0
+    ms = max_over_ranks(s.elapsed_time(e) / K, world)
+    out_tokens = res.tokens
+    # e2e: pinned host prompts in, generated tokens out, inside the timed region
+    host_out = torch.empty(out_tokens.shape, dtype=out_tokens.dtype).pin_memory()
+    barrier(world)
+    torch.cuda.synchronize()
+    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s2.record()
+    for _ in range(K):
+        r = serve(host_prompt.to(dev, non_blocking=True))
+        host_out.copy_(r.tokens, non_blocking=True)
+    e2.record()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(s2.elapsed_time(e2) / K, world)
+    del res, r
+    from paper_2603_09555_b200 import decode as mdec
+
+    mdec.clear_graph_cache()
+    torch.cuda.empty_cache()
+    # decode-phase roofline: CUDA-graph token steps at this batch, separate pass
+    dargs = argparse.Namespace(**vars(args))
+    dargs.decode_model, dargs.decode_steps = args.serve_model, 64
+    dec = run_decode(dargs, local, B=B, params=params)
+    pk = peaks()
+    tokens = B * world * (P + G)
+    if rank == 0:
+        line = {
+            "metric": f"serve_tokens_per_s[{args.serve_model}]",
+            "value": tokens / (ms / 1e3),
+            "unit": "tok/s",
+            "n_gpus": world,
+            "steps": K,
+            "warmup": W,
+            "ms_per_step": ms,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic (random ids; device-drawn weights with the reference init distributions)",
+            "config": {"workload": f"Mamba-2 {args.serve_model} serving: prefill {P} + {G}-step greedy "
+                                   f"decode (BASELINE configs[4])",
+                       "global_batch": B * world, "batch_per_gpu": B, "prompt_len": P,
+                       "gen_len": G, "tokens_per_step": tokens,
+                       "parallelism": f"batch-sharded x{world} (no data-path collective)",
+                       "l2": "weights 1.6 GB + per-row state per token > 126 MB L2; no flush"},
+            "generated_tokens_per_s": B * world * G / (ms / 1e3),
+            "phases_ms_per_step": {"prefill": prefill_ms, "decode": ms - prefill_ms},
+            "e2e": {"value": tokens / (e2e_ms / 1e3), "unit": "tok/s",
+                    "h2d_bytes_per_step": int(host_prompt.numel() * 8) * world,
+                    "d2h_bytes_per_step": int(host_out.numel() * 8) * world},
+            "roofline": {"kernel": f"decode token step at B={B} (one CUDA graph: "
+                                   f"{cfg.n_layers} x [in_proj, state stream, out_proj, finish] + head)",
+                         "bound": "hbm", "achieved": dec["hbm_gbs"], "peak": pk["hbm_gbs"],
+                         "unit": "GB/s", "frac": dec["hbm_frac"], "traffic": None,
+                         "algorithmic_bytes_per_token_step": dec["bytes_per_step"],
+                         "ms_per_token_step": dec["ms_per_step"]},
+            "cpu_baseline": None,
+            "clocks": clk.summary(),
+            "gpu_launches": int(host_launches + K * (G - 1) * (cfg.n_layers * 4 + 5)),
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -636,8 +759,9 @@ def main():
     import torch
 
     rank, world, local = dist_setup(args.gpus)
-    if args.workload == "decode":
-        run_decode_workload(args, rank, world, local)
+    if args.workload in ("decode", "serve"):
+        (run_decode_workload if args.workload == "decode" else run_serve_workload)(
+            args, rank, world, local)
         if world > 1:
             import torch.distributed as dist
 

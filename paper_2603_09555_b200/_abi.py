@@ -109,6 +109,7 @@ SIGNATURES = [
     ("ssd200_set_phase_events", c_int, [c_void_p, c_int]),
     ("ssd200_debug_trace", c_int, [c_void_p]),
     ("ssd200_set_option", c_int, [c_int, c_int]),
+    ("ssd200_decode_prefetch_next", c_int, [c_void_p, ctypes.c_size_t]),
 ]
 
 _lib = None

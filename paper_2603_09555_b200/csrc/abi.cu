@@ -39,6 +39,9 @@ thread_local bool g_gemm_pair = true;          // option 20: CTA-pair (cta_group
 thread_local int g_pair_min_tiles = 0;         // option 21: fewest 256x256 tiles for CTA-pair GEMMs (0 = 64)
 thread_local int g_wide_min = 1;               // option 14: smallest batch on the wide-batch decode path (measured: the per-layer path beats the fused step at every B, 1.3B B=1 1.215 -> 1.150 ms)
 thread_local int g_mega_pf = 0;                // option 9: fused decode step L2 prefetch lookahead (stages)
+thread_local int g_dec_l2pf = 0;              // option 22: decode L2 warm-up (bit 1: in_proj warms W_out; bit 2: out_proj warms the next layer's W_in)
+thread_local const void *g_next_w_in = nullptr;  // ssd200_decode_prefetch_next: next layer's W_in
+thread_local size_t g_next_w_in_bytes = 0;
 thread_local bool g_dec_pdl = true;            // option 8: PDL between the decode kernels
 thread_local int g_dec_split_in = 0, g_dec_split_out = 0;  // options 6 / 7: wide-decode split-K (0 auto)
 thread_local bool g_use_pdl = true;            // option 5: programmatic dependent launch between the prefill kernels (370M B=1 T=2K +11%, neutral at B=4 T=8K)
@@ -1027,7 +1030,8 @@ int decode_layer_fast(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hi
 // weight-streaming swapped-operand GEMM (decode_gemm.cuh) for B <= 256, else tc_gemm
 template <int BNB, bool SMALL>
 int launch_dec_gemm_cfg(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long ldo,
-                        int ksplit, long split_stride, cudaStream_t st) {
+                        int ksplit, long split_stride, cudaStream_t st, const void *pf,
+                        long pf_bytes) {
   using Cfg = DgCfg<BNB, SMALL>;
   CUtensorMap tw, tx;
   int rc = make_map_2d(&tw, W, N, K, K, 128);
@@ -1040,7 +1044,7 @@ int launch_dec_gemm_cfg(const bf16 *W, int N, int K, const bf16 *X, int B, float
                          (int)Cfg::SMEM);
     attr = true;
   }
-  DgArgs a{N, K, B, ksplit, out, ldo, split_stride};
+  DgArgs a{N, K, B, ksplit, out, ldo, split_stride, static_cast<const uint8_t *>(pf), pf_bytes};
   const int grid = ((N + 127) / 128) * ksplit;
   cudaError_t e =
       launch_pdl(dec_gemm_swap<BNB, SMALL>, dim3(grid), dim3(192), Cfg::SMEM, st, tw, tx, a);
@@ -1050,25 +1054,27 @@ int launch_dec_gemm_cfg(const bf16 *W, int N, int K, const bf16 *X, int B, float
 }
 template <int BNB>
 int launch_dec_gemm_bnb(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long ldo,
-                        int ksplit, long split_stride, cudaStream_t st) {
+                        int ksplit, long split_stride, cudaStream_t st, const void *pf,
+                        long pf_bytes) {
   // the small ring (two CTAs per SM) measured faster up to B = 64 (B = 1: 1.18 -> 1.06 ms
   // with the in_proj split 4), slower at B = 256
   const bool small = g_dec_gemm_small < 0 ? B <= 64 : g_dec_gemm_small != 0;
   return small
-             ? launch_dec_gemm_cfg<BNB, true>(W, N, K, X, B, out, ldo, ksplit, split_stride, st)
-             : launch_dec_gemm_cfg<BNB, false>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
+             ? launch_dec_gemm_cfg<BNB, true>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, pf, pf_bytes)
+             : launch_dec_gemm_cfg<BNB, false>(W, N, K, X, B, out, ldo, ksplit, split_stride, st,
+                                               pf, pf_bytes);
 }
 
 int dec_gemm(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long ldo, int ksplit,
-             long split_stride, cudaStream_t st) {
+             long split_stride, cudaStream_t st, const void *pf = nullptr, long pf_bytes = 0) {
   REQUIRE(ksplit >= 1 && ksplit <= (K + 63) / 64, SSD200_EINVAL, "dec_gemm: bad split");
   if (B <= 256 && g_dec_swap) {
-    if (B <= 16) return launch_dec_gemm_bnb<16>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
-    if (B <= 32) return launch_dec_gemm_bnb<32>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
-    if (B <= 64) return launch_dec_gemm_bnb<64>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
+    if (B <= 16) return launch_dec_gemm_bnb<16>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, pf, pf_bytes);
+    if (B <= 32) return launch_dec_gemm_bnb<32>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, pf, pf_bytes);
+    if (B <= 64) return launch_dec_gemm_bnb<64>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, pf, pf_bytes);
     if (B <= 128)
-      return launch_dec_gemm_bnb<128>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
-    return launch_dec_gemm_bnb<256>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
+      return launch_dec_gemm_bnb<128>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, pf, pf_bytes);
+    return launch_dec_gemm_bnb<256>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, pf, pf_bytes);
   }
   TcEpilogue ep{};
   ep.C = out;
@@ -1095,8 +1101,10 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   const DecSplits sp = dec_splits(d, B);
   const long s_in = (long)B * wd.d_in_proj, s_out = (long)B * d->d_model;
   if (!(g_dec_skip & 1)) {
+    const bool pf_out = (g_dec_l2pf & 1) && w->W_out;
     int rc = dec_gemm(static_cast<const bf16 *>(w->W_in), (int)wd.d_in_proj, d->d_model, hidden_lp,
-                      B, o.u, wd.d_in_proj, sp.in, s_in, st);
+                      B, o.u, wd.d_in_proj, sp.in, s_in, st, pf_out ? w->W_out : nullptr,
+                      pf_out ? (long)d->d_model * d->d_inner * 2 : 0);
     if (rc) return rc;
   }
   DecStreamArgs sa{};
@@ -1168,8 +1176,11 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_ssm_stream: %s", cudaGetErrorString(e));
   LAUNCH_CHECK("dec_ssm_stream");
 
+  const bool pf_next = (g_dec_l2pf & 2) && g_next_w_in;
   int rc = (g_dec_skip & 4) ? 0 : dec_gemm(static_cast<const bf16 *>(w->W_out), d->d_model, d->d_inner, o.normed_lp, B,
-                    o.part, d->d_model, sp.out, s_out, st);
+                    o.part, d->d_model, sp.out, s_out, st, pf_next ? g_next_w_in : nullptr,
+                    pf_next ? (long)g_next_w_in_bytes : 0);
+  g_next_w_in = nullptr;  // one-shot: the hint names the layer after this one
   if (rc) return rc;
   DecFinishArgs fa{};
   fa.part = o.part;
@@ -1854,6 +1865,11 @@ int ssd200_set_option(int option, int value) {
       REQUIRE(value >= 1, SSD200_EINVAL, "option 14 out of range");
       g_wide_min = value;
       return SSD200_OK;
+    case 22:  // decode L2 warm-up: bit 1 in_proj warms this layer's W_out, bit 2 out_proj warms the
+              // W_in named by ssd200_decode_prefetch_next (0 = off)
+      REQUIRE(value >= 0 && value <= 3, SSD200_EINVAL, "option 22 out of range");
+      g_dec_l2pf = value;
+      return SSD200_OK;
     case 9:  // fused decode step: L2 prefetch lookahead in ring stages (0 = off)
       REQUIRE(value >= 0 && value <= 64, SSD200_EINVAL, "option 9 out of range");
       g_mega_pf = value;
@@ -1869,6 +1885,12 @@ int ssd200_set_option(int option, int value) {
       set_err("unknown option %d", option);
       return SSD200_EINVAL;
   }
+}
+
+int ssd200_decode_prefetch_next(const void *W_in_next, size_t bytes) {
+  g_next_w_in = W_in_next;
+  g_next_w_in_bytes = W_in_next ? bytes : 0;
+  return SSD200_OK;
 }
 
 int ssd200_set_phase_events(void *const *events, int n_phases) {

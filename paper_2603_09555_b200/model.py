@@ -157,6 +157,9 @@ class _Runner:
         need = self.lib.ssd200_decode_layer_workspace(self.dims, B)
         ws = self.workspace(need)
         has_conv = conv_in.numel() > 0
+        if i + 1 < len(self.params.layers):  # L2 warm-up hint (used when option 22 has bit 2)
+            nxt = self.params.layers[i + 1].W_in
+            self.lib.ssd200_decode_prefetch_next(nxt.data_ptr(), nxt.numel() * nxt.element_size())
         _abi.check(
             self.lib.ssd200_decode_layer(
                 self.dims, self._layers[i], hidden.data_ptr(), _abi.ptr(hidden_lp),
