@@ -574,3 +574,22 @@ def test_generate_graph_cache_reuse_is_exact():
     eb = m.generate(params, p2, 9, cfg=cfg, keep_logits=True, use_graph=False)
     assert torch.equal(a.tokens, ea.tokens) and torch.equal(a.per_step_logits, ea.per_step_logits)
     assert torch.equal(b.tokens, eb.tokens) and torch.equal(b.per_step_logits, eb.per_step_logits)
+
+
+def test_decode_l2_warmup_is_a_pure_hint():
+    """Option 22 (the decode GEMMs bulk-prefetch W_out / the next layer's W_in
+    into L2) only changes timing: logits and tokens are bitwise the default's."""
+    import paper_2603_09555_b200 as m
+    from paper_2603_09555_b200 import _abi
+
+    cfg = _bf16_cfg()
+    params = m.from_reference(m.random_init_host(cfg, 91), cfg)
+    prompt = np.random.default_rng(92).integers(0, cfg.vocab_size, size=(3, 20))
+    base = m.generate(params, prompt, 7, cfg=cfg, keep_logits=True, use_graph=False)
+    try:
+        _abi.lib().ssd200_set_option(22, 3)
+        pf = m.generate(params, prompt, 7, cfg=cfg, keep_logits=True, use_graph=False)
+    finally:
+        _abi.lib().ssd200_set_option(22, 0)
+    assert torch.equal(base.tokens, pf.tokens)
+    assert torch.equal(base.per_step_logits, pf.per_step_logits)
