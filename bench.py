@@ -751,6 +751,13 @@ def run_serve_workload(args, rank, world, local):
         print(json.dumps(line), flush=True)
 
 
+def _weight_gb(model):
+    import paper_2603_09555_b200 as m
+    from paper_2603_09555_b200 import cost
+
+    return cost.n_params(m.named_config(model, compute="bf16")) * 2 / 1e9
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -806,7 +813,9 @@ def main():
             "dtype": "bf16",
             "data": "synthetic (random ids; device-drawn weights with the reference init distributions)",
             "config": {
-                "workload": f"Mamba-2 {args.model} bf16 chunked-SSD prefill (BASELINE configs[1] sweep point)",
+                "workload": f"Mamba-2 {args.model} bf16 chunked-SSD prefill "
+                            + ("(BASELINE configs[3])" if args.model.lower() == "2.7b"
+                               else "(BASELINE configs[1] sweep point)"),
                 "batch_per_gpu": args.batch if not heads else args.batch / world,
                 "global_batch": args.batch if heads else args.batch * world,
                 "seq_len": args.seqlen,
@@ -814,7 +823,8 @@ def main():
                 "head": "tied head on the last position only",
                 "parallelism": (f"SSD-head-group-sharded x{world} (one NCCL all-reduce per layer)"
                                 if heads else f"batch-sharded x{world} (no data-path collective)"),
-                "l2": "working set > 126 MB L2 (activations + 0.74 GB weights per step); no flush",
+                "l2": f"working set > 126 MB L2 (activations + {_weight_gb(args.model):.2f} GB bf16 weights per "
+                      "step); no flush",
             },
             "tflops_per_gpu": res["step_tflops_per_gpu"],
             "mfu": res["step_mfu"],
