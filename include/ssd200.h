@@ -194,10 +194,11 @@ int ssd200_debug_trace(void *device_buffer);
  * default; 9 = fused persistent step for B <= 8); 15 = swapped-operand decode
  * GEMMs (1 default) or tc_gemm (0); 16 = profiling only: skip decode kernels
  * (bit mask 1 in_proj, 2 stream, 4 out_proj, 8 finish); 17 = decode-GEMM
- * ~96 KB ring, two CTAs per SM (-1 auto: B <= 64, 0, 1); 22 = decode L2
+ * ~96 KB ring, two CTAs per SM (-1 auto: B <= option 23, 0, 1); 22 = decode L2
  * warm-up (bit 1: the in_proj GEMM bulk-prefetches the layer's W_out into L2
  * while it streams W_in; bit 2: the out_proj GEMM prefetches the W_in named
- * by ssd200_decode_prefetch_next; 0 default). */
+ * by ssd200_decode_prefetch_next; 0 default); 23 = largest batch on the
+ * decode GEMMs' ~96 KB ring while option 17 is auto. */
 int ssd200_set_option(int option, int value);
 
 /* Names the next layer's W_in (bytes) for option 22 bit 2; consumed (one

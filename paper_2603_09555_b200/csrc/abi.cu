@@ -33,6 +33,7 @@ thread_local bool g_chunkscan_mc = true;       // option 3: B-tile multicast in 
 thread_local int g_out_waves = 1;              // option 4: target CTAs (x SMs) of the output kernel
 thread_local int g_stream_stages = 0, g_stream_cps = 0, g_stream_cw = 8;  // options 11 / 12 / 13
 thread_local int g_dec_gemm_small = -1;        // option 17: decode GEMM ~96 KB ring (two CTAs per SM); -1 auto
+thread_local int g_dec_small_max = 48;         // option 23: largest batch on the ~96 KB ring when option 17 is auto (measured: small ring B = 32 2.23 -> 2.12 ms, big ring B = 64 3.47 -> 3.37 ms)
 thread_local int g_dec_skip = 0;               // option 16: profiling only — skip decode kernels (bit mask)
 thread_local bool g_dec_swap = true;           // option 15: swapped-operand decode GEMM (else tc_gemm)
 thread_local bool g_gemm_pair = true;          // option 20: CTA-pair (cta_group::2) prefill GEMMs (370M prefill +3.6%, 2.7B +11%)
@@ -878,7 +879,8 @@ inline DecSplits dec_splits(const ssd200_dims_t *d, int B) {
   const long mt = B <= 256 ? 1 : (B + 127) / 128;  // dec_gemm_swap: one tile covers the batch
   DecSplits r;
   r.in = pick(mt * ((w.d_in_proj + 127) / 128), d->d_model);
-  if (B <= 64 && g_dec_gemm_small != 0) {  // two CTAs per SM: twice the units
+  const bool small = g_dec_gemm_small < 0 ? B <= g_dec_small_max : g_dec_gemm_small != 0;
+  if (small && B <= 256) {  // two CTAs per SM: twice the units
     const int s2 = 2 * ((int)num_sms() / (int)((w.d_in_proj + 127) / 128));
     int cap = (d->d_model + 63) / 64 / 4;
     if (cap < 1) cap = 1;
@@ -1058,7 +1060,7 @@ int launch_dec_gemm_bnb(const bf16 *W, int N, int K, const bf16 *X, int B, float
                         long pf_bytes) {
   // the small ring (two CTAs per SM) measured faster up to B = 64 (B = 1: 1.18 -> 1.06 ms
   // with the in_proj split 4), slower at B = 256
-  const bool small = g_dec_gemm_small < 0 ? B <= 64 : g_dec_gemm_small != 0;
+  const bool small = g_dec_gemm_small < 0 ? B <= g_dec_small_max : g_dec_gemm_small != 0;
   return small
              ? launch_dec_gemm_cfg<BNB, true>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, pf, pf_bytes)
              : launch_dec_gemm_cfg<BNB, false>(W, N, K, X, B, out, ldo, ksplit, split_stride, st,
@@ -1847,7 +1849,10 @@ int ssd200_set_option(int option, int value) {
       g_stream_cps = value;
       return SSD200_OK;
     case 17:  // decode GEMMs: ~96 KB smem ring so consecutive kernels share SMs (1), 192 KB (0), auto (-1)
-      g_dec_gemm_small = value != 0;
+      g_dec_gemm_small = value < 0 ? -1 : value != 0;
+      return SSD200_OK;
+    case 23:  // largest batch on the decode GEMMs' ~96 KB ring while option 17 is auto
+      g_dec_small_max = value;
       return SSD200_OK;
     case 16:  // profiling only: skip wide-decode kernels (1 in_proj, 2 stream, 4 out_proj, 8 finish)
       g_dec_skip = value;

@@ -27,7 +27,7 @@ def main():
     args = ap.parse_args()
     cfg = m.named_config(args.model, compute="bf16")
     params = m.synthetic_init(cfg, seed=0)
-    defaults = {6: 0, 7: 0, 8: 1, 9: 0, 11: 0, 12: 0, 13: 8, 14: 1, 15: 1, 16: 0, 17: -1, 22: 0}
+    defaults = {6: 0, 7: 0, 8: 1, 9: 0, 11: 0, 12: 0, 13: 8, 14: 1, 15: 1, 16: 0, 17: -1, 22: 0, 23: 48}
     for B in args.batch or [64]:
         prompt = torch.randint(0, cfg.vocab_size, (B, 16), device="cuda")
         _, cache = m.prefill(params, prompt, cfg, logits=None)
