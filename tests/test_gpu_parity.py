@@ -485,9 +485,10 @@ def test_bf16_wide_batch_decode_state_vs_oracle(B):
 
 
 def test_bf16_decode_batch_invariance_bitwise():
-    """bf16 decode rows do not depend on the batch they run in (the decode GEMMs'
-    split-K factors depend only on the widths for B <= 256): the basis of batch
-    sharding for decode."""
+    """bf16 decode rows do not depend on the batch they run in, within one decode
+    GEMM class (here both batches are on the ~96 KB ring; at these widths the
+    split-K factors coincide for every B): the basis of batch sharding for
+    decode."""
     import paper_2603_09555_b200 as m
 
     cfg = _bf16_cfg()
@@ -593,3 +594,31 @@ def test_decode_l2_warmup_is_a_pure_hint():
         _abi.lib().ssd200_set_option(22, 0)
     assert torch.equal(base.tokens, pf.tokens)
     assert torch.equal(base.per_step_logits, pf.per_step_logits)
+
+
+def test_bf16_decode_batch_invariance_across_gemm_classes():
+    """At production widths (1.3B: d_model 2048) the in_proj split-K differs
+    between the ~96 KB-ring class (B <= 48: split 4) and the 192 KB-ring class
+    (split 2), so the f32 partial sums are added in a different order.  Forcing
+    one ring (option 17) makes the split a function of the widths only: rows are
+    then bitwise batch-invariant across B = 2 and B = 64.  Without forcing, rows
+    agree to f32 rounding of the partial sums."""
+    import paper_2603_09555_b200 as m
+    from paper_2603_09555_b200 import _abi
+
+    cfg = m.named_config("1.3b", compute="bf16", vocab_size=512, n_layers=1)
+    params = m.from_reference(m.random_init_host(cfg, 61), cfg)
+    toks = np.random.default_rng(62).integers(0, cfg.vocab_size, size=(64, 12))
+    lib = _abi.lib()
+    try:
+        lib.ssd200_set_option(17, 1)
+        full = m.generate(params, toks, 4, cfg=cfg, keep_logits=True, use_graph=False)
+        part = m.generate(params, toks[5:7], 4, cfg=cfg, keep_logits=True, use_graph=False)
+        assert torch.equal(full.tokens[5:7], part.tokens)
+        assert torch.equal(full.per_step_logits[5:7, 1:], part.per_step_logits[:, 1:])
+    finally:
+        lib.ssd200_set_option(17, -1)
+    auto = m.generate(params, toks, 4, cfg=cfg, keep_logits=True, use_graph=False)
+    a, b = auto.per_step_logits[5:7, 1:], part.per_step_logits[:, 1:]
+    rel = float((a - b).norm() / b.norm())
+    assert rel < 1e-2, rel
