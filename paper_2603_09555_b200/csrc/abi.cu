@@ -1058,8 +1058,8 @@ template <int BNB>
 int launch_dec_gemm_bnb(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long ldo,
                         int ksplit, long split_stride, cudaStream_t st, const void *pf,
                         long pf_bytes) {
-  // the small ring (two CTAs per SM) measured faster up to B = 64 (B = 1: 1.18 -> 1.06 ms
-  // with the in_proj split 4), slower at B = 256
+  // the small ring (two CTAs per SM) measured faster up to B = 32 (B = 1: 1.18 -> 1.06 ms
+  // with the in_proj split 4), slower from B = 64 (3.37 vs 3.47 ms) and at B = 256
   const bool small = g_dec_gemm_small < 0 ? B <= g_dec_small_max : g_dec_gemm_small != 0;
   return small
              ? launch_dec_gemm_cfg<BNB, true>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, pf, pf_bytes)
