@@ -622,3 +622,26 @@ def test_bf16_decode_batch_invariance_across_gemm_classes():
     a, b = auto.per_step_logits[5:7, 1:], part.per_step_logits[:, 1:]
     rel = float((a - b).norm() / b.norm())
     assert rel < 1e-2, rel
+
+
+@pytest.mark.parametrize("B", [64, 200, 264])
+def test_bf16_decode_production_width_wide_batches_vs_oracle(B):
+    """One decode step at 370M widths (d_model 1024, 32 heads of 64 x 128) on the
+    192 KB-ring swapped GEMMs (B = 64: 64-row tiles; B = 200: 256-row tiles) and
+    on the tc_gemm path past 256 rows (B = 264): logits and the updated SSM /
+    conv cache against the oracle on bf16-rounded weights."""
+    import paper_2603_09555_b200 as m
+
+    cfg = m.named_config("370m", compute="bf16", vocab_size=512, n_layers=1)
+    host = m.random_init_host(cfg, 71)
+    params = m.from_reference(host, cfg)
+    toks = np.random.default_rng(72).integers(0, cfg.vocab_size, size=(B, 10))
+    _, cache = m.prefill(params, toks[:, :9], cfg, logits=None)
+    sl, new = m.decode_step(params, cache, toks[:, 9], cfg)
+    rl, rs, rc = orc.prefill(orc.round_weights_bf16(host), toks, cfg.with_policy(compute="f32"))
+    rel = np.linalg.norm(_np(sl) - rl[:, -1]) / np.linalg.norm(rl[:, -1])
+    assert rel <= BF16_BOUND, rel
+    rs = np.stack(rs)
+    assert np.linalg.norm(_np(new.ssm_all) - rs) / np.linalg.norm(rs) <= BF16_BOUND
+    rc = np.stack(rc)
+    assert np.linalg.norm(_np(new.conv_all) - rc) / np.linalg.norm(rc) <= BF16_BOUND
