@@ -645,6 +645,21 @@ struct DssLayout {
 };
 
 // CW consumer warps (RPW = P / CW rows each) + 1 producer warp
+// sum_j p[j * stride] for j = 0 .. n-1, added in j order (the split-K partials'
+// fixed reduction order), with the first 16 loads issued together: a dependent
+// load -> add chain cost one memory latency per split
+__device__ __forceinline__ float sum_splits(const float *__restrict__ p, long stride, int n) {
+  float v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = j < n ? __ldcg(p + j * stride) : 0.f;
+  float acc = 0.f;
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (j < n) acc += v[j];
+  for (int j = 16; j < n; ++j) acc += __ldcg(p + j * stride);
+  return acc;
+}
+
 template <int NQ, int RPW, int CW>
 __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(DecStreamArgs a) {
   constexpr int CT = CW * 32;
@@ -757,9 +772,8 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
   griddep_wait();
   for (int i = threadIdx.x; i < cnt; i += CT) {
     const int t = t0 + i, b = t / H, h = t % H;
-    float raw = 0.f;
-    for (int j = 0; j < ns; ++j)
-      raw += a.proj[j * a.sstride + (size_t)b * a.ldp + a.d_inner + a.conv_dim + h];
+    const float raw = sum_splits(a.proj + (size_t)b * a.ldp + a.d_inner + a.conv_dim + h,
+                                 a.sstride, ns);
     const float dt = clamp_(softplus(raw + a.dt_bias[h]), a.dt_lo, a.dt_hi);
     hdr[i] = make_float2(dt, expf(a.a[h] * dt));
   }
@@ -937,8 +951,7 @@ __global__ __launch_bounds__(256) void dec_out_finish(DecFinishArgs a) {
   if ((int)blockIdx.x >= nb_h) {
     const int c = a.d_inner + ((int)blockIdx.x - nb_h) * 256 + threadIdx.x;  // B / C channel
     if (c >= a.conv_dim) return;
-    float v = 0.f;
-    for (int j = 0; j < a.pnsplit; ++j) v += a.proj[j * a.psstride + (long)b * a.ldp + a.d_inner + c];
+    const float v = sum_splits(a.proj + (long)b * a.ldp + a.d_inner + c, a.psstride, a.pnsplit);
     const float *ci = a.conv_in + ((long)b * a.conv_dim + c) * 3;
     float *co = a.conv_out + ((long)b * a.conv_dim + c) * 3;
     const float w1 = ci[1], w2 = ci[2];
@@ -948,9 +961,7 @@ __global__ __launch_bounds__(256) void dec_out_finish(DecFinishArgs a) {
     return;
   }
   // the split-K partials are requested before the row's norm reduction
-  float acc = 0.f;
-  if (live)
-    for (int j = 0; j < a.nsplit; ++j) acc += a.part[j * a.sstride + (long)b * a.d_model + n];
+  const float acc = live ? sum_splits(a.part + (long)b * a.d_model + n, a.sstride, a.nsplit) : 0.f;
   if (threadIdx.x < 32) {
     float t = 0.f;
     for (int h = threadIdx.x; h < a.H; h += 32) t += a.ssq[(long)b * a.H + h];
