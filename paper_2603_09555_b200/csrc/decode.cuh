@@ -644,7 +644,6 @@ struct DssLayout {
   }
 };
 
-// CW consumer warps (RPW = P / CW rows each) + 1 producer warp
 // sum_j p[j * stride] for j = 0 .. n-1, added in j order (the split-K partials'
 // fixed reduction order), with the first 16 loads issued together: a dependent
 // load -> add chain cost one memory latency per split
@@ -660,6 +659,7 @@ __device__ __forceinline__ float sum_splits(const float *__restrict__ p, long st
   return acc;
 }
 
+// CW consumer warps (RPW = P / CW rows each) + 1 producer warp
 template <int NQ, int RPW, int CW>
 __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(DecStreamArgs a) {
   constexpr int CT = CW * 32;
