@@ -1,21 +1,30 @@
 """Benchmark of the Mamba-2 SSD hot path on B200 (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload prefill|decode|serve] [--model 370m] [--batch B] [--seqlen T]
+                    [--workload prefill|decode|serve] [--model 2.7b] [--batch 32] [--seqlen 8192]
+                    [--shard batch|heads] [--tune field=value ...]
 
-Headline (BASELINE.json configs[1]): Mamba-2 370M bf16 chunked-SSD prefill,
-per-GPU batch B x T tokens, one step = one full prefill (embed, 48 blocks,
-final norm, tied head on the last position) over a batch already resident in
-HBM.  ``value`` = tokens/s summed over ranks (weak scaling: batch-sharded,
-no collective on the data path).  ``e2e`` = the same metric through the
-public API ``prefill`` with the token ids copied from pinned host memory
-and the last-position logits copied back, inside the timed region.
+Headline (BASELINE.json configs[3], the north-star's C4): Mamba-2 2.7B bf16
+chunked-SSD prefill of a GLOBAL batch of 32 sequences x 8192 tokens, one step
+= one full prefill (embed, 64 blocks, final norm, tied head on the last
+position) over token ids already resident in HBM.  The global batch is split
+over the ranks (strong scaling: batch-sharded rows, no collective on the data
+path; ``--shard heads`` instead splits every layer's SSD head groups with one
+NCCL all-reduce after out_proj).  ``value`` = global tokens / max-over-ranks
+step time.  ``e2e`` = the same metric through the public API ``prefill`` with
+the token ids copied from pinned host memory and the last-position logits
+copied back, inside the timed region.
+
+``--gpus N`` with no torchrun environment re-launches itself through
+``torch.distributed.run`` with N ranks on 127.0.0.1 (NCCL_DEBUG=INFO to
+stderr, so the rank count is on record).
 
 The JSON line also carries: ``roofline`` for the dominant kernel (timed live
-with CUDA events around every launch of that phase inside the timed region),
-per-phase time shares, ``cpu_baseline`` (the numpy oracle port of the
-reference timed on this host, bounded sample, rank 0 at N=1), ``decode``
-(1.3B cached decode: tok/s and HBM GB/s of a CUDA-graph step), ``clocks``
+with CUDA events around every launch of that phase), per-phase time shares,
+``cpu_baseline`` (the numpy oracle port of the reference timed on this host,
+bounded sample, rank 0 at N=1), and at N=1 two extra points: ``c2`` (370M
+prefill, B=4, T=8192, BASELINE configs[1]) and ``decode`` (1.3B cached decode
+sweep, configs[2]: tok/s and HBM GB/s of CUDA-graph steps), plus ``clocks``
 sampled by nvidia-smi during the timed region and ``gpu_launches``.
 
 ``--impl reference`` times the reference algorithm's CPU implementation (the
@@ -50,32 +59,53 @@ PHASES = ("in_proj", "conv", "scan", "gated_norm", "out_proj")
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--workload", default="prefill", choices=("prefill", "decode", "serve"))
-    ap.add_argument("--model", default="370m")
-    ap.add_argument("--batch", type=int, default=4, help="per-GPU batch")
+    ap.add_argument("--model", default="2.7b")
+    ap.add_argument("--batch", type=int, default=32, help="GLOBAL prefill batch (split over ranks)")
     ap.add_argument("--seqlen", type=int, default=8192)
+    ap.add_argument("--c2-model", default="370m")
+    ap.add_argument("--c2-batch", type=int, default=4)
+    ap.add_argument("--c2-seqlen", type=int, default=8192)
+    ap.add_argument("--no-c2", action="store_true")
     ap.add_argument("--decode-model", default="1.3b")
     ap.add_argument("--serve-model", default="780m")
     ap.add_argument("--serve-batch", type=int, default=64, help="GLOBAL batch (split over ranks)")
     ap.add_argument("--serve-prompt", type=int, default=4096)
     ap.add_argument("--serve-gen", type=int, default=512)
     ap.add_argument("--decode-batch", type=int, default=1)
-    ap.add_argument("--decode-sweep", default="2,8,16,64,128,256",
-                    help="extra decode batch sizes reported under decode.sweep ('' = none)")
+    ap.add_argument("--decode-sweep", default="1,8,64,256",
+                    help="decode batch sizes reported under decode.sweep ('' = none)")
     ap.add_argument("--decode-steps", type=int, default=64)
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seqlen", type=int, default=2048,
+                    help="sequence length of the bounded CPU sample (extrapolated linearly in T)")
     ap.add_argument("--shard", default="batch", choices=("batch", "heads"),
-                    help="N>1 prefill: batch rows per rank (weak scaling, default) or SSD head "
-                         "groups of one batch with an all-reduce after out_proj (strong scaling)")
-    ap.add_argument("--opt", action="append", default=[],
-                    help="library implementation option k=v (ssd200_set_option), repeatable")
-    ap.add_argument("--fused-conv", default="auto", choices=("auto", "on", "off"),
-                    help="conv1d fused into the in_proj epilogue (default: by width)")
+                    help="N>1: batch rows per rank (default) or SSD head groups of the whole "
+                         "batch with an all-reduce after out_proj")
+    ap.add_argument("--tune", action="append", default=[],
+                    help="implementation choice field=value (ssd200_tuning_t), repeatable")
     return ap.parse_args()
+
+
+def self_launch(args):
+    """--gpus N outside torchrun: re-exec this script under torch.distributed.run
+    with N local ranks (rendezvous on 127.0.0.1) and return its exit status."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # keep stdout to the one JSON line
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 # ---------------------------------------------------------------- distributed
@@ -253,7 +283,7 @@ def run_reference_arm(args):
     if rank != 0:
         return
     K, W = args.steps, args.warmup
-    T = 1024 if args.seqlen > 1024 else args.seqlen
+    T = min(args.cpu_seqlen, args.seqlen)
     vals = []
     for i in range(W + K):
         v, _, desc = cpu_prefill_sample(args.model, T=T, layers=1)
@@ -272,7 +302,7 @@ def run_reference_arm(args):
         "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": f"Mamba-2 {args.model} prefill (reference CPU path, numpy oracle port)",
-                   "batch_per_gpu": args.batch, "seq_len": args.seqlen, "sample_seq_len": T},
+                   "global_batch": args.batch, "seq_len": args.seqlen, "sample_seq_len": T},
         "cpu_baseline": {"value": val, "unit": "tok/s", "cores": _NCPU, "kind": "port",
                          "sample": desc},
         "e2e": {"value": val, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -298,19 +328,17 @@ def run_prefill(args, rank, world, local):
     import torch
 
     import paper_2603_09555_b200 as m
-    from paper_2603_09555_b200 import _abi, model as mmod
+    from paper_2603_09555_b200 import _abi, model as mmod, shard
 
     cfg = m.named_config(args.model, compute="bf16")
-    params = m.synthetic_init(cfg, seed=1234 + rank, device=f"cuda:{local}")
-    B, T = args.batch, args.seqlen
-    g = torch.Generator(device="cpu").manual_seed(rank)
-    host_tok = torch.randint(0, cfg.vocab_size, (B, T), generator=g, dtype=torch.int64).pin_memory()
+    params = m.synthetic_init(cfg, seed=1234, device=f"cuda:{local}")
+    rows = shard.batch_slice(args.batch, rank, world)  # this rank's rows of the global batch
+    B, T = rows.stop - rows.start, args.seqlen
+    g = torch.Generator(device="cpu").manual_seed(0)
+    host_all = torch.randint(0, cfg.vocab_size, (args.batch, T), generator=g, dtype=torch.int64)
+    host_tok = host_all[rows].contiguous().pin_memory()
     dev_tok = host_tok.cuda()
     lib = _abi.lib()
-    lib.ssd200_set_option(1, {"auto": 0, "on": 1, "off": 0}[args.fused_conv])
-    for kv in args.opt:
-        k, v = kv.split("=")
-        lib.ssd200_set_option(int(k), int(v))
 
     # per-phase CUDA events around every layer's phases (5 phases x 2)
     L = cfg.n_layers
@@ -352,7 +380,7 @@ def run_prefill(args, rank, world, local):
     launches = lib.ssd200_launch_count() - n0
     ms = start.elapsed_time(stop) / K
     ms_max = max_over_ranks(ms, world)
-    tokens_total = B * T * world
+    tokens_total = args.batch * T
     value = tokens_total / (ms_max / 1e3)
 
     # e2e through the public API: pinned host ids -> device, logits -> host
@@ -417,22 +445,51 @@ def run_prefill(args, rank, world, local):
         "avg_launch_ms": launch_ms,
         "peak_source": pk["source"] + ", sustained (kernel timed inside a long step)",
     }
-    step_tflops = flops_step / (ms_max / 1e3) / 1e12
+    step_tflops = flops_step / (ms / 1e3) / 1e12  # this rank's work / its own time
+    del params, dev_tok
     return {
         "value": value,
         "ms": ms_max,
         "e2e_ms": e2e_ms,
         "e2e_value": tokens_total / (e2e_ms / 1e3),
-        "h2d": B * T * 8,
-        "d2h": B * cfg.vocab_size * 4,
+        "d2h_global": args.batch * cfg.vocab_size * 4,
         "launches": launches,
         "roofline": roof,
         "phases_ms": {PHASES[p]: float(phase_ms[p]) for p in range(5)},
-        "step_tflops_per_gpu": step_tflops / world,
-        "step_mfu": step_tflops / world / pk["bf16_tflops"],
+        "step_tflops_per_gpu": step_tflops,
+        "step_mfu": step_tflops / pk["bf16_tflops"],
         "clocks": clk.summary(),
         "flops_step": flops_step,
+        "batch_per_gpu": B,
     }
+
+
+def run_prefill_point(model, B, T, K, W, local):
+    """One extra prefill point (no phase pass, no e2e): tok/s and TFLOP/s."""
+    import torch
+
+    import paper_2603_09555_b200 as m
+
+    cfg = m.named_config(model, compute="bf16")
+    params = m.synthetic_init(cfg, seed=99, device=f"cuda:{local}")
+    tok = torch.randint(0, cfg.vocab_size, (B, T), device=f"cuda:{local}")
+    for _ in range(W):
+        m.prefill(params, tok, cfg, logits="last")
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(K):
+        m.prefill(params, tok, cfg, logits="last")
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / K
+    tf = m.flops_prefill(cfg, T, B, head_rows=1) / (ms / 1e3) / 1e12
+    pk = peaks()
+    del params, tok
+    torch.cuda.empty_cache()
+    return {"workload": f"Mamba-2 {model} bf16 prefill (BASELINE configs[1] point)", "batch": B,
+            "seq_len": T, "value": B * T / (ms / 1e3), "unit": "tok/s", "ms_per_step": ms,
+            "tflops": tf, "mfu": tf / pk["bf16_tflops"], "steps": K, "warmup": W}
 
 
 def run_prefill_heads(args, rank, world, local):
@@ -489,7 +546,7 @@ def run_prefill_heads(args, rank, world, local):
     tf = flops / (ms / 1e3) / 1e12
     return {
         "value": B * T / (ms / 1e3), "ms": ms, "e2e_value": B * T / (e2e_ms / 1e3),
-        "h2d": B * T * 8, "d2h": B * cfg.vocab_size * 4, "launches": launches,
+        "d2h_global": B * cfg.vocab_size * 4, "launches": launches, "batch_per_gpu": B,
         "roofline": {"kernel": "whole step (head-sharded)", "bound": "tensor", "achieved": tf / world,
                      "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
                      "frac": tf / world / pk["bf16_tflops_sustained"], "traffic": None},
@@ -541,6 +598,84 @@ def run_decode(args, local, B=None, params=None):
                  "stream (conv + SSM update + gate + sum u^2), out_proj, norm + residual finish; "
                  "head + argmax"),
     }
+
+
+def run_decode_heads(args, rank, world, local):
+    """``--workload decode --shard heads``: one batch of ``--decode-batch`` rows
+    decoded by all ranks, each owning n_heads / N SSD heads of every layer; the
+    token step (every layer's partial in_proj / state stream / out_proj, ONE
+    NCCL all-reduce of [partial | sum u^2] per layer, finish, head, argmax) is
+    one captured CUDA graph (shard.HeadShardedGraphDecoder).  Strong scaling:
+    value = B / max-over-ranks token-step time."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_09555_b200 as m
+    from paper_2603_09555_b200 import cost, shard
+
+    cfg = m.named_config(args.decode_model, compute="bf16")
+    dev = f"cuda:{local}"
+    params = shard.synthetic_shard(cfg, rank, world, seed=7, device=dev)
+    B, W = args.decode_batch, args.warmup
+    n = max(args.steps, 1) * 16
+    prompt = torch.randint(0, cfg.vocab_size, (B, 16), generator=torch.Generator().manual_seed(5))
+    run = shard.HeadShardedPrefill(params, prompt.to(dev), cfg)
+    for i in range(cfg.n_layers):
+        buf = run.partial(i)
+        if world > 1:
+            dist.all_reduce(buf)
+        run.finish()
+    tok = torch.empty((B,), dtype=torch.int64, device=dev)
+    run.logits(argmax=tok)
+    gd = shard.HeadShardedGraphDecoder([shard.HeadShardedDecoder.from_prefill(run)],
+                                       n + 16 * W + 2,
+                                       reduce=shard.nccl_reduce() if world > 1 else None)
+    gd.set_token(tok)
+    gd.step_idx.fill_(1)
+    for _ in range(16 * W):
+        gd.step()
+    with ClockSampler(local) as clk:
+        barrier(world)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(n):
+            gd.step()
+        e.record()
+        torch.cuda.synchronize()
+        barrier(world)
+    ms = max_over_ranks(s.elapsed_time(e) / n, world)
+    loc = params.local
+    # this rank's algorithmic bytes: its weight shard (+ the replicated embedding /
+    # head), its heads' state read + written, the logits
+    nbytes = (cost.decode_step_bytes(cfg, B) - cost.weight_bytes(cfg) - 2 * cost.cache_bytes(cfg, B)
+              + sum(t.numel() * t.element_size() for lp in params.layers
+                    for t in (lp.W_in, lp.W_out))
+              + params.embedding.numel() * 2
+              + 2 * cfg.n_layers * B * (loc.n_heads * cfg.head_dim * cfg.d_state
+                                        + loc.conv_dim * (cfg.conv_kernel - 1)) * 4)
+    gbs = nbytes / (ms / 1e3) / 1e9
+    pk = peaks()
+    if rank == 0:
+        print(json.dumps({
+            "metric": f"decode_tokens_per_s[{args.decode_model}]",
+            "value": B / (ms / 1e3), "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+            "warmup": W, "ms_per_step": ms * 16, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random ids; device-drawn weights with the reference init distributions)",
+            "config": {"workload": f"Mamba-2 {args.decode_model} bf16 cached decode, SSD-head-group "
+                                   f"sharded (BASELINE configs[2])",
+                       "global_batch": B, "heads_per_gpu": loc.n_heads,
+                       "step": "16 greedy tokens (one captured CUDA graph per token, the per-layer "
+                               "NCCL all-reduce inside it)",
+                       "parallelism": f"head-group-sharded x{world}"},
+            "ms_per_token": ms,
+            "roofline": {"kernel": "head-sharded decode token step (one CUDA graph)", "bound": "hbm",
+                         "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": gbs / pk["hbm_gbs"], "traffic": None,
+                         "algorithmic_bytes_per_token_step_per_gpu": nbytes},
+            "e2e": None, "cpu_baseline": None, "clocks": clk.summary(),
+            "gpu_launches": n * (cfg.n_layers * 5 + 5),
+        }), flush=True)
 
 
 def run_decode_workload(args, rank, world, local):
@@ -763,12 +898,33 @@ def main():
     if args.impl == "reference":
         run_reference_arm(args)
         return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(self_launch(args))
+    from paper_2603_09555_b200 import _abi
+
+    opts = dict(kv.split("=") for kv in args.tune)
+    with _abi.tuning(**opts) if opts else _nullctx():
+        run(args)
+
+
+class _nullctx:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
+
+
+def run(args):
     import torch
 
     rank, world, local = dist_setup(args.gpus)
     if args.workload in ("decode", "serve"):
-        (run_decode_workload if args.workload == "decode" else run_serve_workload)(
-            args, rank, world, local)
+        if args.workload == "decode" and args.shard == "heads":
+            run_decode_heads(args, rank, world, local)
+        else:
+            (run_decode_workload if args.workload == "decode" else run_serve_workload)(
+                args, rank, world, local)
         if world > 1:
             import torch.distributed as dist
 
@@ -777,25 +933,28 @@ def main():
         return
     heads = args.shard == "heads"
     res = (run_prefill_heads if heads else run_prefill)(args, rank, world, local)
-    dec = None
-    if not args.no_decode:
-        dec = run_decode(args, local)
-        sweep = [int(x) for x in args.decode_sweep.split(",") if x.strip()]
-        if sweep:
-            import paper_2603_09555_b200 as m
+    torch.cuda.empty_cache()
+    c2 = dec = cpu = None
+    if world == 1 and not args.no_c2:  # extra points at N=1 (the scaling runs stay short)
+        c2 = run_prefill_point(args.c2_model, args.c2_batch, args.c2_seqlen, args.steps,
+                               args.warmup, local)
+    if world == 1 and not args.no_decode:
+        import paper_2603_09555_b200 as m
 
-            dcfg = m.named_config(args.decode_model, compute="bf16")
-            dparams = m.synthetic_init(dcfg, seed=7, device=f"cuda:{local}")
-            dec["sweep"] = []
-            for b in sweep:
-                r = run_decode(args, local, B=b, params=dparams)
-                dec["sweep"].append({k: r[k] for k in ("batch", "ms_per_step", "tok_per_s",
-                                                       "hbm_gbs", "hbm_frac", "bytes_per_step")})
-            del dparams
-            torch.cuda.empty_cache()
-    cpu = None
+        dcfg = m.named_config(args.decode_model, compute="bf16")
+        dparams = m.synthetic_init(dcfg, seed=7, device=f"cuda:{local}")
+        sweep = [int(x) for x in args.decode_sweep.split(",") if x.strip()] or [args.decode_batch]
+        dec = {"model": args.decode_model, "workload": "BASELINE configs[2]: cached decode, "
+               "CUDA-graph token steps", "sweep": []}
+        for b in sweep:
+            r = run_decode(args, local, B=b, params=dparams)
+            dec["sweep"].append({k: r[k] for k in ("batch", "ms_per_step", "tok_per_s",
+                                                   "hbm_gbs", "hbm_frac", "bytes_per_step")})
+        del dparams
+        torch.cuda.empty_cache()
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, secs, desc = cpu_prefill_sample(args.model, T=args.seqlen, layers=1)
+        v, secs, desc = cpu_prefill_sample(args.model, T=min(args.cpu_seqlen, args.seqlen),
+                                           layers=1)
         cpu = {"value": v, "unit": "tok/s", "cores": _NCPU, "kind": "port", "sample": desc,
                "seconds": secs}
     if rank == 0:
@@ -808,35 +967,40 @@ def main():
             "warmup": args.warmup,
             "ms_per_step": res["ms"],
             "higher_is_better": True,
-            "scaling": "strong" if heads else "weak",
+            "scaling": "strong",
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic (random ids; device-drawn weights with the reference init distributions)",
             "config": {
                 "workload": f"Mamba-2 {args.model} bf16 chunked-SSD prefill "
-                            + ("(BASELINE configs[3])" if args.model.lower() == "2.7b"
-                               else "(BASELINE configs[1] sweep point)"),
-                "batch_per_gpu": args.batch if not heads else args.batch / world,
-                "global_batch": args.batch if heads else args.batch * world,
+                            + ("(BASELINE configs[3], north-star C4)" if args.model.lower() == "2.7b"
+                               else "(BASELINE configs[1] point)"),
+                "global_batch": args.batch,
+                "batch_per_gpu": args.batch if heads else res["batch_per_gpu"],
                 "seq_len": args.seqlen,
                 "chunk": 256,
                 "head": "tied head on the last position only",
                 "parallelism": (f"SSD-head-group-sharded x{world} (one NCCL all-reduce per layer)"
-                                if heads else f"batch-sharded x{world} (no data-path collective)"),
+                                if heads else f"batch-sharded x{world} (global batch split, no "
+                                "data-path collective)"),
                 "l2": f"working set > 126 MB L2 (activations + {_weight_gb(args.model):.2f} GB bf16 weights per "
                       "step); no flush",
+                "tuning": dict(kv.split("=") for kv in args.tune) or "library defaults",
             },
             "tflops_per_gpu": res["step_tflops_per_gpu"],
             "mfu": res["step_mfu"],
             "e2e": {"value": res["e2e_value"], "unit": "tok/s",
-                    "h2d_bytes_per_step": res["h2d"] * (1 if heads else world),
-                    "d2h_bytes_per_step": res["d2h"] * (1 if heads else world)},
+                    "h2d_bytes_per_step": args.batch * args.seqlen * 8,
+                    "d2h_bytes_per_step": res["d2h_global"]},
             "roofline": res["roofline"],
             "phases_ms_per_step": res["phases_ms"],
             "cpu_baseline": cpu,
+            "c2": c2,
             "decode": dec,
             "clocks": res["clocks"],
             "gpu_launches": int(res["launches"]),
+            "world": {"ranks": world, "backend": "nccl" if world > 1 else None,
+                      "nccl_version": _nccl_version() if world > 1 else None},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -844,6 +1008,16 @@ def main():
 
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _nccl_version():
+    try:
+        import torch
+
+        v = torch.cuda.nccl.version()
+        return ".".join(map(str, v)) if isinstance(v, tuple) else str(v)
+    except Exception:  # noqa: BLE001
+        return None
 
 
 if __name__ == "__main__":

@@ -46,12 +46,41 @@ enum ssd200_status {
   SSD200_EWORKSPACE = -4    /* workspace too small */
 };
 
+/* Implementation choices of the bf16 tensor-core path, passed PER CALL through
+ * ssd200_dims_t.tuning (NULL = the measured defaults from
+ * ssd200_tuning_defaults).  There is no library-global option state: two
+ * callers on one thread never see each other's choices.  Every setting
+ * computes the same function; those marked [order] change the order of f32
+ * partial sums (results agree to rounding, not bitwise). */
+typedef struct ssd200_tuning {
+  int size;                /* sizeof(ssd200_tuning_t), checked */
+  int prefill_pdl;         /* programmatic dependent launch between prefill kernels (1) */
+  int gemm_pair;           /* CTA-pair (cta_group::2) 256x256 prefill GEMM tiles (1) */
+  int pair_min_tiles;      /* ... from this many 256x256 tiles (64) */
+  int scan_variant;        /* 0 auto, 1 fused per-(b,h) chunk walk, 2 parallel chunk states + pass */
+  int chunkscan_multicast; /* chunk walk: 4-CTA clusters share each chunk's B tile by TMA multicast (1) */
+  int out_waves;           /* output kernel: head groups until >= out_waves x SMs CTAs (1) */
+  int dec_pdl;             /* PDL between the decode kernels (1) */
+  int dec_swap;            /* decode GEMMs: swapped-operand weight-streaming kernel (1) or tc_gemm (0) */
+  int dec_small_ring;      /* [order] decode GEMMs: ~96 KB ring (1), 192 KB (0), -1 auto (B <= dec_small_max) */
+  int dec_small_max;       /* largest batch on the ~96 KB ring when dec_small_ring is auto (48) */
+  int dec_split_in;        /* [order] decode in_proj split-K factor (0 auto) */
+  int dec_split_out;       /* [order] decode out_proj split-K factor (0 auto) */
+  int stream_stages;       /* decode state stream: ring stages (0 = as many as fit) */
+  int stream_cps;          /* decode state stream: CTAs per SM (0 auto, 1, 2) */
+  int stream_cw;           /* decode state stream: consumer warps (8 or 16) */
+  int out_interleave;      /* SSD output kernel: the two row tiles of a chunk run side by side (1) */
+} ssd200_tuning_t;
+
+void ssd200_tuning_defaults(ssd200_tuning_t *t);
+
 /* Model widths + numerics (model.py:20-70).  a = -exp(A_log) is host-computed
  * (ssd.py:99-112) so the bf16e ablation rounds exactly like the reference. */
 typedef struct ssd200_dims {
   int dtype; /* enum ssd200_dtype: compute mode */
   int d_model, d_inner, n_heads, head_dim, d_state, n_groups, conv_kernel, chunk_size;
   double norm_eps, dt_min, dt_max;
+  const ssd200_tuning_t *tuning; /* NULL = defaults (see ssd200_tuning_t) */
 } ssd200_dims_t;
 
 typedef struct ssd200_layer {
@@ -77,9 +106,11 @@ int ssd200_chunk_scan(int dtype, const void *X, const void *dt, const void *a, c
                       size_t workspace_bytes, ssd200_stream_t stream);
 
 /* ---- embedding gather (model.py:198, decode.py:96) ----------------------
- * tokens int64 (rows) already range-checked by the caller. */
-int ssd200_embed(const ssd200_dims_t *d, const int64_t *tokens, int rows, const void *embedding,
-                 void *hidden, void *hidden_lp, ssd200_stream_t stream);
+ * tokens int64 (rows).  Host callers range-check ids like model.py:191-195;
+ * for ids that live on the device (no host sync) the kernel checks them: an
+ * id outside [0, vocab) yields a NaN row (never an out-of-bounds read). */
+int ssd200_embed(const ssd200_dims_t *d, const int64_t *tokens, int rows, int vocab,
+                 const void *embedding, void *hidden, void *hidden_lp, ssd200_stream_t stream);
 
 /* ---- block_forward (model.py:124-174) over (batch, seqlen) ---------------
  * hidden/hidden_lp updated in place; writes the layer's final SSM state and
@@ -142,24 +173,6 @@ int ssd200_head(const ssd200_dims_t *d, int vocab, const void *hidden, int64_t h
                 int64_t *argmax_out, int rows, void *workspace, size_t workspace_bytes,
                 ssd200_stream_t stream);
 
-/* ---- one whole decode_step in a single persistent kernel (bf16 mode) ----
- * decode.py:77-144 for batch <= 8: embed tokens, every layer (in_proj,
- * conv/SSM update in place, gate, out_proj + norm + residual), final norm,
- * tied head, argmax (ties -> lowest id).  layers_dev is a DEVICE array of
- * n_layers ssd200_layer_t.  ssm (n_layers, B, H, P, N) and conv
- * (n_layers, B, conv_dim, k-1) are updated in place; hidden (B, d_model) f32
- * and hidden_lp are scratch.  barrier_state: two uint32
- * owned by the caller (reset by every call).  Returns
- * SSD200_EUNSUPPORTED for configurations the fused step does not cover
- * (the per-layer entry points handle those). */
-size_t ssd200_decode_step_workspace(const ssd200_dims_t *d, int batch);
-int ssd200_decode_step(const ssd200_dims_t *d, const ssd200_layer_t *layers_dev, int n_layers,
-                       int vocab, const void *embedding, const void *final_norm_w,
-                       const int64_t *tokens, void *hidden, void *hidden_lp, void *ssm,
-                       void *conv, void *logits, int64_t *argmax_out, unsigned *barrier_state,
-                       int batch, void *workspace, size_t workspace_bytes,
-                       ssd200_stream_t stream);
-
 /* ---- raw bf16 tensor-core GEMM (tcgen05 + TMA + TMEM), for tests/bench --
  * C (M,N) f32 = A (M,K) bf16 row-major  x  B^T where B is (N,K) bf16 row-major.
  * K % 8 == 0 (16-byte TMA row pitch); ragged M/N/K tiles are zero-filled. */
@@ -174,38 +187,6 @@ uint64_t ssd200_launch_count(void);
  * (p: 0 in_proj, 1 conv, 2 scan, 3 gated norm, 4 out_proj); events are
  * cudaEvent_t handles owned by the caller.  Pass NULL to disable. */
 int ssd200_set_phase_events(void *const *events, int n_phases);
-/* Debug: device buffer (>= 8192 uint64) that ssd200_decode_step fills with
- * %globaltimer stamps of CTA 0's phases; NULL disables. */
-int ssd200_debug_trace(void *device_buffer);
-/* Implementation choices (thread-local): option 1 = conv1d+SiLU fused into
- * the in_proj GEMM epilogue (1) instead of the separate conv kernel (0, default);
- * option 2 = force the fused chunk-state + inter-chunk pass scan kernel
- * (default: when batch * heads fills the GPU); option 3 = share each chunk's
- * B tile across 4-CTA clusters by TMA multicast in that kernel (1, default)
- * or load it per CTA (0); option 4 = output-kernel CTA target in multiples of
- * the SM count (head-group split, default 1); option 5 = programmatic
- * dependent launch between the prefill kernels (1 default, 0 off); option 20 =
- * CTA-pair (cta_group::2) prefill GEMMs (1 default, 0 off).
- * Decode (bf16): options 6 / 7 = in_proj / out_proj split-K factor (0 auto);
- * 8 = PDL between the decode kernels (1 default); 9 = fused step's L2
- * prefetch lookahead in ring stages (0 default); 11 / 12 / 13 = state-stream
- * ring stages (0 = as many as fit) / CTAs per SM (0 auto, 1, 2) / consumer
- * warps (8 default, 16); 14 = smallest batch on the per-layer wide path (1
- * default; 9 = fused persistent step for B <= 8); 15 = swapped-operand decode
- * GEMMs (1 default) or tc_gemm (0); 16 = profiling only: skip decode kernels
- * (bit mask 1 in_proj, 2 stream, 4 out_proj, 8 finish); 17 = decode-GEMM
- * ~96 KB ring, two CTAs per SM (-1 auto: B <= option 23, 0, 1); 22 = decode L2
- * warm-up (bit 1: the in_proj GEMM bulk-prefetches the layer's W_out into L2
- * while it streams W_in; bit 2: the out_proj GEMM prefetches the W_in named
- * by ssd200_decode_prefetch_next; 0 default); 23 = largest batch on the
- * decode GEMMs' ~96 KB ring while option 17 is auto. */
-int ssd200_set_option(int option, int value);
-
-/* Names the next layer's W_in (bytes) for option 22 bit 2; consumed (one
- * shot) by the next ssd200_decode_layer call's out_proj.  A performance hint
- * only: results do not depend on it.  (No reference counterpart: decode.py
- * runs the layers back to back on the CPU.) */
-int ssd200_decode_prefetch_next(const void *W_in_next, size_t bytes);
 
 #ifdef __cplusplus
 }

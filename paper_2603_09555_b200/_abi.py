@@ -7,6 +7,8 @@ missing or a call fails, this module raises.
 
 from __future__ import annotations
 
+import contextlib
+import contextvars
 import ctypes
 import os
 import threading
@@ -28,6 +30,16 @@ c_size_t = ctypes.c_size_t
 c_double = ctypes.c_double
 
 
+class Tuning(ctypes.Structure):
+    """ssd200_tuning_t: implementation choices passed per call (NULL = defaults)."""
+
+    _fields_ = [(n, c_int) for n in (
+        "size", "prefill_pdl", "gemm_pair", "pair_min_tiles", "scan_variant",
+        "chunkscan_multicast", "out_waves", "dec_pdl", "dec_swap", "dec_small_ring",
+        "dec_small_max", "dec_split_in", "dec_split_out", "stream_stages", "stream_cps",
+        "stream_cw", "out_interleave")]
+
+
 class Dims(ctypes.Structure):
     _fields_ = [
         ("dtype", c_int),
@@ -42,6 +54,7 @@ class Dims(ctypes.Structure):
         ("norm_eps", c_double),
         ("dt_min", c_double),
         ("dt_max", c_double),
+        ("tuning", ctypes.POINTER(Tuning)),
     ]
 
 
@@ -62,7 +75,8 @@ SIGNATURES = [
         c_int,
         [c_int] + [c_void_p] * 9 + [c_int] * 7 + [c_void_p, c_size_t, c_void_p],
     ),
-    ("ssd200_embed", c_int, [ctypes.POINTER(Dims), c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("ssd200_tuning_defaults", None, [ctypes.POINTER(Tuning)]),
+    ("ssd200_embed", c_int, [ctypes.POINTER(Dims), c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("ssd200_prefill_layer_workspace", c_size_t, [ctypes.POINTER(Dims), c_int, c_int]),
     (
         "ssd200_prefill_layer",
@@ -98,18 +112,9 @@ SIGNATURES = [
         c_int,
         [ctypes.POINTER(Dims), c_int, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_size_t, c_void_p],
     ),
-    ("ssd200_decode_step_workspace", c_size_t, [ctypes.POINTER(Dims), c_int]),
-    (
-        "ssd200_decode_step",
-        c_int,
-        [ctypes.POINTER(Dims), c_void_p, c_int, c_int] + [c_void_p] * 10 + [c_int, c_void_p, c_size_t, c_void_p],
-    ),
     ("ssd200_gemm_bf16", c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p]),
     ("ssd200_launch_count", ctypes.c_uint64, []),
     ("ssd200_set_phase_events", c_int, [c_void_p, c_int]),
-    ("ssd200_debug_trace", c_int, [c_void_p]),
-    ("ssd200_set_option", c_int, [c_int, c_int]),
-    ("ssd200_decode_prefetch_next", c_int, [c_void_p, ctypes.c_size_t]),
 ]
 
 _lib = None
@@ -167,3 +172,39 @@ def require_cuda(*tensors) -> None:
     for t in tensors:
         if t is not None and not t.is_cuda:
             raise ValueError("ssd200 kernels take CUDA tensors")
+
+
+# ------------------------------------------------------------------ tuning
+# Implementation choices travel with each call inside ssd200_dims_t (the
+# library keeps no option state).  ``tuning(**fields)`` scopes overrides to a
+# with-block (tests and A/B measurements); outside one, calls pass NULL and
+# the library uses its measured defaults.
+_TUNING: contextvars.ContextVar = contextvars.ContextVar("ssd200_tuning", default=None)
+
+
+def default_tuning() -> Tuning:
+    t = Tuning()
+    lib().ssd200_tuning_defaults(ctypes.byref(t))
+    return t
+
+
+@contextlib.contextmanager
+def tuning(**fields):
+    base = _TUNING.get()
+    t = Tuning()
+    src = base if base is not None else default_tuning()
+    ctypes.memmove(ctypes.addressof(t), ctypes.addressof(src), ctypes.sizeof(Tuning))
+    for k, v in fields.items():
+        if k not in dict(Tuning._fields_) or k == "size":
+            raise ValueError(f"unknown tuning field {k!r}")
+        setattr(t, k, int(v))
+    tok = _TUNING.set(t)
+    try:
+        yield t
+    finally:
+        _TUNING.reset(tok)
+
+
+def current_tuning():
+    """The Tuning in scope (or None: library defaults)."""
+    return _TUNING.get()

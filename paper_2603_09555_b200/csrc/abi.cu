@@ -5,7 +5,10 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <atomic>
 #include <mutex>
+#include <set>
+#include <tuple>
 #include <string>
 #include <type_traits>
 
@@ -13,7 +16,6 @@
 #include "common.cuh"
 #include "simt.cuh"
 #include "decode.cuh"
-#include "decode_mega.cuh"
 #include "ssd_tc.cuh"
 #include "tc_gemm.cuh"
 #include "decode_gemm.cuh"
@@ -24,28 +26,43 @@ namespace {
 
 thread_local std::string g_err;
 thread_local uint64_t g_launches = 0;
-thread_local void *const *g_phase_ev = nullptr;
+thread_local void *const *g_phase_ev = nullptr;  // bench instrumentation only
 thread_local int g_nphase = 0;
-thread_local void *g_mega_trace = nullptr;  // debug: device buffer of >= 8192 u64
-thread_local int g_force_fused_conv = 0;  // option 1: 1 = fused-conv in_proj epilogue (else separate)
-thread_local bool g_force_chunkscan = false;   // tests: exercise the fused state+pass scan
-thread_local bool g_chunkscan_mc = true;       // option 3: B-tile multicast in the chunk scan
-thread_local int g_out_waves = 1;              // option 4: target CTAs (x SMs) of the output kernel
-thread_local int g_stream_stages = 0, g_stream_cps = 0, g_stream_cw = 8;  // options 11 / 12 / 13
-thread_local int g_dec_gemm_small = -1;        // option 17: decode GEMM ~96 KB ring (two CTAs per SM); -1 auto
-thread_local int g_dec_small_max = 48;         // option 23: largest batch on the ~96 KB ring when option 17 is auto (measured: small ring B = 32 2.23 -> 2.12 ms, big ring B = 64 3.47 -> 3.37 ms)
-thread_local int g_dec_skip = 0;               // option 16: profiling only — skip decode kernels (bit mask)
-thread_local bool g_dec_swap = true;           // option 15: swapped-operand decode GEMM (else tc_gemm)
-thread_local bool g_gemm_pair = true;          // option 20: CTA-pair (cta_group::2) prefill GEMMs (370M prefill +3.6%, 2.7B +11%)
-thread_local int g_pair_min_tiles = 0;         // option 21: fewest 256x256 tiles for CTA-pair GEMMs (0 = 64)
-thread_local int g_wide_min = 1;               // option 14: smallest batch on the wide-batch decode path (measured: the per-layer path beats the fused step at every B, 1.3B B=1 1.215 -> 1.150 ms)
-thread_local int g_mega_pf = 0;                // option 9: fused decode step L2 prefetch lookahead (stages)
-thread_local int g_dec_l2pf = 0;              // option 22: decode L2 warm-up (bit 1: in_proj warms W_out; bit 2: out_proj warms the next layer's W_in)
-thread_local const void *g_next_w_in = nullptr;  // ssd200_decode_prefetch_next: next layer's W_in
-thread_local size_t g_next_w_in_bytes = 0;
-thread_local bool g_dec_pdl = true;            // option 8: PDL between the decode kernels
-thread_local int g_dec_split_in = 0, g_dec_split_out = 0;  // options 6 / 7: wide-decode split-K (0 auto)
-thread_local bool g_use_pdl = true;            // option 5: programmatic dependent launch between the prefill kernels (370M B=1 T=2K +11%, neutral at B=4 T=8K)
+
+// Implementation choices come with each call (ssd200_dims_t.tuning); TuneScope
+// makes them visible to the launch helpers for the duration of that call only.
+ssd200_tuning_t make_default_tuning() {
+  ssd200_tuning_t t{};
+  t.size = (int)sizeof(ssd200_tuning_t);
+  t.prefill_pdl = 1;         // 370M B=1 T=2K +11%, neutral at B=4 T=8K
+  t.gemm_pair = 1;           // 370M prefill +3.6%, 2.7B +11%
+  t.pair_min_tiles = 64;     // pairs win from 64 tiles (370M B=1 T=4K 559K -> 616K tok/s)
+  t.scan_variant = 0;
+  t.chunkscan_multicast = 1;
+  t.out_waves = 1;
+  t.dec_pdl = 1;
+  t.dec_swap = 1;
+  t.dec_small_ring = -1;
+  t.dec_small_max = 48;      // small ring B = 32 2.23 -> 2.12 ms, big ring B = 64 3.47 -> 3.37 ms
+  t.dec_split_in = 0;
+  t.dec_split_out = 0;
+  t.stream_stages = 0;
+  t.stream_cps = 0;
+  t.stream_cw = 8;
+  t.out_interleave = 1;
+  return t;
+}
+const ssd200_tuning_t kDefaultTuning = make_default_tuning();
+thread_local const ssd200_tuning_t *g_tune = nullptr;
+inline const ssd200_tuning_t &tune() { return g_tune ? *g_tune : kDefaultTuning; }
+struct TuneScope {
+  const ssd200_tuning_t *prev;
+  explicit TuneScope(const ssd200_dims_t *d) : prev(g_tune) {
+    g_tune = (d && d->tuning && d->tuning->size == (int)sizeof(ssd200_tuning_t)) ? d->tuning
+                                                                                  : nullptr;
+  }
+  ~TuneScope() { g_tune = prev; }
+};
 
 enum { PH_IN_PROJ = 0, PH_CONV = 1, PH_SCAN = 2, PH_NORM = 3, PH_OUT_PROJ = 4 };
 
@@ -102,15 +119,36 @@ struct Carve {
   bool ok() const { return used <= cap; }
 };
 
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
+// SM count of the calling thread's current device (cached per device)
 int num_sms() {
-  static int n = 0;
+  static std::atomic<int> cache[64];
+  const int dev = current_device();
+  if (dev < 0 || dev >= 64) return 148;
+  int n = cache[dev].load(std::memory_order_relaxed);
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
   return n;
+}
+
+// opt a kernel into `bytes` of dynamic shared memory on the current device
+// (the attribute is per device; set once per (kernel, device, size), thread-safe)
+template <typename... KArgs>
+void smem_attr(void (*kern)(KArgs...), int bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void *, int, int>> done;
+  const auto key = std::make_tuple(reinterpret_cast<const void *>(kern), current_device(), bytes);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.insert(key).second)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 // --------------------------------------------------------------- TMA maps
@@ -191,13 +229,13 @@ cudaError_t launch_ex(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, s
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t st, Args... args) {
-  return launch_ex(g_dec_pdl, kern, grid, block, smem, st, args...);
+  return launch_ex(tune().dec_pdl, kern, grid, block, smem, st, args...);
 }
 // prefill kernels: PDL per option 5
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pf(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                       cudaStream_t st, Args... args) {
-  return launch_ex(g_use_pdl, kern, grid, block, smem, st, args...);
+  return launch_ex(tune().prefill_pdl, kern, grid, block, smem, st, args...);
 }
 
 template <int BN, int EPI>
@@ -209,16 +247,11 @@ int launch_tc_gemm_bn(const bf16 *A, long lda, const bf16 *B, long ldb, int M, i
   if (rc) return rc;
   rc = make_map_2d(&tb, B, N, K, ldb, BN);
   if (rc) return rc;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(tc_gemm_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Cfg::SMEM);
-    attr_set = true;
-  }
+  smem_attr(tc_gemm_kernel<BN, EPI>, (int)Cfg::SMEM);
   const int ks = (EPI == TC_EPI_F32 && ep.ksplit > 1) ? ep.ksplit : 1;
   const int tiles = ((M + Cfg::BM - 1) / Cfg::BM) * ((N + BN - 1) / BN) * ks;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  cudaError_t e = launch_ex(pdl || g_use_pdl, tc_gemm_kernel<BN, EPI>, dim3(grid), dim3(320),
+  cudaError_t e = launch_ex(pdl || tune().prefill_pdl, tc_gemm_kernel<BN, EPI>, dim3(grid), dim3(320),
                             Cfg::SMEM, st, ta, tb, M, N, K, ep);
   REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "tc_gemm_kernel: %s", cudaGetErrorString(e));
   LAUNCH_CHECK("tc_gemm_kernel");
@@ -235,12 +268,7 @@ int launch_tc_gemm_pair(const bf16 *A, long lda, const bf16 *B, long ldb, int M,
   if (rc) return rc;
   rc = make_map_2d(&tb, B, N, K, ldb, BN / 2);
   if (rc) return rc;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(tc_gemm_kernel<BN, EPI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Cfg::SMEM);
-    attr_set = true;
-  }
+  smem_attr(tc_gemm_kernel<BN, EPI, true>, (int)Cfg::SMEM);
   const int tiles = ((M + 255) / 256) * ((N + BN - 1) / BN);
   const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
   cudaLaunchConfig_t cfg = {};
@@ -254,7 +282,7 @@ int launch_tc_gemm_pair(const bf16 *A, long lda, const bf16 *B, long ldb, int M,
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = (pdl || g_use_pdl) ? 1 : 0;
+  at[1].val.programmaticStreamSerializationAllowed = (pdl || tune().prefill_pdl) ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, EPI, true>, ta, tb, M, N, K, ep);
@@ -267,36 +295,31 @@ int launch_tc_gemm_pair(const bf16 *A, long lda, const bf16 *B, long ldb, int M,
 template <int EPI>
 int tc_gemm(const bf16 *A, long lda, const bf16 *B, long ldb, int M, int N, int K,
             const TcEpilogue &ep, cudaStream_t st, bool pdl = false) {
-  pdl = pdl && g_dec_pdl;
+  pdl = pdl && tune().dec_pdl;
   REQUIRE(M > 0 && N > 0 && K > 0, SSD200_EINVAL, "tc_gemm: empty problem");
   REQUIRE(K % 8 == 0, SSD200_EINVAL, "tc_gemm: K must be a multiple of 8");
   REQUIRE(ep.ksplit <= 1 || (EPI == TC_EPI_F32 && ep.ksplit <= (K + 63) / 64), SSD200_EINVAL,
           "tc_gemm: split-K needs the F32 epilogue and at least one K block per split");
   if (EPI == TC_EPI_F32 && ep.ksplit > 1)  // split-K: always 128-wide tiles (most tiles)
     return launch_tc_gemm_bn<128, EPI>(A, lda, B, ldb, M, N, K, ep, st, pdl);
-  if constexpr (EPI != TC_EPI_INPROJ_CONV) {
+  {
     // CTA pairs when 256 x 256 tiles still cover the SMs several times
     const long tiles_pair = (long)((M + 255) / 256) * ((N + 255) / 256);
     // measured: pairs win from 64 tiles (370M B=1 T=4K 559K -> 616K tok/s, B=2 T=2K
     // 655K -> 685K); at 32 tiles (B=1 T=2K out_proj) the 128-wide single tiles win
-    const long min_pair = g_pair_min_tiles > 0 ? g_pair_min_tiles : 64;
-    if (g_gemm_pair && N > 128 && tiles_pair >= min_pair)
+    const long min_pair = tune().pair_min_tiles > 0 ? tune().pair_min_tiles : 64;
+    if (tune().gemm_pair && N > 128 && tiles_pair >= min_pair)
       return launch_tc_gemm_pair<256, EPI>(A, lda, B, ldb, M, N, K, ep, st, pdl);
   }
   // 128-wide tiles when 256-wide ones would leave SMs idle (few row tiles: decode batches)
   // (prefill at B = 1 / short T: the out_proj's 256-wide tiles covered 64 of 148 SMs)
   const long tiles256 = (long)((M + 127) / 128) * ((N + 255) / 256);
-  if (N <= 128 || (EPI != TC_EPI_INPROJ_CONV && tiles256 < num_sms()))
+  if (N <= 128 || tiles256 < num_sms())
     return launch_tc_gemm_bn<128, EPI>(A, lda, B, ldb, M, N, K, ep, st, pdl);
   return launch_tc_gemm_bn<256, EPI>(A, lda, B, ldb, M, N, K, ep, st, pdl);
 }
 
 // --------------------------------------------------------------- SSD scan
-template <typename T, typename TI> struct ScanKernels {
-  static bool attrs_done;
-};
-template <typename T, typename TI> bool ScanKernels<T, TI>::attrs_done = false;
-
 inline size_t scan_ws_bytes(size_t elt, long B, long T, long H, long P, long N, long L) {
   long Nc = (T + L - 1) / L;
   return align_up(B * Nc * H * P * N * elt) + align_up(B * H * Nc * elt);
@@ -321,13 +344,8 @@ int run_scan(SsdArgs<T, TI> a, void *ws, size_t ws_bytes, cudaStream_t st) {
       sizeof(T);
   REQUIRE(smem1 <= 220 * 1024 && smem3 <= 220 * 1024, SSD200_EUNSUPPORTED,
           "scan shared memory too large");
-  if (!ScanKernels<T, TI>::attrs_done) {
-    cudaFuncSetAttribute(ssd_chunk_state<T, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         220 * 1024);
-    cudaFuncSetAttribute(ssd_chunk_out<T, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         220 * 1024);
-    ScanKernels<T, TI>::attrs_done = true;
-  }
+  smem_attr(ssd_chunk_state<T, TI>, 220 * 1024);
+  smem_attr(ssd_chunk_out<T, TI>, 220 * 1024);
   ssd_chunk_state<T, TI><<<dim3(a.Nc, a.H, a.B), 256, smem1, st>>>(a);
   LAUNCH_CHECK("ssd_chunk_state");
   const int PN = a.P * a.N;
@@ -436,12 +454,13 @@ int make_map_3d(CUtensorMap *m, const void *ptr, long B, long T, long cols, long
 }
 
 // smallest divisor of H giving at least `target` CTAs over `units` work units
-// (and at most max_hg heads per group)
-inline int pick_groups(int H, long units, long target, int max_hg = 1 << 30) {
+// (at most max_hg heads per group, heads per group a multiple of `mult`)
+inline int pick_groups(int H, long units, long target, int max_hg = 1 << 30, int mult = 1) {
+  auto ok = [&](int ng) { return H % ng == 0 && H / ng <= max_hg && (H / ng) % mult == 0; };
   for (int ng = 1; ng <= H; ++ng)
-    if (H % ng == 0 && H / ng <= max_hg && units * ng >= target) return ng;
+    if (ok(ng) && units * ng >= target) return ng;
   for (int ng = 1; ng <= H; ++ng)
-    if (H % ng == 0 && H / ng <= max_hg) return ng;
+    if (ok(ng)) return ng;
   return H;
 }
 
@@ -450,16 +469,9 @@ inline int pick_groups(int H, long units, long target, int max_hg = 1 << 30) {
 int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act, long conv_dim,
                 const bf16 *z, long z_ld, const float *dt, float *final_state, bf16 *u_out,
                 float *ssq, int *ng_out, void *scan_ws, int B, int Tn, cudaStream_t st) {
-  static bool attrs = false;
-  if (!attrs) {
-    cudaFuncSetAttribute(ssd_tc_state, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)StateSmem::TOTAL);
-    cudaFuncSetAttribute(ssd_tc_out, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)OutSmem::TOTAL);
-    cudaFuncSetAttribute(ssd_tc_chunkscan, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)ScanSmem::TOTAL);
-    attrs = true;
-  }
+  smem_attr(ssd_tc_state, (int)StateSmem::TOTAL);
+  smem_attr(ssd_tc_out, (int)OutSmem::TOTAL);
+  smem_attr(ssd_tc_chunkscan, (int)ScanSmem::TOTAL);
   const int H = d->n_heads;
   TcSsdArgs a{};
   a.B = B;
@@ -483,7 +495,6 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
   a.final_state = final_state;
   a.u_out = u_out;
   a.ssq = ssq;
-  a.trace = static_cast<unsigned long long *>(g_mega_trace);
   CUtensorMap tm_act, tm_prev, tm_z, tm_u;
   int rc = make_map_3d(&tm_act, act, B, Tn, conv_dim, conv_dim, 128);
   if (rc) return rc;
@@ -501,13 +512,14 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
   LAUNCH_CHECK("ssd_tc_cumsum");
   // measured (370M, T = 2K..16K): the fused walk beats parallel states + pass from
   // B * H = 32 up (B = 1: 240 K -> 392 K tok/s at T = 2K, 640 K -> 755 K at T = 16K)
-  if ((long)B * H >= sms / 6 || g_force_chunkscan) {
+  const int variant = tune().scan_variant;
+  if (variant == 1 || (variant == 0 && (long)B * H >= sms / 6)) {
     // chunk states + inter-chunk pass fused: one CTA per (b, h), chunks in order
     // clusters of 4 heads of one batch row share each chunk's B tile by multicast
-    const int mc = (H % 4 == 0 && g_chunkscan_mc) ? 4 : 1;
+    const int mc = (H % 4 == 0 && tune().chunkscan_multicast) ? 4 : 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(B * H);
-    cfg.blockDim = dim3(192);
+    cfg.blockDim = dim3(CHUNKSCAN_THREADS);
     cfg.dynamicSmemBytes = ScanSmem::TOTAL;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
@@ -516,7 +528,7 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = g_use_pdl ? 1 : 0;
+    attr[1].val.programmaticStreamSerializationAllowed = tune().prefill_pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     cudaError_t e = cudaLaunchKernelEx(&cfg, ssd_tc_chunkscan, tm_act, a, mc);
@@ -536,13 +548,16 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
     LAUNCH_CHECK("ssd_tc_pass");
   }
   // outputs (+ D skip + gate)
-  a.NG = pick_groups(H, (long)B * a.Nc * 2, g_out_waves * sms, OutSmem::MAX_HG);
+  // head groups of whole 8-head slices: sum u^2 leaves per slice, so the grouping
+  // (which depends on B) does not change any row's result
+  a.interleave = tune().out_interleave;
+  a.NG = pick_groups(H, (long)B * a.Nc * 2, (tune().out_waves > 0 ? tune().out_waves : 1) * sms, OutSmem::MAX_HG, 8);
   a.HG = H / a.NG;
   REQUIRE(launch_pf(ssd_tc_out, dim3(B * a.Nc * 2 * a.NG), dim3(OUT_THREADS), OutSmem::TOTAL, st,
                      tm_act, tm_prev, tm_z, tm_u, a) == cudaSuccess,
           SSD200_ELAUNCH, "ssd_tc_out launch");
   LAUNCH_CHECK("ssd_tc_out");
-  *ng_out = a.NG;
+  *ng_out = (H / 8) * OUT_KW;  // sum u^2 partials per row, (8-head slice, column half)
   return SSD200_OK;
 }
 
@@ -652,13 +667,14 @@ int prefill_layer_simt(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidde
   return SSD200_OK;
 }
 
-// sum of the per-head-group partial sums of u^2 -> column `col` of a strided row
+// sum of the slice partial sums of u^2 ((ng, rows), slice-major) -> column `col`
+// of a strided row
 __global__ void ssq_groups_kernel(const float *__restrict__ ssq, int ng, long rows,
                                   float *__restrict__ dst, long ld, int col) {
   const long r = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   float s = 0.f;
-  for (int g = 0; g < ng; ++g) s += ssq[r * ng + g];
+  for (int g = 0; g < ng; ++g) s += ssq[g * rows + r];
   dst[r * ld + col] = s;
 }
 
@@ -670,7 +686,9 @@ __global__ void resid_norm_finish_kernel(float *__restrict__ hidden, bf16 *__res
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= rows * d_model) return;
   const long r = i / d_model, n = i % d_model;
-  const float sc = rsqrtf(part[r * ld + d_model] * inv_d + eps);
+  // same formula as dec_out_finish / the out_proj epilogue: only the all-reduce
+  // order separates a head-sharded row from an unsharded one
+  const float sc = 1.f / sqrtf(part[r * ld + d_model] * inv_d + eps);
   const float v = hidden[i] + sc * part[r * ld + n];
   hidden[i] = v;
   lp[i] = __float2bfloat16_rn(v);
@@ -706,41 +724,13 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
   ep.dt_bias = static_cast<const float *>(w->dt_bias);
   ep.dt_lo = (float)d->dt_min;
   ep.dt_hi = (float)d->dt_max;
-  // conv fused into the in_proj epilogue only when the K loop (d_model) is
-  // long enough to hide the extra epilogue work; otherwise the standalone
-  // streaming conv kernel is faster (measured: 370M d_model 1024 -> separate).
-  // conv1d + SiLU fused into the in_proj epilogue: measured slower than the
-  // separate TMA-tiled conv kernel at 370M and 2.7B (the epilogue becomes the
-  // GEMM's bottleneck), so it is opt-in
-  const bool fuse_conv = tc_ssd_eligible(d) && k == 4 && g_force_fused_conv == 1;
   phase_mark(PH_IN_PROJ, 0, st);
-  int rc;
-  if (fuse_conv) {
-    // conv1d + SiLU fused into the in_proj epilogue (3-row halo tiles)
-    if (Tn < k - 1) {
-      cudaError_t e = cudaMemsetAsync(conv_out, 0, sizeof(float) * B * wd.conv_dim * (k - 1), st);
-      REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "memset conv tail: %s", cudaGetErrorString(e));
-    }
-    ep.act = act;
-    ep.d_inner = d->d_inner;
-    ep.conv_dim = (int)wd.conv_dim;
-    ep.T = Tn;
-    ep.conv_w = static_cast<const float *>(w->conv_w);
-    ep.conv_b = static_cast<const float *>(w->conv_b);
-    ep.conv_tail = conv_out;
-    rc = tc_gemm<TC_EPI_INPROJ_CONV>(hidden_lp, d->d_model, static_cast<const bf16 *>(w->W_in),
-                                     d->d_model, (int)rows, (int)wd.d_in_proj, d->d_model, ep, st);
-    if (rc) return rc;
-    phase_mark(PH_IN_PROJ, 1, st);
-    phase_mark(PH_CONV, 0, st);
-  } else {
-    rc = tc_gemm<TC_EPI_INPROJ>(hidden_lp, d->d_model, static_cast<const bf16 *>(w->W_in),
-                                d->d_model, (int)rows, (int)wd.d_in_proj, d->d_model, ep, st);
-    if (rc) return rc;
-    phase_mark(PH_IN_PROJ, 1, st);
-    phase_mark(PH_CONV, 0, st);
-  }
-  if (!fuse_conv) {
+  int rc = tc_gemm<TC_EPI_INPROJ>(hidden_lp, d->d_model, static_cast<const bf16 *>(w->W_in),
+                                  d->d_model, (int)rows, (int)wd.d_in_proj, d->d_model, ep, st);
+  if (rc) return rc;
+  phase_mark(PH_IN_PROJ, 1, st);
+  phase_mark(PH_CONV, 0, st);
+  {
     if (k > 1) {
       REQUIRE(launch_pf(conv_tail_kernel<float, bf16>,
                          dim3(blocks_for((long)B * wd.conv_dim * (k - 1))), dim3(256), 0, st,
@@ -803,6 +793,7 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
     er.C_lp = hidden_lp;
     er.ssq = ssq;
     er.ng = ng;
+    er.ssq_ld = rows;
     er.inv_d = 1.f / (float)d->d_inner;
     er.eps = (float)d->norm_eps;
     rc = tc_gemm<TC_EPI_RESID_NORM>(u_gated, d->d_inner, static_cast<const bf16 *>(w->W_out),
@@ -861,7 +852,7 @@ template <typename T> struct DecodeWs {
   float *ssq;        // wide-batch bf16: (B, H) sum u^2
 };
 
-// split-K factors of the wide-batch (B > DEC_MAX_B) bf16 decode GEMMs: enough
+// split-K factors of the bf16 decode GEMMs: enough
 // (row tile x column tile x K range) work units to cover the SMs, >= 4 K blocks
 // of 64 per range.  The weights are read once either way; only the f32
 // partials (a few MB) are extra traffic.
@@ -879,7 +870,7 @@ inline DecSplits dec_splits(const ssd200_dims_t *d, int B) {
   const long mt = B <= 256 ? 1 : (B + 127) / 128;  // dec_gemm_swap: one tile covers the batch
   DecSplits r;
   r.in = pick(mt * ((w.d_in_proj + 127) / 128), d->d_model);
-  const bool small = g_dec_gemm_small < 0 ? B <= g_dec_small_max : g_dec_gemm_small != 0;
+  const bool small = tune().dec_small_ring < 0 ? B <= tune().dec_small_max : tune().dec_small_ring != 0;
   if (small && B <= 256) {  // two CTAs per SM: twice the units
     const int s2 = 2 * ((int)num_sms() / (int)((w.d_in_proj + 127) / 128));
     int cap = (d->d_model + 63) / 64 / 4;
@@ -887,8 +878,9 @@ inline DecSplits dec_splits(const ssd200_dims_t *d, int B) {
     r.in = s2 < 1 ? 1 : (s2 > cap ? cap : s2);
   }
   r.out = pick(mt * ((d->d_model + 127) / 128), d->d_inner);
-  if (g_dec_split_in > 0 && g_dec_split_in <= (d->d_model + 63) / 64) r.in = g_dec_split_in;
-  if (g_dec_split_out > 0 && g_dec_split_out <= (d->d_inner + 63) / 64) r.out = g_dec_split_out;
+  const int si = tune().dec_split_in, so = tune().dec_split_out;
+  if (si > 0 && si <= (d->d_model + 63) / 64) r.in = si;
+  if (so > 0 && so <= (d->d_inner + 63) / 64) r.out = so;
   return r;
 }
 
@@ -906,7 +898,7 @@ bool carve_decode(const ssd200_dims_t *d, int B, void *ws, size_t cap, DecodeWs<
   Widths w = widths(d);
   Carve cv(ws, cap);
   const bool big = std::is_same<T, float>::value && d->dtype == SSD200_BF16 &&
-                   (B >= g_wide_min || force_big) && dec_big_eligible(d);
+                   dec_big_eligible(d);
   const DecSplits sp = big ? dec_splits(d, B) : DecSplits{1, 1};
   o.u = cv.take<T>((size_t)sp.in * B * w.d_in_proj);
   o.part = big ? cv.take<float>((size_t)sp.out * B * d->d_model) : nullptr;
@@ -924,129 +916,19 @@ constexpr int GEMV_MAX_ROWS = 16;
 // at B = 16: SIMT gemv_nk 315 us vs tc_gemm ~80 us for the 1.3B in_proj)
 constexpr int GEMV_BF16_MAX_ROWS = 8;
 
-inline bool dec_fast_eligible(const ssd200_dims_t *d, int B) {
-  return d->dtype == SSD200_BF16 && B >= 1 && B <= DEC_MAX_B && d->d_model % 256 == 0 &&
-         d->d_inner % 256 == 0 && d->d_state <= 256 && d->d_state % 4 == 0 &&
-         d->head_dim % 4 == 0 && d->conv_kernel >= 1 && d->conv_kernel <= 16;
-}
-
-
-// streaming GEMV launch: ring depth from a ~108 KB budget (two CTAs of
-// consecutive kernels can co-reside under PDL), grid = one CTA per SM
-template <int EPI>
-int launch_dec_stream(const DecArgs &a, cudaStream_t st, int *grid_out = nullptr) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dec_gemv_stream<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         220 * 1024);
-    attr = true;
-  }
-  DecStream cfg;
-  cfg.stage_bytes = (uint32_t)DS_ROWS * a.K * 2;
-  const size_t xb = (size_t)a.B * a.K * 2;
-  long stages = ((long)108 * 1024 - (long)xb) / (long)cfg.stage_bytes;
-  if (stages < 2) stages = 2;
-  if (stages > 8) stages = 8;
-  cfg.stages = (int)stages;
-  const size_t smem = (size_t)cfg.stages * cfg.stage_bytes + xb;
-  REQUIRE(smem <= 220 * 1024, SSD200_EUNSUPPORTED, "decode GEMV: K=%d, B=%d too large", a.K,
-          a.B);
-  const int groups = (a.N + DS_ROWS - 1) / DS_ROWS;
-  const int grid = groups < num_sms() ? groups : num_sms();
-  if (grid_out) *grid_out = grid;
-  cudaError_t e = launch_pdl(dec_gemv_stream<EPI>, dim3(grid), dim3(DS_THREADS), smem, st, a, cfg);
-  REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_gemv_stream: %s", cudaGetErrorString(e));
-  LAUNCH_CHECK("dec_gemv_stream");
-  return SSD200_OK;
-}
-
-// bf16 small-batch decode layer: 3 HBM-streaming kernels (decode.cuh)
-int decode_layer_fast(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hidden,
-                      bf16 *hidden_lp, const float *ssm_in, float *ssm_out, const float *conv_in,
-                      float *conv_out, int B, DecodeWs<float> &o, cudaStream_t st) {
-  Widths wd = widths(d);
-  constexpr int PS = 4;
-  float *z = o.u;
-  float *act = z + (size_t)B * d->d_inner;
-  float *dtv = act + (size_t)B * wd.conv_dim;
-  bf16 *ug = o.normed_lp;
-  float *ssq = o.y;
-  DecArgs a{};
-  a.B = B;
-  a.N = (int)wd.d_in_proj;
-  a.K = d->d_model;
-  a.W = static_cast<const bf16 *>(w->W_in);
-  a.X = hidden_lp;
-  a.d_inner = d->d_inner;
-  a.conv_dim = (int)wd.conv_dim;
-  a.H = d->n_heads;
-  a.k = d->conv_kernel;
-  a.z = z;
-  a.act = act;
-  a.dt = dtv;
-  a.conv_in = conv_in;
-  a.conv_out = conv_out;
-  a.conv_w = static_cast<const float *>(w->conv_w);
-  a.conv_b = static_cast<const float *>(w->conv_b);
-  a.dt_bias = static_cast<const float *>(w->dt_bias);
-  a.dt_lo = (float)d->dt_min;
-  a.dt_hi = (float)d->dt_max;
-  int rc = launch_dec_stream<DEC_EPI_IN>(a, st);
-  if (rc) return rc;
-  DecSsmArgs s{};
-  s.H = d->n_heads;
-  s.P = d->head_dim;
-  s.G = d->n_groups;
-  s.N = d->d_state;
-  s.d_inner = d->d_inner;
-  s.conv_dim = (int)wd.conv_dim;
-  s.PS = PS;
-  s.act = act;
-  s.z = z;
-  s.dt = dtv;
-  s.a = static_cast<const float *>(w->a);
-  s.D = static_cast<const float *>(w->D);
-  s.ssm_in = ssm_in;
-  s.ssm_out = ssm_out;
-  s.u = ug;
-  s.ssq = ssq;
-  cudaError_t e = launch_pdl(dec_ssm, dim3(d->n_heads * PS, B), dim3(128), 0, st, s);
-  REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_ssm: %s", cudaGetErrorString(e));
-  LAUNCH_CHECK("dec_ssm");
-  DecArgs o2{};
-  o2.B = B;
-  o2.N = d->d_model;
-  o2.K = d->d_inner;
-  o2.W = static_cast<const bf16 *>(w->W_out);
-  o2.X = ug;
-  o2.ssq = ssq;
-  o2.nssq = d->n_heads * PS;
-  o2.inv_d = 1.f / (float)d->d_inner;
-  o2.eps = (float)d->norm_eps;
-  o2.hidden = hidden;
-  o2.hidden_lp = hidden_lp;
-  return launch_dec_stream<DEC_EPI_OUT>(o2, st);
-}
-
 // part[s, b, n] = sum_{k in range s} W[n, k] X[b, k] for decode batches: the
 // weight-streaming swapped-operand GEMM (decode_gemm.cuh) for B <= 256, else tc_gemm
 template <int BNB, bool SMALL>
 int launch_dec_gemm_cfg(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long ldo,
-                        int ksplit, long split_stride, cudaStream_t st, const void *pf,
-                        long pf_bytes) {
+                        int ksplit, long split_stride, cudaStream_t st) {
   using Cfg = DgCfg<BNB, SMALL>;
   CUtensorMap tw, tx;
   int rc = make_map_2d(&tw, W, N, K, K, 128);
   if (rc) return rc;
   rc = make_map_2d(&tx, X, B, K, K, BNB);
   if (rc) return rc;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dec_gemm_swap<BNB, SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Cfg::SMEM);
-    attr = true;
-  }
-  DgArgs a{N, K, B, ksplit, out, ldo, split_stride, static_cast<const uint8_t *>(pf), pf_bytes};
+  smem_attr(dec_gemm_swap<BNB, SMALL>, (int)Cfg::SMEM);
+  DgArgs a{N, K, B, ksplit, out, ldo, split_stride};
   const int grid = ((N + 127) / 128) * ksplit;
   cudaError_t e =
       launch_pdl(dec_gemm_swap<BNB, SMALL>, dim3(grid), dim3(192), Cfg::SMEM, st, tw, tx, a);
@@ -1056,27 +938,25 @@ int launch_dec_gemm_cfg(const bf16 *W, int N, int K, const bf16 *X, int B, float
 }
 template <int BNB>
 int launch_dec_gemm_bnb(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long ldo,
-                        int ksplit, long split_stride, cudaStream_t st, const void *pf,
-                        long pf_bytes) {
+                        int ksplit, long split_stride, cudaStream_t st) {
   // the small ring (two CTAs per SM) measured faster up to B = 32 (B = 1: 1.18 -> 1.06 ms
   // with the in_proj split 4), slower from B = 64 (3.37 vs 3.47 ms) and at B = 256
-  const bool small = g_dec_gemm_small < 0 ? B <= g_dec_small_max : g_dec_gemm_small != 0;
+  const bool small = tune().dec_small_ring < 0 ? B <= tune().dec_small_max : tune().dec_small_ring != 0;
   return small
-             ? launch_dec_gemm_cfg<BNB, true>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, pf, pf_bytes)
-             : launch_dec_gemm_cfg<BNB, false>(W, N, K, X, B, out, ldo, ksplit, split_stride, st,
-                                               pf, pf_bytes);
+             ? launch_dec_gemm_cfg<BNB, true>(W, N, K, X, B, out, ldo, ksplit, split_stride, st)
+             : launch_dec_gemm_cfg<BNB, false>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
 }
 
 int dec_gemm(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long ldo, int ksplit,
-             long split_stride, cudaStream_t st, const void *pf = nullptr, long pf_bytes = 0) {
+             long split_stride, cudaStream_t st) {
   REQUIRE(ksplit >= 1 && ksplit <= (K + 63) / 64, SSD200_EINVAL, "dec_gemm: bad split");
-  if (B <= 256 && g_dec_swap) {
-    if (B <= 16) return launch_dec_gemm_bnb<16>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, pf, pf_bytes);
-    if (B <= 32) return launch_dec_gemm_bnb<32>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, pf, pf_bytes);
-    if (B <= 64) return launch_dec_gemm_bnb<64>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, pf, pf_bytes);
+  if (B <= 256 && tune().dec_swap) {
+    if (B <= 16) return launch_dec_gemm_bnb<16>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
+    if (B <= 32) return launch_dec_gemm_bnb<32>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
+    if (B <= 64) return launch_dec_gemm_bnb<64>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
     if (B <= 128)
-      return launch_dec_gemm_bnb<128>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, pf, pf_bytes);
-    return launch_dec_gemm_bnb<256>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, pf, pf_bytes);
+      return launch_dec_gemm_bnb<128>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
+    return launch_dec_gemm_bnb<256>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
   }
   TcEpilogue ep{};
   ep.C = out;
@@ -1086,7 +966,7 @@ int dec_gemm(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long
   return tc_gemm<TC_EPI_F32>(X, K, W, K, B, N, K, ep, st, true);
 }
 
-// wide-batch bf16 decode layer (B > DEC_MAX_B), 4 PDL-chained launches:
+// bf16 decode layer, 4 PDL-chained launches:
 //   tc_gemm F32 split-K in_proj -> dec_ssm_stream (TMA-pipelined conv + state
 //   update + gate + sum u^2) -> tc_gemm F32 split-K out_proj -> dec_out_finish
 //   (norm row scale + residual, B / C conv windows rolled).
@@ -1102,11 +982,9 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   Widths wd = widths(d);
   const DecSplits sp = dec_splits(d, B);
   const long s_in = (long)B * wd.d_in_proj, s_out = (long)B * d->d_model;
-  if (!(g_dec_skip & 1)) {
-    const bool pf_out = (g_dec_l2pf & 1) && w->W_out;
+  {
     int rc = dec_gemm(static_cast<const bf16 *>(w->W_in), (int)wd.d_in_proj, d->d_model, hidden_lp,
-                      B, o.u, wd.d_in_proj, sp.in, s_in, st, pf_out ? w->W_out : nullptr,
-                      pf_out ? (long)d->d_model * d->d_inner * 2 : 0);
+                      B, o.u, wd.d_in_proj, sp.in, s_in, st);
     if (rc) return rc;
   }
   DecStreamArgs sa{};
@@ -1140,11 +1018,11 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   // small-ring decode GEMMs: B = 8 1.42 -> 1.29, B = 64 3.97 -> 3.51, B = 256
   // 12.1 -> 10.9 ms/step; neutral at B = 1, where there are fewer tiles than SMs)
   const int ntiles_all = B * d->n_heads;
-  const int cps = g_stream_cps == 1 ? 1
-                  : g_stream_cps == 2 ? 2
+  const int cps = tune().stream_cps == 1 ? 1
+                  : tune().stream_cps == 2 ? 2
                   : (ntiles_all >= 2 * num_sms() ? 2 : 1);
   int stages = (int)((cps == 2 ? 105u * 1024u : 214u * 1024u) / lay.total);
-  if (g_stream_stages > 0 && g_stream_stages < stages) stages = g_stream_stages;
+  if (tune().stream_stages > 0 && tune().stream_stages < stages) stages = tune().stream_stages;
   sa.stages = stages > DSS_MAX_STAGES ? DSS_MAX_STAGES : stages;
   REQUIRE(sa.stages >= 2, SSD200_EUNSUPPORTED, "decode state tile too large for the smem ring");
   const size_t smem = (size_t)sa.stages * lay.total;
@@ -1153,36 +1031,24 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   const int grid = ntiles < cps * num_sms() ? ntiles : cps * num_sms();
   REQUIRE((ntiles + grid - 1) / grid <= DSS_MAX_TILES, SSD200_EUNSUPPORTED,
           "decode: %d state tiles per CTA exceed %d", (ntiles + grid - 1) / grid, DSS_MAX_TILES);
-  const int cw = g_stream_cw == 16 ? 16 : 8;  // consumer warps
+  const int cw = tune().stream_cw == 16 ? 16 : 8;  // consumer warps
   const int nq = d->d_state <= 128 ? 1 : 2, rpw = d->head_dim / cw;
   e = cudaErrorInvalidValue;
 #define DSS_CASE(NQ, RPW, CW)                                                                  \
   if (nq == NQ && rpw == RPW && cw == CW) {                                                    \
-    static bool attr = false;                                                                  \
-    if (!attr) {                                                                               \
-      cudaFuncSetAttribute(dec_ssm_stream<NQ, RPW, CW>,                                        \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, 214 * 1024);           \
-      attr = true;                                                                             \
-    }                                                                                          \
+    smem_attr(dec_ssm_stream<NQ, RPW, CW>, 214 * 1024);                                        \
     e = launch_pdl(dec_ssm_stream<NQ, RPW, CW>, dim3(grid), dim3(CW * 32 + 32), smem, st, sa); \
   }
-  if (g_dec_skip & 2) {
-    e = cudaSuccess;
-  } else {
     DSS_CASE(1, 1, 8) DSS_CASE(1, 2, 8) DSS_CASE(1, 4, 8) DSS_CASE(1, 8, 8)
     DSS_CASE(2, 1, 8) DSS_CASE(2, 2, 8) DSS_CASE(2, 4, 8) DSS_CASE(2, 8, 8)
     DSS_CASE(1, 1, 16) DSS_CASE(1, 2, 16) DSS_CASE(1, 4, 16)
     DSS_CASE(2, 1, 16) DSS_CASE(2, 2, 16) DSS_CASE(2, 4, 16)
-  }
 #undef DSS_CASE
   REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_ssm_stream: %s", cudaGetErrorString(e));
   LAUNCH_CHECK("dec_ssm_stream");
 
-  const bool pf_next = (g_dec_l2pf & 2) && g_next_w_in;
-  int rc = (g_dec_skip & 4) ? 0 : dec_gemm(static_cast<const bf16 *>(w->W_out), d->d_model, d->d_inner, o.normed_lp, B,
-                    o.part, d->d_model, sp.out, s_out, st, pf_next ? g_next_w_in : nullptr,
-                    pf_next ? (long)g_next_w_in_bytes : 0);
-  g_next_w_in = nullptr;  // one-shot: the hint names the layer after this one
+  int rc = dec_gemm(static_cast<const bf16 *>(w->W_out), d->d_model, d->d_inner, o.normed_lp, B,
+                    o.part, d->d_model, sp.out, s_out, st);
   if (rc) return rc;
   DecFinishArgs fa{};
   fa.part = o.part;
@@ -1206,7 +1072,7 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   fa.pout = pout;
   fa.pld = pld;
   const int gbx = (d->d_model + 255) / 256 + (int)((wd.conv_dim - d->d_inner + 255) / 256);
-  e = (g_dec_skip & 8) ? cudaSuccess : launch_pdl(dec_out_finish, dim3(gbx, B), dim3(256), 0, st, fa);
+  e = launch_pdl(dec_out_finish, dim3(gbx, B), dim3(256), 0, st, fa);
   REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_out_finish: %s", cudaGetErrorString(e));
   LAUNCH_CHECK("dec_out_finish");
   return SSD200_OK;
@@ -1224,22 +1090,10 @@ int decode_layer_impl(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidden
   const bool lp = d->dtype == SSD200_BF16;
   const int k = d->conv_kernel;
   if constexpr (std::is_same<T, float>::value) {
-    if (lp && B >= g_wide_min && dec_big_eligible(d)) {
+    if (lp && dec_big_eligible(d)) {
       REQUIRE(hidden_lp, SSD200_EINVAL, "bf16 mode needs the hidden_lp shadow");
       return decode_layer_big(d, w, hidden, hidden_lp, ssm_in, ssm_out, conv_in, conv_out, B, o,
                               st);
-    }
-    if (dec_fast_eligible(d, B) && hidden_lp) {
-      static bool attrs = false;
-      if (!attrs) {
-        cudaFuncSetAttribute(dec_gemv<DEC_EPI_IN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
-        cudaFuncSetAttribute(dec_gemv<DEC_EPI_OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
-        attrs = true;
-      }
-      return decode_layer_fast(d, w, hidden, hidden_lp, ssm_in, ssm_out, conv_in, conv_out, B, o,
-                               st);
     }
   }
   // in_proj
@@ -1361,35 +1215,6 @@ int head_bf16(const ssd200_dims_t *d, int V, const float *hidden, long hrs, cons
               const bf16 *E, float *logits, int64_t *amax, int rows, void *ws, size_t ws_bytes,
               cudaStream_t st) {
   Carve cv(ws, ws_bytes);
-  if (rows <= DEC_MAX_B && d->d_model % 256 == 0 && !(g_dec_swap && d->d_model % 8 == 0)) {
-    // fused final RMSNorm + tied-head GEMV + per-CTA argmax partials (decode.cuh)
-    const int grid = num_sms();  // upper bound of launch_dec_stream's grid
-    float *pv = cv.take<float>((size_t)grid * rows);
-    int *pi = cv.take<int>((size_t)grid * rows);
-    REQUIRE(cv.ok(), SSD200_EWORKSPACE, "head workspace %zu < %zu", ws_bytes, cv.used);
-    DecArgs a{};
-    a.B = rows;
-    a.N = V;
-    a.K = d->d_model;
-    a.W = E;
-    a.hidden = const_cast<float *>(hidden);
-    a.hstride = hrs;
-    a.final_w = fw;
-    a.eps = (float)d->norm_eps;
-    a.logits = logits;
-    a.amax_val = pv;
-    a.amax_idx = pi;
-    int used_grid = grid;
-    int rc = launch_dec_stream<DEC_EPI_HEAD>(a, st, &used_grid);
-    if (rc) return rc;
-    if (amax) {
-      cudaError_t e = launch_pdl(dec_argmax, dim3(1), dim3(32 * rows), 0, st, (const float *)pv,
-                                 (const int *)pi, used_grid, rows, amax);
-      REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_argmax: %s", cudaGetErrorString(e));
-      LAUNCH_CHECK("dec_argmax");
-    }
-    return SSD200_OK;
-  }
   bf16 *normed = cv.take<bf16>((size_t)rows * d->d_model);
   float *lg = logits ? logits : cv.take<float>((size_t)rows * V);
   constexpr int AM_CHUNK = 2048;
@@ -1400,7 +1225,7 @@ int head_bf16(const ssd200_dims_t *d, int V, const float *hidden, long hrs, cons
   rmsnorm_rows<float, bf16><<<rows, 256, 0, st>>>(hidden, hrs, fw, normed, d->d_model,
                                                   d->d_model, (float)d->norm_eps);
   LAUNCH_CHECK("rmsnorm_rows");
-  if (rows <= 256 && g_dec_swap && d->d_model % 8 == 0) {
+  if (rows <= 256 && tune().dec_swap && d->d_model % 8 == 0) {
     // decode batches: the embedding streamed once as the UMMA M side (decode_gemm.cuh)
     int rc = dec_gemm(E, V, d->d_model, normed, rows, lg, V, 1, 0, st);
     if (rc) return rc;
@@ -1434,7 +1259,11 @@ int head_bf16(const ssd200_dims_t *d, int V, const float *hidden, long hrs, cons
 // =============================================================== C ABI
 extern "C" {
 
-int ssd200_abi_version(void) { return 1; }
+int ssd200_abi_version(void) { return 2; }
+
+void ssd200_tuning_defaults(ssd200_tuning_t *t) {
+  if (t) *t = kDefaultTuning;
+}
 
 const char *ssd200_last_error(void) { return g_err.c_str(); }
 
@@ -1487,28 +1316,30 @@ int ssd200_chunk_scan(int dtype, const void *X, const void *dt, const void *a, c
   return SSD200_EINVAL;
 }
 
-int ssd200_embed(const ssd200_dims_t *d, const int64_t *tokens, int rows, const void *embedding,
-                 void *hidden, void *hidden_lp, ssd200_stream_t stream) {
+int ssd200_embed(const ssd200_dims_t *d, const int64_t *tokens, int rows, int vocab,
+                 const void *embedding, void *hidden, void *hidden_lp, ssd200_stream_t stream) {
   int rc = check_dims(d);
   if (rc) return rc;
-  REQUIRE(tokens && embedding && hidden && rows >= 1, SSD200_EINVAL, "embed: bad arguments");
+  REQUIRE(tokens && embedding && hidden && rows >= 1 && vocab >= 1, SSD200_EINVAL,
+          "embed: bad arguments");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (d->dtype == SSD200_F32)
     embed_kernel<float, float><<<rows, 256, 0, st>>>(tokens, (const float *)embedding, d->d_model,
-                                                     (float *)hidden, nullptr);
+                                                     vocab, (float *)hidden, nullptr);
   else if (d->dtype == SSD200_F64)
     embed_kernel<double, double><<<rows, 256, 0, st>>>(tokens, (const double *)embedding,
-                                                       d->d_model, (double *)hidden, nullptr);
+                                                       d->d_model, vocab, (double *)hidden, nullptr);
   else {
     REQUIRE(hidden_lp, SSD200_EINVAL, "bf16 mode needs hidden_lp");
     embed_kernel<float, bf16><<<rows, 256, 0, st>>>(tokens, (const bf16 *)embedding, d->d_model,
-                                                    (float *)hidden, (bf16 *)hidden_lp);
+                                                    vocab, (float *)hidden, (bf16 *)hidden_lp);
   }
   LAUNCH_CHECK("embed_kernel");
   return SSD200_OK;
 }
 
 size_t ssd200_prefill_layer_workspace(const ssd200_dims_t *d, int batch, int seqlen) {
+  TuneScope scope(d);
   if (check_dims(d) || batch < 1 || seqlen < 1) return 0;
   size_t need = 0;
   if (d->dtype == SSD200_F64) {
@@ -1524,6 +1355,7 @@ size_t ssd200_prefill_layer_workspace(const ssd200_dims_t *d, int batch, int seq
 int ssd200_prefill_layer(const ssd200_dims_t *d, const ssd200_layer_t *w, void *hidden,
                          void *hidden_lp, void *ssm_out, void *conv_out, int batch, int seqlen,
                          void *workspace, size_t workspace_bytes, ssd200_stream_t stream) {
+  TuneScope scope(d);
   int rc = check_dims(d);
   if (rc) return rc;
   REQUIRE(w && hidden && ssm_out && batch >= 1 && seqlen >= 1, SSD200_EINVAL,
@@ -1548,6 +1380,7 @@ int ssd200_prefill_layer_partial(const ssd200_dims_t *d, const ssd200_layer_t *w
                                  const void *hidden_lp, float *partial, long partial_ld,
                                  void *ssm_out, void *conv_out, int batch, int seqlen,
                                  void *workspace, size_t workspace_bytes, ssd200_stream_t stream) {
+  TuneScope scope(d);
   int rc = check_dims(d);
   if (rc) return rc;
   REQUIRE(d->dtype == SSD200_BF16, SSD200_EUNSUPPORTED, "prefill_layer_partial: bf16 mode only");
@@ -1575,6 +1408,7 @@ int ssd200_resid_norm_finish(int d_model, int d_inner_full, double eps, void *hi
 }
 
 size_t ssd200_decode_layer_workspace(const ssd200_dims_t *d, int batch) {
+  TuneScope scope(d);
   if (check_dims(d) || batch < 1) return 0;
   size_t need = 0;
   if (d->dtype == SSD200_F64) {
@@ -1592,6 +1426,7 @@ int ssd200_decode_layer_partial(const ssd200_dims_t *d, const ssd200_layer_t *w,
                                 const void *ssm_in, void *ssm_out, const void *conv_in,
                                 void *conv_out, int batch, void *workspace,
                                 size_t workspace_bytes, ssd200_stream_t stream) {
+  TuneScope scope(d);
   int rc = check_dims(d);
   if (rc) return rc;
   REQUIRE(d->dtype == SSD200_BF16 && dec_big_eligible(d), SSD200_EUNSUPPORTED,
@@ -1616,6 +1451,7 @@ int ssd200_decode_layer(const ssd200_dims_t *d, const ssd200_layer_t *w, void *h
                         void *hidden_lp, const void *ssm_in, void *ssm_out, const void *conv_in,
                         void *conv_out, int batch, void *workspace, size_t workspace_bytes,
                         ssd200_stream_t stream) {
+  TuneScope scope(d);
   int rc = check_dims(d);
   if (rc) return rc;
   REQUIRE(w && hidden && ssm_in && ssm_out && batch >= 1, SSD200_EINVAL,
@@ -1634,6 +1470,7 @@ int ssd200_decode_layer(const ssd200_dims_t *d, const ssd200_layer_t *w, void *h
 }
 
 size_t ssd200_head_workspace(const ssd200_dims_t *d, int vocab, int rows) {
+  TuneScope scope(d);
   if (check_dims(d) || rows < 1 || vocab < 1) return 0;
   size_t elt = d->dtype == SSD200_F64 ? 8 : 4;
   size_t nel = d->dtype == SSD200_BF16 ? 2 : elt;
@@ -1647,6 +1484,7 @@ int ssd200_head(const ssd200_dims_t *d, int vocab, const void *hidden, int64_t h
                 const void *final_norm_w, const void *embedding, void *logits,
                 int64_t *argmax_out, int rows, void *workspace, size_t workspace_bytes,
                 ssd200_stream_t stream) {
+  TuneScope scope(d);
   int rc = check_dims(d);
   if (rc) return rc;
   REQUIRE(hidden && final_norm_w && embedding && rows >= 1 && vocab >= 1, SSD200_EINVAL,
@@ -1676,227 +1514,7 @@ int ssd200_gemm_bf16(const void *A, const void *B, void *C, int M, int N, int K,
                              static_cast<cudaStream_t>(stream));
 }
 
-// ---------------------------------------------------------------- fused step
-static bool mega_eligible(const ssd200_dims_t *d, int B) {
-  return d->dtype == SSD200_BF16 && B >= 1 && B <= DEC_MAX_B && (B < g_wide_min || !dec_big_eligible(d)) && d->d_model % 256 == 0 &&
-         d->d_inner % 256 == 0 && d->d_state <= 256 && d->d_state % 4 == 0 &&
-         d->head_dim % 4 == 0 && d->conv_kernel >= 1 && d->conv_kernel <= 16 &&
-         (size_t)2 * d->d_inner * 2 <= MEGA_STAGE && (size_t)2 * d->d_model * 2 <= MEGA_STAGE;
-}
-
-static int mega_bt(int B) { return B <= 1 ? 1 : B <= 2 ? 2 : B <= 4 ? 4 : 8; }
-
-static int mega_stages(const ssd200_dims_t *d, int B, size_t *smem) {
-  const size_t xb = (size_t)mega_bt(B) * (d->d_inner > d->d_model ? d->d_inner : d->d_model) * 2;
-  const size_t cap = 216 * 1024;  // + ~8 KB of static smem stays under the 227 KB CTA limit
-  int S = 3;
-  while (S > 2 && (size_t)S * MEGA_STAGE + xb > cap) --S;
-  *smem = (size_t)S * MEGA_STAGE + xb;
-  return *smem <= cap ? S : 0;
-}
-
-static size_t mega_carve(const ssd200_dims_t *d, int B, void *ws, MegaArgs *a) {
-  Widths w = widths(d);
-  Carve cv(ws, SIZE_MAX);
-  float *z = cv.take<float>((size_t)B * d->d_inner);
-  float *act = cv.take<float>((size_t)B * w.conv_dim);
-  float *dt = cv.take<float>((size_t)B * d->n_heads);
-  bf16 *u = cv.take<bf16>((size_t)B * d->d_inner);
-  float *usq = cv.take<float>((size_t)B * d->d_inner);
-  float *pv = cv.take<float>((size_t)1024 * B);
-  int *pi = cv.take<int>((size_t)1024 * B);
-  if (a) {
-    a->z = z;
-    a->act = act;
-    a->dt = dt;
-    a->u = u;
-    a->upart = usq;  // (grid, B) <= (B, d_inner) floats
-    a->amax_val = pv;
-    a->amax_idx = pi;
-  }
-  return cv.used;
-}
-
-size_t ssd200_decode_step_workspace(const ssd200_dims_t *d, int batch) {
-  if (check_dims(d) || batch < 1) return 0;
-  return mega_carve(d, batch, nullptr, nullptr);
-}
-
-int ssd200_decode_step(const ssd200_dims_t *d, const ssd200_layer_t *layers_dev, int n_layers,
-                       int vocab, const void *embedding, const void *final_norm_w,
-                       const int64_t *tokens, void *hidden, void *hidden_lp, void *ssm,
-                       void *conv, void *logits, int64_t *argmax_out, unsigned *barrier_state,
-                       int batch, void *workspace, size_t workspace_bytes,
-                       ssd200_stream_t stream) {
-  int rc = check_dims(d);
-  if (rc) return rc;
-  REQUIRE(layers_dev && embedding && final_norm_w && tokens && hidden && hidden_lp && ssm &&
-              barrier_state && n_layers >= 1 && vocab >= 1,
-          SSD200_EINVAL, "decode_step: bad arguments");
-  REQUIRE(d->conv_kernel == 1 || conv, SSD200_EINVAL, "decode_step: conv state is null");
-  REQUIRE(mega_eligible(d, batch), SSD200_EUNSUPPORTED,
-          "decode_step: fused step needs bf16, batch <= %d and 256-multiple widths", DEC_MAX_B);
-  size_t smem = 0;
-  const int S = mega_stages(d, batch, &smem);
-  REQUIRE(S >= 2, SSD200_EUNSUPPORTED, "decode_step: batch %d too large for the smem ring", batch);
-  const size_t need = mega_carve(d, batch, nullptr, nullptr);
-  REQUIRE(workspace_bytes >= need, SSD200_EWORKSPACE, "decode_step workspace %zu < %zu",
-          workspace_bytes, need);
-  REQUIRE(num_sms() <= d->d_inner && (d->d_inner + num_sms() - 1) / num_sms() <= MEGA_MAX_NK &&
-              (d->d_inner + num_sms() - 1) / num_sms() / d->head_dim + 2 <= MEGA_MAX_DT,
-          SSD200_EUNSUPPORTED, "decode_step: d_inner / head_dim outside the fused step's split");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  mega_embed<<<batch, 256, 0, st>>>(tokens, (const bf16 *)embedding, d->d_model, (float *)hidden,
-                                    (bf16 *)hidden_lp, barrier_state);
-  LAUNCH_CHECK("mega_embed");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(decode_mega<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
-    cudaFuncSetAttribute(decode_mega<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
-    cudaFuncSetAttribute(decode_mega<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
-    cudaFuncSetAttribute(decode_mega<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024);
-    attr = true;
-  }
-  Widths w = widths(d);
-  MegaArgs a{};
-  mega_carve(d, batch, workspace, &a);
-  a.B = batch;
-  a.L = n_layers;
-  a.V = vocab;
-  a.stages = S;
-  a.pf_ahead = g_mega_pf;
-  a.d_model = d->d_model;
-  a.d_inner = d->d_inner;
-  a.conv_dim = (int)w.conv_dim;
-  a.d_in_proj = (int)w.d_in_proj;
-  a.H = d->n_heads;
-  a.P = d->head_dim;
-  a.G = d->n_groups;
-  a.N = d->d_state;
-  a.k = d->conv_kernel;
-  a.PS = 4;
-  a.eps = (float)d->norm_eps;
-  a.dt_lo = (float)d->dt_min;
-  a.dt_hi = (float)d->dt_max;
-  a.layers = layers_dev;
-  a.E = (const bf16 *)embedding;
-  a.final_w = (const float *)final_norm_w;
-  a.hidden = (float *)hidden;
-  a.hidden_lp = (bf16 *)hidden_lp;
-  a.ssm = (float *)ssm;
-  a.conv = (float *)conv;
-  a.logits = (float *)logits;
-  a.argmax_out = argmax_out;
-  a.bar_count = barrier_state;
-  a.bc_flag = barrier_state + 1;
-  a.trace = static_cast<unsigned long long *>(g_mega_trace);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(num_sms());
-  cfg.blockDim = dim3(MEGA_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attrs[1];
-  attrs[0].id = cudaLaunchAttributeCooperative;
-  attrs[0].val.cooperative = 1;
-  cfg.attrs = attrs;
-  cfg.numAttrs = 1;
-  cudaError_t e;
-  switch (mega_bt(batch)) {
-    case 1: e = cudaLaunchKernelEx(&cfg, decode_mega<1>, a); break;
-    case 2: e = cudaLaunchKernelEx(&cfg, decode_mega<2>, a); break;
-    case 4: e = cudaLaunchKernelEx(&cfg, decode_mega<4>, a); break;
-    default: e = cudaLaunchKernelEx(&cfg, decode_mega<8>, a); break;
-  }
-  REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "decode_mega: %s", cudaGetErrorString(e));
-  LAUNCH_CHECK("decode_mega");
-  return SSD200_OK;
-}
-
 uint64_t ssd200_launch_count(void) { return g_launches; }
-
-int ssd200_debug_trace(void *device_buffer) {
-  g_mega_trace = device_buffer;
-  return SSD200_OK;
-}
-
-int ssd200_set_option(int option, int value) {
-  switch (option) {
-    case 1:  // force the conv1d fused into the in_proj epilogue (else size-based)
-      g_force_fused_conv = value;
-      return SSD200_OK;
-    case 2:  // force the fused chunk-state + pass scan kernel (else size-based)
-      g_force_chunkscan = value != 0;
-      return SSD200_OK;
-    case 3:  // chunk scan: share each chunk's B tile across 4-CTA clusters by TMA multicast
-      g_chunkscan_mc = value != 0;
-      return SSD200_OK;
-    case 5:  // programmatic dependent launch between consecutive kernels (1 on, 0 off)
-      g_use_pdl = value != 0;
-      return SSD200_OK;
-    case 6:  // wide-batch decode: in_proj split-K factor (0 = auto)
-      g_dec_split_in = value;
-      return SSD200_OK;
-    case 7:  // wide-batch decode: out_proj split-K factor (0 = auto)
-      g_dec_split_out = value;
-      return SSD200_OK;
-    case 11:  // wide-batch decode stream: ring stages (0 = as many as fit)
-      g_stream_stages = value;
-      return SSD200_OK;
-    case 13:  // wide-batch decode stream: consumer warps (8 or 16)
-      g_stream_cw = value;
-      return SSD200_OK;
-    case 12:  // wide-batch decode stream: CTAs per SM (1 or 2; 0 = by tile count)
-      g_stream_cps = value;
-      return SSD200_OK;
-    case 17:  // decode GEMMs: ~96 KB smem ring so consecutive kernels share SMs (1), 192 KB (0), auto (-1)
-      g_dec_gemm_small = value < 0 ? -1 : value != 0;
-      return SSD200_OK;
-    case 23:  // largest batch on the decode GEMMs' ~96 KB ring while option 17 is auto
-      g_dec_small_max = value;
-      return SSD200_OK;
-    case 16:  // profiling only: skip wide-decode kernels (1 in_proj, 2 stream, 4 out_proj, 8 finish)
-      g_dec_skip = value;
-      return SSD200_OK;
-    case 15:  // wide-batch decode GEMMs: swapped-operand weight-streaming kernel (1) or tc_gemm (0)
-      g_dec_swap = value != 0;
-      return SSD200_OK;
-    case 20:  // prefill GEMMs: CTA pairs (cluster of 2, cta_group::2, 256 x 256 tiles) (1) or single CTAs (0)
-      g_gemm_pair = value != 0;
-      return SSD200_OK;
-    case 21:  // CTA-pair GEMMs from this many 256 x 256 tiles (0 = 64)
-      g_pair_min_tiles = value;
-      return SSD200_OK;
-    case 14:  // smallest batch that takes the wide-batch decode path (default 1; 9 = fused step for B <= 8)
-      REQUIRE(value >= 1, SSD200_EINVAL, "option 14 out of range");
-      g_wide_min = value;
-      return SSD200_OK;
-    case 22:  // decode L2 warm-up: bit 1 in_proj warms this layer's W_out, bit 2 out_proj warms the
-              // W_in named by ssd200_decode_prefetch_next (0 = off)
-      REQUIRE(value >= 0 && value <= 3, SSD200_EINVAL, "option 22 out of range");
-      g_dec_l2pf = value;
-      return SSD200_OK;
-    case 9:  // fused decode step: L2 prefetch lookahead in ring stages (0 = off)
-      REQUIRE(value >= 0 && value <= 64, SSD200_EINVAL, "option 9 out of range");
-      g_mega_pf = value;
-      return SSD200_OK;
-    case 8:  // programmatic dependent launch between the decode kernels (1 on, 0 off)
-      g_dec_pdl = value != 0;
-      return SSD200_OK;
-    case 4:  // output kernel: split heads into groups until >= value x SMs CTAs exist
-      REQUIRE(value >= 1 && value <= 64, SSD200_EINVAL, "option 4 out of range");
-      g_out_waves = value;
-      return SSD200_OK;
-    default:
-      set_err("unknown option %d", option);
-      return SSD200_EINVAL;
-  }
-}
-
-int ssd200_decode_prefetch_next(const void *W_in_next, size_t bytes) {
-  g_next_w_in = W_in_next;
-  g_next_w_in_bytes = W_in_next ? bytes : 0;
-  return SSD200_OK;
-}
 
 int ssd200_set_phase_events(void *const *events, int n_phases) {
   REQUIRE(n_phases >= 0 && n_phases <= 5, SSD200_EINVAL, "n_phases must be in [0, 5]");

@@ -1,239 +1,19 @@
-// Cached decode step for the bf16 mode (decode.py:77-144), small batch
-// (B <= DEC_MAX_B).  Per layer, three HBM-streaming kernels:
-//
-//   dec_gemv<EPI_IN>   u = h_lp . W_in^T, epilogue per output feature:
-//                        z       -> z (f32)
-//                        xBC     -> conv window roll + taps + SiLU (conv state in place)
-//                                   (decode.py:103-108, roll_and_insert :65-69)
-//                        dt_raw  -> dt = clip(softplus(. + dt_bias))     (decode.py:111-114)
-//   dec_ssm            h <- e^{a dt} h + dt x (x) B ; y = C.h + D x ; u = y silu(z) ;
-//                      partial sum u^2                                    (decode.py:119-133)
-//   dec_gemv<EPI_OUT>  hidden += rsqrt(mean u^2 + eps) * (u . W_out'^T)  (decode.py:133-140;
-//                      norm_w folded into W_out'), bf16 shadow refreshed
-// and for the tied head
-//   dec_gemv<EPI_HEAD> logits = rmsnorm(hidden) . E^T with per-CTA argmax partials
-//   dec_argmax         final greedy pick, ties -> lowest id (decode.py:72-74)
-//
-// The GEMV streams each weight row once with 16-byte non-allocating loads,
-// one warp per row, the activations staged in shared memory.  Every kernel
-// calls griddepcontrol.wait before touching its predecessor's outputs, so
-// the launch can overlap the previous kernel under programmatic dependent
-// launch, and issues its own weight loads before that wait.
+// Cached decode step for the bf16 mode (decode.py:77-144): the per-layer
+// state stream (dec_ssm_stream), the norm + residual finish (dec_out_finish)
+// and the greedy argmax of the head (argmax_part / argmax_final).  The
+// weight-streaming projections are dec_gemm_swap (decode_gemm.cuh).
 #pragma once
 
 #include "common.cuh"
 
 namespace ssd200 {
 
-constexpr int DEC_MAX_B = 8;
-
-
 __device__ __forceinline__ void named_barrier_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-__device__ __forceinline__ uint4 ld_stream(const void *p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
-__device__ __forceinline__ float dot8(const uint4 &w, const uint4 &x) {
-  const __nv_bfloat162 *wp = reinterpret_cast<const __nv_bfloat162 *>(&w);
-  const __nv_bfloat162 *xp = reinterpret_cast<const __nv_bfloat162 *>(&x);
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float2 a = __bfloat1622float2(wp[i]);
-    const float2 b = __bfloat1622float2(xp[i]);
-    s = fmaf(a.x, b.x, s);
-    s = fmaf(a.y, b.y, s);
-  }
-  return s;
-}
-
-enum { DEC_EPI_IN = 0, DEC_EPI_OUT = 1, DEC_EPI_HEAD = 2 };
-
-struct DecArgs {
-  int B, N, K;              // GEMV: rows N of W (features), reduction K
-  const bf16 *W;            // (N, K)
-  const bf16 *X;            // (B, K) activations (bf16); HEAD: null (uses hidden)
-  // EPI_IN
-  int d_inner, conv_dim, H, k;
-  float *z, *act, *dt;      // (B, d_inner), (B, conv_dim), (B, H)
-  const float *conv_in;     // (B, conv_dim, k-1)
-  float *conv_out;
-  const float *conv_w, *conv_b, *dt_bias;
-  float dt_lo, dt_hi;
-  // EPI_OUT
-  const float *ssq;         // (B, nssq) partial sums of u^2
-  int nssq;
-  float inv_d, eps;
-  float *hidden;            // (B, N) f32 residual (OUT) / input of the head (HEAD)
-  bf16 *hidden_lp;          // (B, N)
-  // EPI_HEAD
-  long hstride;             // row stride of hidden (elements)
-  const float *final_w;     // (K)
-  float *logits;            // (B, N) or null
-  float *amax_val;          // (gridDim, B) per-CTA partials
-  int *amax_idx;
-};
-
-// one warp per weight row; rows strided over the grid
-template <int EPI>
-__global__ __launch_bounds__(256) void dec_gemv(DecArgs a) {
-  extern __shared__ __align__(128) uint8_t dsm[];
-  bf16 *xs = reinterpret_cast<bf16 *>(dsm);  // (B, K)
-  __shared__ float s_scale[DEC_MAX_B];
-  __shared__ float s_best[8][DEC_MAX_B];
-  __shared__ int s_bidx[8][DEC_MAX_B];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int B = a.B, K = a.K;
-  const int nwarps_total = gridDim.x * 8;
-  const int first = blockIdx.x * 8 + warp;
-  const int kchunks = K / 256;  // 256 bf16 per warp-wide 16-byte load
-  uint4 w[16];
-  auto load_chunk = [&](int n, int c0) {
-    const bf16 *wr = a.W + (size_t)n * K + lane * 8;
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (c0 + i < kchunks) w[i] = ld_stream(wr + (c0 + i) * 256);
-  };
-  // this warp's first weight row is in flight before waiting on the producer
-  if (first < a.N) load_chunk(first, 0);
-  griddep_wait();
-  griddep_launch();
-  // stage activations
-  if (EPI == DEC_EPI_HEAD) {
-    // final RMSNorm of hidden rows (numerics.py:161-166), bf16 for the GEMV
-    for (int b = warp; b < B; b += 8) {
-      float ss = 0.f;
-      const float *hr = a.hidden + (size_t)b * a.hstride;
-      for (int k = lane; k < K; k += 32) ss += hr[k] * hr[k];
-      ss = warp_sum(ss);
-      if (lane == 0) s_scale[b] = 1.f / sqrtf(ss / (float)K + a.eps);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < B * K; i += blockDim.x) {
-      const int b = i / K, k = i % K;
-      xs[i] = __float2bfloat16_rn(a.hidden[(size_t)b * a.hstride + k] * s_scale[b] * a.final_w[k]);
-    }
-  } else {
-    const uint4 *src = reinterpret_cast<const uint4 *>(a.X);
-    uint4 *dst = reinterpret_cast<uint4 *>(xs);
-    for (int i = threadIdx.x; i < B * K / 8; i += blockDim.x) dst[i] = src[i];
-    if (EPI == DEC_EPI_OUT && threadIdx.x < B) {
-      float s = 0.f;
-      for (int j = 0; j < a.nssq; ++j) s += a.ssq[threadIdx.x * a.nssq + j];
-      s_scale[threadIdx.x] = 1.f / sqrtf(s * a.inv_d + a.eps);
-    }
-  }
-  __syncthreads();
-  float best[DEC_MAX_B];
-  int bidx[DEC_MAX_B];
-#pragma unroll
-  for (int b = 0; b < DEC_MAX_B; ++b) {
-    best[b] = -INFINITY;
-    bidx[b] = 0x7fffffff;
-  }
-  for (int n = first; n < a.N; n += nwarps_total) {
-    float acc[DEC_MAX_B];
-#pragma unroll
-    for (int b = 0; b < DEC_MAX_B; ++b) acc[b] = 0.f;
-    for (int c0 = 0; c0 < kchunks; c0 += 16) {
-      if (n != first || c0 != 0) load_chunk(n, c0);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        if (c0 + i < kchunks) {
-          const int kk = (c0 + i) * 256 + lane * 8;
-#pragma unroll
-          for (int b = 0; b < DEC_MAX_B; ++b)
-            if (b < B) acc[b] += dot8(w[i], *reinterpret_cast<const uint4 *>(xs + b * K + kk));
-        }
-      }
-    }
-#pragma unroll
-    for (int b = 0; b < DEC_MAX_B; ++b)
-      if (b < B) acc[b] = warp_sum(acc[b]);
-    // epilogue: lane b handles batch row b
-    float v = 0.f;
-#pragma unroll
-    for (int b = 0; b < DEC_MAX_B; ++b)
-      if (lane == b) v = acc[b];
-    const int b = lane;
-    if (EPI == DEC_EPI_HEAD) {
-      if (b < B) {
-        if (a.logits) a.logits[(size_t)b * a.N + n] = v;
-        // rows are visited in increasing n: strict > keeps the lowest id on ties
-#pragma unroll
-        for (int bb = 0; bb < DEC_MAX_B; ++bb)
-          if (bb == b && v > best[bb]) {
-            best[bb] = v;
-            bidx[bb] = n;
-          }
-      }
-    } else if (b < B) {
-      if (EPI == DEC_EPI_IN) {
-        if (n < a.d_inner) {
-          a.z[(size_t)b * a.d_inner + n] = v;
-        } else if (n < a.d_inner + a.conv_dim) {
-          const int ch = n - a.d_inner, km = a.k - 1;
-          const float *ci = a.conv_in + ((size_t)b * a.conv_dim + ch) * km;
-          float *co = a.conv_out + ((size_t)b * a.conv_dim + ch) * km;
-          float win[16];
-          for (int j = 0; j < km; ++j) win[j] = ci[j];
-          win[km] = v;
-          float s = 0.f;
-          for (int j = 0; j <= km; ++j) s += win[j] * a.conv_w[(size_t)ch * a.k + j];
-          a.act[(size_t)b * a.conv_dim + ch] = silu(s + a.conv_b[ch]);
-          for (int j = 0; j < km; ++j) co[j] = win[j + 1];
-        } else {
-          const int h = n - a.d_inner - a.conv_dim;
-          a.dt[(size_t)b * a.H + h] = clamp_(softplus(v + a.dt_bias[h]), a.dt_lo, a.dt_hi);
-        }
-      } else {  // DEC_EPI_OUT
-        float *hp = a.hidden + (size_t)b * a.N + n;
-        const float nv = *hp + s_scale[b] * v;
-        *hp = nv;
-        a.hidden_lp[(size_t)b * a.N + n] = __float2bfloat16_rn(nv);
-      }
-    }
-  }
-  if (EPI == DEC_EPI_HEAD) {
-    // lane b of each warp holds the warp's best for row b; reduce over warps
-#pragma unroll
-    for (int bb = 0; bb < DEC_MAX_B; ++bb)
-      if (lane == bb) {
-        s_best[warp][bb] = best[bb];
-        s_bidx[warp][bb] = bidx[bb];
-      }
-    __syncthreads();
-    if (threadIdx.x < B) {
-      const int bb = threadIdx.x;
-      float bv = -INFINITY;
-      int bi = 0x7fffffff;
-      for (int w = 0; w < 8; ++w) {
-        const float ov = s_best[w][bb];
-        const int oi = s_bidx[w][bb];
-        if (ov > bv || (ov == bv && oi < bi)) {
-          bv = ov;
-          bi = oi;
-        }
-      }
-      a.amax_val[blockIdx.x * B + bb] = bv;
-      a.amax_idx[blockIdx.x * B + bb] = bi;
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
-// TMA-streaming GEMV (v2).  One CTA per SM; warp 8 streams this CTA's rows of
-// W in groups of 8 rows (8*K*2 bytes, contiguous) with cp.async.bulk into a
-// STAGES-deep smem ring; warps 0..7 each take one row of a group.  The
-// weight stream starts before griddepcontrol.wait (weights do not depend on
-// the predecessor), so under PDL it overlaps the previous kernel's tail.
+// bulk-copy (cp.async.bulk) + mbarrier helpers of the state stream
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
                                          uint64_t *bar) {
@@ -272,320 +52,8 @@ __device__ __forceinline__ void mbar_wait_s(uint64_t *bar, uint32_t parity) {
   }
 }
 
-constexpr int DS_ROWS = 8;       // rows per stage (one per consumer warp)
-constexpr int DS_THREADS = 288;  // 8 consumer warps + 1 producer warp
-
-struct DecStream {
-  int stages;
-  uint32_t stage_bytes;  // DS_ROWS * K * 2
-};
-
-template <int EPI>
-__global__ __launch_bounds__(DS_THREADS, 1) void dec_gemv_stream(DecArgs a, DecStream cfg) {
-  extern __shared__ __align__(128) uint8_t dsm[];
-  __shared__ __align__(8) uint64_t full[8], empty[8];
-  __shared__ float s_scale[DEC_MAX_B];
-  __shared__ float s_best[8][DEC_MAX_B];
-  __shared__ int s_bidx[8][DEC_MAX_B];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int B = a.B, K = a.K;
-  const int S = cfg.stages;
-  uint8_t *ring = dsm;
-  bf16 *xs = reinterpret_cast<bf16 *>(dsm + (size_t)S * cfg.stage_bytes);
-  // rows of this CTA: contiguous range, whole groups of DS_ROWS
-  const int groups_total = (a.N + DS_ROWS - 1) / DS_ROWS;
-  const int g0 = (int)((long)groups_total * blockIdx.x / gridDim.x);
-  const int g1 = (int)((long)groups_total * (blockIdx.x + 1) / gridDim.x);
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init_s(&full[s], 1);
-      mbar_init_s(&empty[s], 8);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (warp == 8) {
-    // ---------------- producer: stream the weight row groups
-    if (lane == 0) {
-      int s = 0;
-      uint32_t ph = 0;
-      for (int gi = g0; gi < g1; ++gi) {
-        const int r0 = gi * DS_ROWS;
-        const int nr = min(DS_ROWS, a.N - r0);
-        const uint32_t bytes = (uint32_t)nr * K * 2;
-        mbar_wait_s(&empty[s], ph ^ 1);
-        mbar_expect_s(&full[s], bytes);
-        for (int r = 0; r < nr; ++r)  // one bulk copy per row: more requests in flight
-          bulk_g2s(ring + (size_t)s * cfg.stage_bytes + (size_t)r * K * 2,
-                   a.W + (size_t)(r0 + r) * K, (uint32_t)K * 2, &full[s]);
-        if (++s == S) {
-          s = 0;
-          ph ^= 1;
-        }
-      }
-    }
-    griddep_wait();
-    griddep_launch();
-    return;
-  }
-  // ---------------- consumers
-  griddep_wait();
-  griddep_launch();
-  if (EPI == DEC_EPI_HEAD) {
-    // final RMSNorm of the hidden rows (numerics.py:161-166), bf16 for the GEMV
-    if (warp < B) {
-      const float4 *hr = reinterpret_cast<const float4 *>(a.hidden + (size_t)warp * a.hstride);
-      float ss = 0.f;
-      for (int k = lane; k < K / 4; k += 32) {
-        const float4 v = hr[k];
-        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
-      }
-      ss = warp_sum(ss);
-      if (lane == 0) s_scale[warp] = 1.f / sqrtf(ss / (float)K + a.eps);
-    }
-    named_barrier_sync(1, 256);
-    for (int i = threadIdx.x; i < B * K / 4; i += 256) {
-      const int b = (i * 4) / K, k = (i * 4) % K;
-      const float4 v = *reinterpret_cast<const float4 *>(a.hidden + (size_t)b * a.hstride + k);
-      const float4 fw = *reinterpret_cast<const float4 *>(a.final_w + k);
-      const float sc = s_scale[b];
-      __nv_bfloat162 lo = __floats2bfloat162_rn(v.x * sc * fw.x, v.y * sc * fw.y);
-      __nv_bfloat162 hi = __floats2bfloat162_rn(v.z * sc * fw.z, v.w * sc * fw.w);
-      uint2 pk;
-      pk.x = *reinterpret_cast<uint32_t *>(&lo);
-      pk.y = *reinterpret_cast<uint32_t *>(&hi);
-      *reinterpret_cast<uint2 *>(xs + (size_t)b * K + k) = pk;
-    }
-  } else {
-    const uint4 *src = reinterpret_cast<const uint4 *>(a.X);
-    uint4 *dst = reinterpret_cast<uint4 *>(xs);
-    for (int i = threadIdx.x; i < B * K / 8; i += 256) dst[i] = src[i];
-    if (EPI == DEC_EPI_OUT && warp < B) {
-      float s = 0.f;
-      for (int j = lane; j < a.nssq; j += 32) s += a.ssq[warp * a.nssq + j];
-      s = warp_sum(s);
-      if (lane == 0) s_scale[warp] = 1.f / sqrtf(s * a.inv_d + a.eps);
-    }
-  }
-  named_barrier_sync(1, 256);
-  float best[DEC_MAX_B];
-  int bidx[DEC_MAX_B];
-#pragma unroll
-  for (int b = 0; b < DEC_MAX_B; ++b) {
-    best[b] = -INFINITY;
-    bidx[b] = 0x7fffffff;
-  }
-  const int kchunks = K / 256;
-  int s = 0;
-  uint32_t ph = 0;
-  for (int gi = g0; gi < g1; ++gi) {
-    const int n = gi * DS_ROWS + warp;
-    // epilogue inputs that do not depend on the GEMV: load before the stage wait
-    float e_old = 0.f, e_w[4] = {0.f, 0.f, 0.f, 0.f}, e_win[3] = {0.f, 0.f, 0.f}, e_b = 0.f;
-    if (lane < B && n < a.N) {
-      if (EPI == DEC_EPI_OUT) {
-        e_old = a.hidden[(size_t)lane * a.N + n];
-      } else if (EPI == DEC_EPI_IN && a.k == 4 && n >= a.d_inner && n < a.d_inner + a.conv_dim) {
-        const int ch = n - a.d_inner;
-        const float *ci = a.conv_in + ((size_t)lane * a.conv_dim + ch) * 3;
-#pragma unroll
-        for (int j = 0; j < 3; ++j) e_win[j] = ci[j];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) e_w[j] = a.conv_w[(size_t)ch * 4 + j];
-        e_b = a.conv_b[ch];
-      }
-    }
-    mbar_wait_s(&full[s], ph);
-    const bf16 *wr = reinterpret_cast<const bf16 *>(ring + (size_t)s * cfg.stage_bytes) +
-                     (size_t)warp * K + lane * 8;
-    float acc[DEC_MAX_B];
-#pragma unroll
-    for (int b = 0; b < DEC_MAX_B; ++b) acc[b] = 0.f;
-    if (n < a.N) {
-      for (int c = 0; c < kchunks; ++c) {
-        const uint4 w = *reinterpret_cast<const uint4 *>(wr + c * 256);
-#pragma unroll
-        for (int b = 0; b < DEC_MAX_B; ++b)
-          if (b < B)
-            acc[b] += dot8(w, *reinterpret_cast<const uint4 *>(xs + (size_t)b * K + c * 256 + lane * 8));
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive_s(&empty[s]);
-    if (++s == S) {
-      s = 0;
-      ph ^= 1;
-    }
-    if (n >= a.N) continue;
-#pragma unroll
-    for (int b = 0; b < DEC_MAX_B; ++b)
-      if (b < B) acc[b] = warp_sum(acc[b]);
-    float v = 0.f;
-#pragma unroll
-    for (int b = 0; b < DEC_MAX_B; ++b)
-      if (lane == b) v = acc[b];
-    const int b = lane;
-    if (b >= B) continue;
-    if (EPI == DEC_EPI_HEAD) {
-      if (a.logits) a.logits[(size_t)b * a.N + n] = v;
-#pragma unroll
-      for (int bb = 0; bb < DEC_MAX_B; ++bb)
-        if (bb == b && v > best[bb]) {  // rows ascend: strict > keeps the lowest id
-          best[bb] = v;
-          bidx[bb] = n;
-        }
-    } else if (EPI == DEC_EPI_IN) {
-      if (n < a.d_inner) {
-        a.z[(size_t)b * a.d_inner + n] = v;
-      } else if (n < a.d_inner + a.conv_dim) {
-        const int ch = n - a.d_inner, km = a.k - 1;
-        float *co = a.conv_out + ((size_t)b * a.conv_dim + ch) * km;
-        if (a.k == 4) {  // taps oldest first, window prefetched above
-          const float acc2 = e_win[0] * e_w[0] + e_win[1] * e_w[1] + e_win[2] * e_w[2] + v * e_w[3];
-          a.act[(size_t)b * a.conv_dim + ch] = silu(acc2 + e_b);
-          co[0] = e_win[1];
-          co[1] = e_win[2];
-          co[2] = v;
-        } else {
-          const float *ci = a.conv_in + ((size_t)b * a.conv_dim + ch) * km;
-          float win[16];
-          for (int j = 0; j < km; ++j) win[j] = ci[j];
-          win[km] = v;
-          float acc2 = 0.f;
-          for (int j = 0; j <= km; ++j) acc2 += win[j] * a.conv_w[(size_t)ch * a.k + j];
-          a.act[(size_t)b * a.conv_dim + ch] = silu(acc2 + a.conv_b[ch]);
-          for (int j = 0; j < km; ++j) co[j] = win[j + 1];
-        }
-      } else {
-        const int h = n - a.d_inner - a.conv_dim;
-        a.dt[(size_t)b * a.H + h] = clamp_(softplus(v + a.dt_bias[h]), a.dt_lo, a.dt_hi);
-      }
-    } else {  // DEC_EPI_OUT
-      const float nv = e_old + s_scale[b] * v;
-      a.hidden[(size_t)b * a.N + n] = nv;
-      a.hidden_lp[(size_t)b * a.N + n] = __float2bfloat16_rn(nv);
-    }
-  }
-  if (EPI == DEC_EPI_HEAD) {
-#pragma unroll
-    for (int bb = 0; bb < DEC_MAX_B; ++bb)
-      if (lane == bb) {
-        s_best[warp][bb] = best[bb];
-        s_bidx[warp][bb] = bidx[bb];
-      }
-    named_barrier_sync(1, 256);
-    if (threadIdx.x < B) {
-      const int bb = threadIdx.x;
-      float bv = -INFINITY;
-      int bi = 0x7fffffff;
-      for (int w = 0; w < 8; ++w) {
-        const float ov = s_best[w][bb];
-        const int oi = s_bidx[w][bb];
-        if (ov > bv || (ov == bv && oi < bi)) {
-          bv = ov;
-          bi = oi;
-        }
-      }
-      a.amax_val[blockIdx.x * B + bb] = bv;
-      a.amax_idx[blockIdx.x * B + bb] = bi;
-    }
-  }
-}
-
-// final argmax over the per-CTA partials; one warp per batch row
-__global__ void dec_argmax(const float *__restrict__ val, const int *__restrict__ idx, int nparts,
-                           int B, int64_t *__restrict__ out) {
-  griddep_wait();
-  const int b = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (b >= B) return;
-  float bv = -INFINITY;
-  int bi = 0x7fffffff;
-  for (int i = lane; i < nparts; i += 32) {
-    const float v = val[i * B + b];
-    const int j = idx[i * B + b];
-    if (v > bv || (v == bv && j < bi)) {
-      bv = v;
-      bi = j;
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ov > bv || (ov == bv && oi < bi)) {
-      bv = ov;
-      bi = oi;
-    }
-  }
-  if (lane == 0) out[b] = bi == 0x7fffffff ? 0 : bi;
-}
-
-// SSM step + D skip + gate for one (b, head, row-split): grid (H*PS, B),
-// 128 threads; warps over head rows p, lanes over state columns n.
-// ssm_out may alias ssm_in (each element read then written by one thread).
-struct DecSsmArgs {
-  int H, P, G, N, d_inner, conv_dim, PS;
-  const float *act, *z, *dt, *a, *D;
-  const float *ssm_in;
-  float *ssm_out;
-  bf16 *u;      // (B, d_inner) gated output
-  float *ssq;   // (B, H*PS) partial sums of u^2
-};
-
-__global__ __launch_bounds__(128) void dec_ssm(DecSsmArgs s) {
-  __shared__ float bs[256], cs[256], red[4];
-  griddep_wait();
-  griddep_launch();
-  const int hs = blockIdx.x, b = blockIdx.y;
-  const int h = hs / s.PS, part = hs % s.PS;
-  const int g = h / (s.H / s.G);
-  const float *arow = s.act + (size_t)b * s.conv_dim;
-  for (int n = threadIdx.x; n < s.N; n += blockDim.x) {
-    bs[n] = arow[s.d_inner + g * s.N + n];
-    cs[n] = arow[s.d_inner + s.G * s.N + g * s.N + n];
-  }
-  __syncthreads();
-  const float dt = s.dt[(size_t)b * s.H + h];
-  const float decay = expf(s.a[h] * dt);
-  const float Dh = s.D[h];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int rows = s.P / s.PS;
-  const size_t base = (((size_t)b * s.H + h) * s.P) * s.N;
-  float ss = 0.f;
-  for (int pp = part * rows + warp; pp < (part + 1) * rows; pp += 4) {
-    const float xv = arow[h * s.P + pp];
-    const float dx = dt * xv;
-    float acc = 0.f;
-    const float4 *src = reinterpret_cast<const float4 *>(s.ssm_in + base + (size_t)pp * s.N);
-    float4 *dst = reinterpret_cast<float4 *>(s.ssm_out + base + (size_t)pp * s.N);
-    for (int n4 = lane; n4 < s.N / 4; n4 += 32) {
-      float4 hv = src[n4];
-      const int n = n4 * 4;
-      hv.x = decay * hv.x + dx * bs[n];
-      hv.y = decay * hv.y + dx * bs[n + 1];
-      hv.z = decay * hv.z + dx * bs[n + 2];
-      hv.w = decay * hv.w + dx * bs[n + 3];
-      dst[n4] = hv;
-      acc = fmaf(cs[n], hv.x, acc);
-      acc = fmaf(cs[n + 1], hv.y, acc);
-      acc = fmaf(cs[n + 2], hv.z, acc);
-      acc = fmaf(cs[n + 3], hv.w, acc);
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      const float y = acc + Dh * xv;
-      const float u = y * silu(s.z[(size_t)b * s.d_inner + h * s.P + pp]);
-      s.u[(size_t)b * s.d_inner + h * s.P + pp] = __float2bfloat16_rn(u);
-      ss += u * u;
-    }
-  }
-  if (lane == 0) red[warp] = ss;
-  __syncthreads();
-  if (threadIdx.x == 0) s.ssq[(size_t)b * s.H * s.PS + hs] = red[0] + red[1] + red[2] + red[3];
-}
-
 // ---------------------------------------------------------------------------
-// Wide-batch decode (bf16 mode, B > DEC_MAX_B): the SSM state dominates the
+// Decode (bf16 mode): at wide batches the SSM state dominates the
 // step's bytes (1.3B, B = 64: 13.2 GB of f32 state read + written vs 2.7 GB of
 // weights), so the layer's middle is one streaming kernel.
 //

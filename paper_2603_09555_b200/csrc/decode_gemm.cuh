@@ -39,8 +39,6 @@ struct DgArgs {
   int ksplit;
   float *out;         // (ksplit, B, ldo)
   long ldo, split_stride;
-  const uint8_t *pf;  // optional: bytes to warm into L2 for a later kernel (split over the CTAs)
-  long pf_bytes;
 };
 
 template <int BNB, bool SMALL = false>
@@ -131,18 +129,6 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;
     const int n = n_blk * 128 + q * 32 + lane;
     float *dst = a.out + (size_t)ks * a.split_stride + n;
-    if (a.pf_bytes > 0 && warp == 2 && lane == 0) {
-      // L2 warm-up of weights a later kernel streams (the epilogue warps are idle until the
-      // MMAs finish): this CTA's 16-byte-aligned slice, 32 KB per bulk prefetch
-      const long per = ((a.pf_bytes + gridDim.x - 1) / gridDim.x + 15) & ~15L;
-      const long lo = (long)blockIdx.x * per;
-      const long hi = min(lo + per, a.pf_bytes & ~15L);
-      for (long o = lo; o < hi; o += 32768) {
-        const uint32_t nb = (uint32_t)min(32768L, hi - o);
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pf + o), "r"(nb)
-                     : "memory");
-      }
-    }
     sm100::mbar_wait(&tdone, 0);
     sm100::tc_fence_after();
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);

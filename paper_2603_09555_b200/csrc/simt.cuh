@@ -14,12 +14,13 @@ namespace ssd200 {
 // =========================================================================
 template <typename T, typename TE>
 __global__ void embed_kernel(const int64_t *__restrict__ tok, const TE *__restrict__ E, int d_model,
-                             T *__restrict__ hid, bf16 *__restrict__ hid_lp) {
+                             int vocab, T *__restrict__ hid, bf16 *__restrict__ hid_lp) {
   const int r = blockIdx.x;
   const int64_t id = tok[r];
-  const TE *src = E + (size_t)id * d_model;
+  const bool ok = id >= 0 && id < vocab;  // device-resident ids: a bad id poisons its row
+  const TE *src = E + (size_t)(ok ? id : 0) * d_model;
   for (int c = threadIdx.x; c < d_model; c += blockDim.x) {
-    T v = cvt<T>(src[c]);
+    T v = ok ? cvt<T>(src[c]) : (T)NAN;
     hid[(size_t)r * d_model + c] = v;
     if (hid_lp) hid_lp[(size_t)r * d_model + c] = cvt<bf16>(v);
   }

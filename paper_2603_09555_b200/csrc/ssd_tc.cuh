@@ -25,6 +25,7 @@ constexpr int TC_P = 64, TC_N = 128, TC_L = 256;
 
 struct TcSsdArgs {
   int B, T, H, Nc, NG, HG;  // HG = heads per group = H / NG
+  int interleave;           // ssd_tc_out block order (see there)
   int d_inner;
   const bf16 *z;      // gate, (rows, z_ld) — first d_inner columns of the in_proj output
   long z_ld;
@@ -39,8 +40,7 @@ struct TcSsdArgs {
   bf16 *prev;         // (B, Nc, H, N, P) bf16: state entering each chunk (transposed)
   float *final_state; // (B, H, P, N)
   bf16 *u_out;        // (rows, d_inner)
-  float *ssq;         // (rows, NG) partial sum of u^2
-  unsigned long long *trace;  // debug: clock stamps of CTA 0 (or null)
+  float *ssq;         // (H/8 * OUT_KW, rows) partial sums of u^2 per (8-head slice, column half)
 };
 
 __device__ __forceinline__ unsigned long long clk64() {
@@ -289,7 +289,10 @@ __global__ void __launch_bounds__(192, 1)
         const int l = tid + rr * 128;
         const int t = c * TC_L + l;
         const float *dtr = p.dtT + ((long)b * p.H + h) * csb + (long)c * TC_L;
-        const float w = t < p.T ? dtr[l] * ex2((cend - cs[l]) * kLog2e) : 0.f;
+        // the same bf16 row weight and packed multiply as ssd_tc_chunkscan, so both
+        // scan variants give bitwise-equal chunk states (batch invariance)
+        const __nv_bfloat162 w2 = __float2bfloat162_rn(
+            t < p.T ? dtr[l] * ex2((cend - cs[l]) * kLog2e) : 0.f);
         uint4 *row = reinterpret_cast<uint4 *>(xb + l * 128);
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch) {
@@ -297,10 +300,7 @@ __global__ void __launch_bounds__(192, 1)
           uint4 v = row[pc];
           __nv_bfloat162 *e = reinterpret_cast<__nv_bfloat162 *>(&v);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            float2 f = __bfloat1622float2(e[j]);
-            e[j] = __floats2bfloat162_rn(f.x * w, f.y * w);
-          }
+          for (int j = 0; j < 4; ++j) e[j] = __hmul2(e[j], w2);
           row[pc] = v;
         }
       }
@@ -377,7 +377,13 @@ __global__ __launch_bounds__(256) void ssd_tc_pass(TcSsdArgs p) {
 //   prev_c = s ;  s = e^{cs_end,c} s + S_c          (running state in registers:
 //                                                    thread n holds s[:, n])
 // Two smem stages (B^T 64 KB + X 32 KB) and two TMEM accumulators pipeline
-// chunk c+1's load/scale/MMA under chunk c's state update.
+// chunk c+1's load/scale/MMA under chunk c's state update.  Eight math warps
+// (two per TMEM lane quarter): each scales one X row per chunk and keeps half
+// of one state row (32 of the 64 head columns) — the per-chunk critical path
+// (scale, TMEM read-out, bf16 prev store, state update) is latency-bound, so
+// more warps per scheduler shorten it.
+constexpr int CHUNKSCAN_THREADS = 64 + 256;  // TMA warp, MMA warp, 8 math warps
+
 struct ScanSmem {
   static constexpr uint32_t STG = 98304;  // Bt [2 n-blocks][256 l][64 n] + X [256 l][64 p]
   static constexpr uint32_t XO = 65536;
@@ -388,7 +394,7 @@ struct ScanSmem {
 // mc = CTAs per cluster (1 or 4): the heads h..h+3 of one batch row share every
 // chunk's B tile, so with mc = 4 each CTA loads a quarter of it and multicasts it
 // to the cluster (and a stage is refilled only once all four have consumed it).
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(CHUNKSCAN_THREADS, 1)
     ssd_tc_chunkscan(const __grid_constant__ CUtensorMap tm_act, TcSsdArgs p, int mc) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t *sm = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -406,10 +412,10 @@ __global__ void __launch_bounds__(192, 1)
     sm100::tma_prefetch(&tm_act);
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&full[i], 1);
-      sm100::mbar_init(&xsd[i], 128);
+      sm100::mbar_init(&xsd[i], 256);
       sm100::mbar_init(&sfull[i], 1);
       sm100::mbar_init(&stfree[i], mc);  // every CTA of the cluster frees the stage
-      sm100::mbar_init(&tfree[i], 128);
+      sm100::mbar_init(&tfree[i], 256);
     }
     sm100::fence_barrier_init();
   }
@@ -430,7 +436,6 @@ __global__ void __launch_bounds__(192, 1)
         const int st = c & 1;
         uint8_t *stg = sm + st * ScanSmem::STG;
         sm100::mbar_wait(&stfree[st], ((c >> 1) & 1) ^ 1);
-        if (p.trace && blockIdx.x == 0 && c < 64) p.trace[4096 + c * 8 + 0] = clk64();
         sm100::mbar_arrive_expect_tx(&full[st], ScanSmem::STG);
         if (mc == 4) {  // this CTA's quarter of B, to all four CTAs
           const int j = crank >> 1, q = crank & 1;
@@ -454,9 +459,7 @@ __global__ void __launch_bounds__(192, 1)
         const int st = c & 1;
         const uint32_t par = (c >> 1) & 1;
         sm100::mbar_wait(&xsd[st], par);
-        if (p.trace && blockIdx.x == 0 && c < 64) p.trace[4096 + c * 8 + 1] = clk64();
         sm100::mbar_wait(&tfree[st], par ^ 1);
-        if (p.trace && blockIdx.x == 0 && c < 64) p.trace[4096 + c * 8 + 2] = clk64();
         sm100::tc_fence_after();
         const uint32_t a0 = sm100::smem_u32(sm + st * ScanSmem::STG);
         const uint32_t x0 = a0 + ScanSmem::XO;
@@ -474,58 +477,51 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    const int tid = threadIdx.x - 64;  // 0..127: X rows in the scale step, state row n later
-    const int q = warp & 3;
-    const int n = q * 32 + lane;
+    const int tid = threadIdx.x - 64;  // 0..255: X row in the scale step
+    const int q = warp & 3;            // TMEM lane quarter
+    const int half = (warp - 2) >> 2;  // state columns [32 half, 32 half + 32)
+    const int n = q * 32 + lane;       // state row (TMEM lane)
     const float *csg = p.cs + ((long)b * p.H + h) * csb;
     const float *dtg = p.dtT + ((long)b * p.H + h) * csb;
     const float *ceg = p.cs_end + ((long)b * p.H + h) * Nc;
-    // row weights w_l = dt_l e^{cs_end - cs_l} of a chunk: loaded one chunk ahead
+    // row weight w_l = dt_l e^{cs_end - cs_l} of a chunk: loaded one chunk ahead
     // so the global-load latency stays off the scale step
     struct RowW {
-      float dt[2], cs[2], cend;
+      float dt, cs, cend;
     };
     auto load_w = [&](int c, RowW &f) {
       if (c >= Nc) return;
-#pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        const long t = (long)c * TC_L + tid + rr * 128;
-        f.dt[rr] = t < p.T ? dtg[t] : 0.f;
-        f.cs[rr] = csg[t];
-      }
+      const long t = (long)c * TC_L + tid;
+      f.dt = t < p.T ? dtg[t] : 0.f;
+      f.cs = csg[t];
       f.cend = ceg[c];
     };
     auto scale = [&](int c, const RowW &f) {
       const int st = c & 1;
       sm100::mbar_wait(&full[st], (c >> 1) & 1);
-      if (p.trace && blockIdx.x == 0 && tid == 0 && c < 64) p.trace[4096 + c * 8 + 3] = clk64();
       uint8_t *xb = sm + st * ScanSmem::STG + ScanSmem::XO;
+      const int l = tid;
+      const __nv_bfloat162 w2 = __float2bfloat162_rn(f.dt * ex2((f.cend - f.cs) * kLog2e));
+      uint4 *row = reinterpret_cast<uint4 *>(xb + l * 128);
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        const int l = tid + rr * 128;
-        const __nv_bfloat162 w2 =
-            __float2bfloat162_rn(f.dt[rr] * ex2((f.cend - f.cs[rr]) * kLog2e));
-        uint4 *row = reinterpret_cast<uint4 *>(xb + l * 128);
+      for (int ch = 0; ch < 8; ++ch) {  // packed bf16 multiply (X is a bf16 MMA operand)
+        // every 16-byte chunk of the row gets the same weight, so visit them in a
+        // lane-rotated order: the 8 lanes of a shared-memory phase hit 8 bank groups
+        const int pc = (ch + l) & 7;
+        uint4 v = row[pc];
+        __nv_bfloat162 *e = reinterpret_cast<__nv_bfloat162 *>(&v);
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {  // packed bf16 multiply (X is a bf16 MMA operand)
-          // every 16-byte chunk of the row gets the same weight, so visit them in a
-          // lane-rotated order: the 8 lanes of a shared-memory phase hit 8 banks groups
-          const int pc = (ch + l) & 7;
-          uint4 v = row[pc];
-          __nv_bfloat162 *e = reinterpret_cast<__nv_bfloat162 *>(&v);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) e[j] = __hmul2(e[j], w2);
-          row[pc] = v;
-        }
+        for (int j = 0; j < 4; ++j) e[j] = __hmul2(e[j], w2);
+        row[pc] = v;
       }
       sm100::fence_proxy_async();
       sm100::mbar_arrive(&xsd[st]);
-      if (p.trace && blockIdx.x == 0 && tid == 0 && c < 64) p.trace[4096 + c * 8 + 4] = clk64();
     };
-    float s[TC_P];
+    float s[32];
     const long sbase = ((long)b * p.H + h) * TC_P * TC_N + n;
 #pragma unroll
-    for (int pp = 0; pp < TC_P; ++pp) s[pp] = p.init ? p.init[sbase + (long)pp * TC_N] : 0.f;
+    for (int pp = 0; pp < 32; ++pp)
+      s[pp] = p.init ? p.init[sbase + (long)(32 * half + pp) * TC_N] : 0.f;
     // chunk k's weights live in wa (k even) / wb (k odd); chunk k+2's are fetched
     // right after scale(k), two chunks before they are needed
     RowW wa, wb;
@@ -545,22 +541,19 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       const int st = c & 1;
+      const float decay = expf(ceg[c]);
       sm100::mbar_wait(&sfull[st], (c >> 1) & 1);
-      if (p.trace && blockIdx.x == 0 && tid == 0 && c < 64) p.trace[4096 + c * 8 + 5] = clk64();
       sm100::tc_fence_after();
-      uint32_t r0[32], r1[32];
-      const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + st * TC_P;
-      sm100::tmem_ld32(ta, r0);
-      sm100::tmem_ld32(ta + 32, r1);
+      uint32_t r0[32];
+      sm100::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + st * TC_P + 32 * half, r0);
       sm100::tmem_ld_wait();
       sm100::tc_fence_before();
       sm100::mbar_arrive(&tfree[st]);
-      const float decay = expf(ceg[c]);
-      // state entering chunk c, stored [n][p]: this thread's 64 values are contiguous
+      // state entering chunk c, stored [n][p]: this thread's 32 values are contiguous
       uint4 *pv = reinterpret_cast<uint4 *>(
-          p.prev + ((((long)b * Nc + c) * p.H + h) * TC_N + n) * TC_P);
+          p.prev + ((((long)b * Nc + c) * p.H + h) * TC_N + n) * TC_P + 32 * half);
 #pragma unroll
-      for (int g = 0; g < TC_P / 8; ++g) {
+      for (int g = 0; g < 4; ++g) {
         uint32_t w[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -570,14 +563,10 @@ __global__ void __launch_bounds__(192, 1)
         pv[g] = make_uint4(w[0], w[1], w[2], w[3]);
       }
 #pragma unroll
-      for (int pp = 0; pp < 32; ++pp) {
-        s[pp] = decay * s[pp] + __uint_as_float(r0[pp]);
-        s[pp + 32] = decay * s[pp + 32] + __uint_as_float(r1[pp]);
-      }
-      if (p.trace && blockIdx.x == 0 && tid == 0 && c < 64) p.trace[4096 + c * 8 + 6] = clk64();
+      for (int pp = 0; pp < 32; ++pp) s[pp] = decay * s[pp] + __uint_as_float(r0[pp]);
     }
 #pragma unroll
-    for (int pp = 0; pp < TC_P; ++pp) p.final_state[sbase + (long)pp * TC_N] = s[pp];
+    for (int pp = 0; pp < 32; ++pp) p.final_state[sbase + (long)(32 * half + pp) * TC_N] = s[pp];
   }
   __syncthreads();
   if (mc > 1) sm100::cluster_sync();  // no CTA leaves while peers may still signal it

@@ -12,6 +12,8 @@
 //     Ydiag = M . X_h        (K = 128(R+1)), A operand read from TMEM   ssd.py:149
 //     Yoff  = C_R . prev_h^T (K = N = 128)                               ssd.py:196
 //     y = Ydiag + e^{cs_l} Yoff + D_h x;  u = y * silu(z);  sum u^2       model.py:166-167
+//   sum u^2 leaves as one partial per (8-head slice, column half) — independent of
+//   the head grouping, so the norm's row scale is batch-invariant.
 //
 // M lives in TMEM (tcgen05.st by the math warps, consumed as the A operand of
 // tcgen05.mma), double buffered: the math warps build M_{h+1} while the tensor
@@ -27,7 +29,7 @@
 // every 32-column chunk of M, CW = 32 / OUT_KW (so the expensive diagonal chunk
 // is shared evenly) and runs the epilogue on head columns [EW k, EW (k+1)),
 // EW = 64 / OUT_KW.
-// Block order: the heavier R = 1 tiles first, then R = 0.
+// Block order: R = 1 / R = 0 tiles of one (b, c, g) side by side (L2 reuse).
 #pragma once
 
 #include <type_traits>
@@ -46,9 +48,6 @@ constexpr int OUT_MW = 4 * OUT_KW;     // math warps
 constexpr int OUT_EW = TC_P / OUT_KW;  // epilogue head columns per warp
 constexpr int OUT_MATH = OUT_MW * 32;  // math threads
 constexpr int OUT_THREADS = OUT_MATH + 64;
-#ifndef SSD200_OUT_TRACE
-#define SSD200_OUT_TRACE 0  // 1: clock64 stamps of CTA 0 into TcSsdArgs::trace (scripts/trace_ssd_out.py)
-#endif
 
 struct OutSmem {
   static constexpr uint32_t CR = 0;           // C rows of the tile: 2 x [128 l][64 n] (SW128)
@@ -57,8 +56,7 @@ struct OutSmem {
   static constexpr uint32_t P0 = X0 + 2 * 32768;  // 2 x [128 n][64 p]
   static constexpr uint32_t Z0 = P0 + 2 * 16384;  // gate z of the current head [128 l][64 p]
   static constexpr uint32_t WC = Z0 + 16384;       // per warp 4 x 8 OUT_CW f32 (cs2, cf, dt, cr)
-  static constexpr uint32_t SQ = WC + OUT_MW * 4 * 8 * OUT_CW * 4;  // ssq of slices 1..
-  static constexpr uint32_t DH = SQ + (OUT_KW - 1) * 512;  // D of the group's heads (<= 128)
+  static constexpr uint32_t DH = WC + OUT_MW * 4 * 8 * OUT_CW * 4;  // D of the group's heads (<= 128)
   static constexpr uint32_t BAR = DH + 512;
   static constexpr uint32_t TOTAL = BAR + 256 + 1024;
   static constexpr int MAX_HG = 128;  // heads per CTA (DH table)
@@ -91,9 +89,12 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
   uint32_t *tslot = reinterpret_cast<uint32_t *>(bar_cb + 18);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // interleaved (default): the two row tiles of one (b, c, g) are neighbours in
+  // launch order, so they run together and the X / prev tiles both read come
+  // from L2 the second time; else the heavier R = 1 tiles first, then R = 0
   const int half_grid = gridDim.x >> 1;
-  const int R = blockIdx.x < half_grid ? 1 : 0;
-  int idx = R ? blockIdx.x : blockIdx.x - half_grid;
+  const int R = p.interleave ? ((blockIdx.x & 1) ^ 1) : (blockIdx.x < half_grid ? 1 : 0);
+  int idx = p.interleave ? (blockIdx.x >> 1) : (R ? blockIdx.x : blockIdx.x - half_grid);
   const int g = idx % p.NG;
   idx /= p.NG;
   const int b = idx / p.Nc, c = idx % p.Nc;
@@ -178,21 +179,8 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
         const int buf = i & 1;
         const uint32_t par = (i >> 1) & 1;
         const uint32_t yd = tmem + TM_Y + buf * 128, yo = yd + 64;
-#if SSD200_OUT_TRACE
-        unsigned long long *tr =
-            (p.trace && blockIdx.x == 0 && i < 64) ? p.trace + i * 8 : nullptr;
-#endif
-#if SSD200_OUT_TRACE
-        if (tr) tr[0] = clk64();
-#endif
         sm100::mbar_wait(&yfree[buf], par ^ 1);
-#if SSD200_OUT_TRACE
-        if (tr) tr[1] = clk64();
-#endif
         sm100::mbar_wait(&bar_p[buf], par);
-#if SSD200_OUT_TRACE
-        if (tr) tr[2] = clk64();
-#endif
         sm100::tc_fence_after();
         const uint32_t pb = sm100::smem_u32(sm + OutSmem::P0 + buf * 16384);
 #pragma unroll
@@ -204,9 +192,6 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
         sm100::mma_commit(&pfree[buf]);
         sm100::mbar_wait(&bar_x[buf], par);
         sm100::mbar_wait(&mrdy[buf], par);
-#if SSD200_OUT_TRACE
-        if (tr) tr[3] = clk64();
-#endif
         sm100::tc_fence_after();
         const uint32_t xb = sm100::smem_u32(sm + OutSmem::X0 + buf * 32768);
         const uint32_t am = tmem + TM_M + buf * 128;
@@ -214,9 +199,6 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
           const uint64_t bd = sm100::sw128_desc(xb + k * 2048, 8192, 1024);
           sm100::mma_bf16_ts(yd, am + k * 8, bd, idy, k > 0);
         }
-#if SSD200_OUT_TRACE
-        if (tr) tr[7] = clk64();
-#endif
         sm100::mma_commit(&bar_y[buf]);  // accumulators ready, M buffer and X tile free
         sm100::mma_commit(&xfree[buf]);
       }
@@ -241,7 +223,6 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
     float *wcf = wcs + 8 * CW;
     float *wdt = wcs + 16 * CW;
     float *wcr = wcs + 24 * CW;
-    float *sq_s = reinterpret_cast<float *>(sm + OutSmem::SQ);
     float *d_s = reinterpret_cast<float *>(sm + OutSmem::DH);
     // G row of this thread: NS bf16 in 16-byte pieces XOR-swizzled by row
     // (conflict-free); pieces 4j + CP kw + [0, CP) are this warp's slice of chunk j
@@ -338,9 +319,6 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
           pd[e] = *reinterpret_cast<uint32_t *>(&v);
         }
         st_m(mt + 16 * jd, pd, true);
-#if SSD200_OUT_TRACE
-        if (p.trace && blockIdx.x == 0 && lane == 0 && mw == 0 && hh < 16) p.trace[6144 + hh * 16 + 2] = clk64();
-#endif
       }
       // off-diagonal chunks: M = (G * cf) * rf on packed bf16 pairs (M is bf16 anyway)
       const uint32_t *wcfb = reinterpret_cast<const uint32_t *>(wcf);
@@ -362,20 +340,8 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
           pk[e] = *reinterpret_cast<const uint32_t *>(&m);
         }
         st_m(mt + 16 * j, pk, j < jd);
-#if SSD200_OUT_TRACE
-        if (p.trace && blockIdx.x == 0 && lane == 0 && mw == 0 && hh < 16) p.trace[6144 + hh * 16 + 3 + j] = clk64();
-#endif
       }
-#if SSD200_OUT_TRACE
-      const unsigned long long t_st = clk64();
-#endif
       sm100::tmem_st_wait();
-#if SSD200_OUT_TRACE
-      if (p.trace && blockIdx.x == 0 && lane == 0 && hh - 1 < 16 && hh >= 1) {
-        p.trace[2048 + (mw * 16 + hh - 1) * 8 + 4] = t_st;
-        p.trace[2048 + (mw * 16 + hh - 1) * 8 + 5] = clk64();
-      }
-#endif
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&mrdy[hh & 1]);
@@ -434,26 +400,11 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
       uint4 xv[EW / 8], zv[EW / 8];  // x (D skip) and z (gate) of head i, columns [pc, pc+EW)
       const float el = ex2(csl);
       const float Dh = d_s[i];
-#if SSD200_OUT_TRACE
-      unsigned long long *tw = (p.trace && blockIdx.x == 0 && lane == 0 && i < 16)
-                                   ? p.trace + 2048 + (mw * 16 + i) * 8
-                                   : nullptr;
-      if (tw) tw[0] = clk64();
-#endif
       if (i + 1 < p.HG) {  // M_{i+1} into the other buffer while the tensor core runs head i
         csl = commit(nxt);
-#if SSD200_OUT_TRACE
-        if (p.trace && blockIdx.x == 0 && lane == 0 && mw == 0 && i + 1 < 16) p.trace[6144 + (i + 1) * 16 + 0] = clk64();
-#endif
         if (i + 2 < p.HG) fetch(i + 2, nxt);
-#if SSD200_OUT_TRACE
-        if (p.trace && blockIdx.x == 0 && lane == 0 && mw == 0 && i + 1 < 16) p.trace[6144 + (i + 1) * 16 + 1] = clk64();
-#endif
         build(i + 1, csl);
       }
-#if SSD200_OUT_TRACE
-      if (tw) tw[1] = clk64();
-#endif
       sm100::mbar_wait(bar_z, i & 1);  // z tile of head i (TMA, SWIZZLE_128B)
 #pragma unroll
       for (int cc = 0; cc < EW / 8; ++cc)
@@ -467,9 +418,6 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&xfree[buf]);
       }
-#if SSD200_OUT_TRACE
-      if (tw) tw[2] = clk64();
-#endif
       sm100::tc_fence_after();
       // ---- epilogue(i) on columns [pc, pc+EW) in 16-column steps, overlapping MMA(i+1)
       const uint32_t ydt = tmem + lane_off + TM_Y + buf * 128 + pc;
@@ -515,17 +463,15 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
         sm100::bulk_wait_read0();
         sm100::mbar_arrive(zfree);
       }
-#if SSD200_OUT_TRACE
-      if (tw) tw[3] = clk64();
-#endif
-    }
-    if (kw > 0) sq_s[(kw - 1) * 128 + row] = ssq;
-    named_bar(1, OUT_MATH);
-    if (kw == 0 && valid) {
-      float s = ssq;
-#pragma unroll
-      for (int k = 1; k < OUT_KW; ++k) s += sq_s[(k - 1) * 128 + row];
-      p.ssq[((long)b * p.T + t) * p.NG + g] = s;
+      // sum u^2 of this warp's columns over the 8-head slice that ends here:
+      // one partial per (slice, column half), slice-major (n_slices * OUT_KW, rows),
+      // so the out_proj's row scale sums the same partials in the same order
+      // whatever head grouping (and hence batch) this launch used
+      if ((i & 7) == 7) {
+        if (valid)
+          p.ssq[(long)(((h0 + i) >> 3) * OUT_KW + kw) * ((long)p.B * p.T) + (long)b * p.T + t] = ssq;
+        ssq = 0.f;
+      }
     }
   }
   __syncthreads();

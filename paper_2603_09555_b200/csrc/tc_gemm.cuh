@@ -25,21 +25,17 @@
 
 namespace ssd200 {
 
-// TC_EPI_RESID_NORM: hidden += acc * rstd(row), rstd = 1/sqrt(sum_g ssq[row,g]/d + eps):
+// TC_EPI_RESID_NORM: hidden += acc * rstd(row), rstd = 1/sqrt(sum_g ssq[g,row]/d + eps)
+// (the partials are summed in slice order g = 0, 1, ..: a fixed function of the
+// widths, so a row's scale does not depend on the batch it runs in):
 // the gated RMSNorm's row scale applied after the GEMM (it commutes with it;
 // norm_w is folded into W_out's columns at load time) — numerics.py:149-158.
-// TC_EPI_INPROJ_CONV: in_proj with the causal depthwise conv (k = 4) + SiLU of
-// the xBC columns fused (numerics.py:169-189): M tiles overlap by a 3-row halo
-// (row stride 125), the taps' history rows come from neighbouring TMEM lanes
-// (warp shuffles, plus a small smem exchange across warps); writes z (bf16),
-// post-conv xBC (bf16), dt (f32) and the pre-activation conv tail (f32).
 enum {
   TC_EPI_F32 = 0,
   TC_EPI_BF16 = 1,
   TC_EPI_INPROJ = 2,
   TC_EPI_RESID = 3,
-  TC_EPI_RESID_NORM = 4,
-  TC_EPI_INPROJ_CONV = 5
+  TC_EPI_RESID_NORM = 4
 };
 
 struct TcEpilogue {
@@ -51,15 +47,10 @@ struct TcEpilogue {
   int H;
   const float *dt_bias;
   float dt_lo, dt_hi;
-  const float *ssq;  // RESID_NORM: (M, ng) partial sums of u^2
+  const float *ssq;  // RESID_NORM: (ng, ssq_ld) partial sums of u^2, slice-major
   int ng;
+  long ssq_ld;
   float inv_d, eps;
-  // INPROJ_CONV
-  bf16 *act;            // (M, conv_dim) post-conv xBC
-  int d_inner, conv_dim, T;
-  const float *conv_w;  // (conv_dim, 4)
-  const float *conv_b;  // (conv_dim)
-  float *conv_tail;     // (M / T, conv_dim, 3)
   // F32 only: split-K.  ksplit > 1 cuts the K blocks into ksplit ranges (extra
   // tiles for small-M GEMMs, decode batches); range s writes its partial
   // product to C + s * split_stride, the consumer sums them in a fixed order.
@@ -67,10 +58,6 @@ struct TcEpilogue {
   long split_stride;
 };
 
-template <int EPI> struct TcRows {
-  static constexpr int STRIDE = EPI == TC_EPI_INPROJ_CONV ? 125 : 128;  // output rows per tile
-  static constexpr int HALO = 128 - STRIDE;
-};
 
 // PAIR: a CTA pair (cluster of 2, cta_group::2) computes a 256 x BN tile; each
 // CTA stages its 128 rows of A and half (BN / 2 rows) of B, the leader issues
@@ -185,7 +172,6 @@ __global__ void __launch_bounds__(320, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int M, int N, int K, TcEpilogue ep) {
   using Cfg = TcCfg<BN, PAIR>;
-  static_assert(!PAIR || (EPI != TC_EPI_INPROJ_CONV), "pair mode: no halo tiles");
   constexpr int BM = Cfg::BM, BK = Cfg::BK, STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned, derived from smem_raw by an offset so that the compiler
@@ -201,7 +187,7 @@ __global__ void __launch_bounds__(320, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int RSTRIDE = TcRows<EPI>::STRIDE, HALO = TcRows<EPI>::HALO;
+  constexpr int RSTRIDE = 128;  // output rows per tile
   // pair mode: tiles are 256 rows per cluster; rank r owns rows [128 r, 128 r + 128)
   const uint32_t rank = PAIR ? sm100::cluster_rank() : 0u;
   const int cta0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
@@ -212,7 +198,6 @@ __global__ void __launch_bounds__(320, 1)
   const int ksplit = (EPI == TC_EPI_F32 && ep.ksplit > 1) ? ep.ksplit : 1;
   const int num_tiles = num_mn * ksplit;
   const int num_kb = (K + BK - 1) / BK;
-  __shared__ float xch[2][2][4][3][32];  // INPROJ_CONV: [half][buf][quarter][row][col]
 
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tmA);
@@ -262,7 +247,7 @@ __global__ void __launch_bounds__(320, 1)
           } else {
           sm100::mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
           sm100::tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * BK,
-                             m_blk * RSTRIDE - HALO);
+                             m_blk * RSTRIDE);
           sm100::tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, &full[s], kb * BK, n_blk * BN);
           }
           if (++s == STAGES) {
@@ -329,14 +314,13 @@ __global__ void __launch_bounds__(320, 1)
       const int as = local & 1;
       const uint32_t aph = (local >> 1) & 1;
       const int i_row = q * 32 + lane;                 // tile row == TMEM lane
-      const int row0 = PAIR ? m_blk * 256 + (int)rank * 128 : m_blk * RSTRIDE - HALO;
-      const int m = row0 + i_row;                      // global row (HALO = 0: m_blk*128+i)
-      const bool out_row = i_row >= HALO && m < M;
+      const int row0 = PAIR ? m_blk * 256 + (int)rank * 128 : m_blk * RSTRIDE;
+      const int m = row0 + i_row;                      // global row
       // row-only inputs before the wait: the norm scale and the first residual chunk
       float rowscale = 1.f;
       if (EPI == TC_EPI_RESID_NORM && m < M) {
         float s = 0.f;
-        for (int gg = 0; gg < ep.ng; ++gg) s += ep.ssq[(size_t)m * ep.ng + gg];
+        for (int gg = 0; gg < ep.ng; ++gg) s += ep.ssq[(size_t)gg * ep.ssq_ld + m];
         rowscale = 1.f / sqrtf(s * ep.inv_d + ep.eps);
       }
       // transposed view of a 32 x 32 chunk: lanes 0-15 / 16-31 take rows 2i / 2i+1,
@@ -394,91 +378,7 @@ __global__ void __launch_bounds__(320, 1)
         uint32_t r[32];
         sm100::tmem_ld32(trow + cc, r);
         sm100::tmem_ld_wait();
-        if constexpr (EPI == TC_EPI_INPROJ_CONV) {
-          if (n0 >= ep.d_inner && n0 < ep.d_inner + ep.conv_dim) {
-            // ---- xBC chunk: causal k=4 conv + SiLU across rows (lanes)
-            const int xb = (cc >> 6) & 1;
-            if (lane >= 29) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) xch[half][xb][q][lane - 29][j] = __uint_as_float(r[j]);
-            }
-            asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
-            const int t = out_row ? m % ep.T : 0;
-            const int c0 = n0 - ep.d_inner;
-            uint32_t pk[16];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const float v = __uint_as_float(r[j]);
-              float h1 = __shfl_up_sync(0xffffffffu, v, 1);
-              float h2 = __shfl_up_sync(0xffffffffu, v, 2);
-              float h3 = __shfl_up_sync(0xffffffffu, v, 3);
-              if (lane < 3 && q > 0) {
-                const float p0 = xch[half][xb][q - 1][0][j];  // previous warp's lane 29
-                const float p1 = xch[half][xb][q - 1][1][j];  // lane 30
-                const float p2 = xch[half][xb][q - 1][2][j];  // lane 31
-                if (lane == 0) {
-                  h1 = p2;
-                  h2 = p1;
-                  h3 = p0;
-                } else if (lane == 1) {
-                  h2 = p2;
-                  h3 = p1;
-                } else {
-                  h3 = p2;
-                }
-              }
-              if (t < 1) h1 = 0.f;  // zero history before the sequence start
-              if (t < 2) h2 = 0.f;
-              if (t < 3) h3 = 0.f;
-              const float4 wc = reinterpret_cast<const float4 *>(ep.conv_w)[c0 + j];
-              const float a = wc.x * h3 + wc.y * h2 + wc.z * h1 + wc.w * v + ep.conv_b[c0 + j];
-              const float o = silu_fast(a);
-              if (j & 1)
-                pk[j >> 1] |= (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(o)) << 16;
-              else
-                pk[j >> 1] = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(o));
-            }
-            {  // post-conv xBC, stored row-contiguously through the transpose buffer
-#pragma unroll
-              for (int j = 0; j < 16; ++j) xpb[lane * 17 + j] = pk[j];
-              __syncwarp();
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                const int ir = q * 32 + 2 * i + tr, mr = m_w + 2 * i + tr;
-                if (ir >= HALO && mr < M)
-                  reinterpret_cast<uint32_t *>(ep.act + (size_t)mr * ep.conv_dim + c0)[tc] =
-                      xpb[(2 * i + tr) * 17 + tc];
-              }
-              __syncwarp();
-            }
-            if (out_row) {
-              if (t >= ep.T - 3) {  // pre-activation conv tail, newest last (model.py:144-147)
-                float *tail = ep.conv_tail + ((size_t)(m / ep.T) * ep.conv_dim + c0) * 3 +
-                              (t - (ep.T - 3));
-#pragma unroll
-                for (int j = 0; j < 32; ++j) tail[j * 3] = __uint_as_float(r[j]);
-              }
-            }
-          } else if (n0 + 32 <= ep.d_inner && vec_ok) {
-            // z columns (bf16), stored row-contiguously
-            bf16 *C = reinterpret_cast<bf16 *>(ep.C);
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              xpb[lane * 17 + j] = pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-            __syncwarp();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int ir = q * 32 + 2 * i + tr, mr = m_w + 2 * i + tr;
-              if (ir >= HALO && mr < M)
-                reinterpret_cast<uint32_t *>(C + (size_t)mr * ep.ldc + n0)[tc] =
-                    xpb[(2 * i + tr) * 17 + tc];
-            }
-            __syncwarp();
-          } else if (out_row) {
-            // dt columns (f32 softplus) and ragged z chunks, like TC_EPI_INPROJ
-            tc_store_chunk<TC_EPI_INPROJ>(ep, r, m, n0, N, 1.f);
-          }
-        } else if constexpr (RESID) {
+        if constexpr (RESID) {
           // hidden += acc * rowscale: f32 + bf16 shadow, stored row-contiguously
           float *C = reinterpret_cast<float *>(ep.C);
           if (rvec) {
@@ -551,8 +451,6 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) hv[j] = hn[j];
       }
-      if constexpr (EPI == TC_EPI_INPROJ_CONV)  // exchange buffers free for the next tile
-        asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) {

@@ -10,13 +10,15 @@ synchronisation until the tokens are read back.
 
 from __future__ import annotations
 
+import weakref
+
 import numpy as np
 import torch
 
 from . import _abi
 from .cache import GenerationResult, Mamba2Cache, state_dtype
 from .config import ModelConfig
-from .model import PolicyAudit, _audit, _Runner, check_tokens, layer_table, prefill
+from .model import PolicyAudit, _audit, _Runner, check_tokens, prefill
 from .params import ModelParams
 
 
@@ -25,31 +27,6 @@ def cache_init(cfg: ModelConfig, batch: int, device="cuda") -> Mamba2Cache:
     if batch < 1:
         raise ValueError("batch must be >= 1")
     return Mamba2Cache.empty(cfg, batch, device=device, zero=True)
-
-
-def _fused_step(r: _Runner, cfg, tok, cache: Mamba2Cache, logits, argmax, bar) -> bool:
-    """The whole step as one persistent kernel (ssd200_decode_step), cache
-    updated in place.  Returns False when the configuration is outside the
-    fused kernel's coverage (the caller then runs the per-layer sequence)."""
-    if cfg.policy.compute != "bf16" or tok.shape[0] > 8:
-        return False
-    B = tok.shape[0]
-    hidden = torch.empty((B, cfg.d_model), dtype=torch.float32, device=r.dev)
-    lp = torch.empty((B, cfg.d_model), dtype=torch.bfloat16, device=r.dev)
-    need = r.lib.ssd200_decode_step_workspace(r.dims, B)
-    ws = r.workspace(need)
-    rc = r.lib.ssd200_decode_step(
-        r.dims, layer_table(r.params).data_ptr(), cfg.n_layers, cfg.vocab_size,
-        r.params.embedding.data_ptr(), r.params.final_norm_w.data_ptr(), tok.data_ptr(),
-        hidden.data_ptr(), lp.data_ptr(), cache.ssm_all.data_ptr(),
-        cache.conv_all.data_ptr() if cache.conv_all.numel() else None,
-        _abi.ptr(logits), _abi.ptr(argmax), bar.data_ptr(), B, ws.data_ptr(), ws.numel(),
-        r.stream,
-    )
-    if rc == _abi.EUNSUPPORTED:
-        return False
-    _abi.check(rc, "ssd200_decode_step")
-    return True
 
 
 def _step_into(r: _Runner, cfg, tok, cache_in: Mamba2Cache, cache_out: Mamba2Cache,
@@ -88,9 +65,9 @@ class GreedyDecoder:
     token (and optionally the logits) at the device-side step counter."""
 
     def __init__(self, params: ModelParams, cfg: ModelConfig, cache: Mamba2Cache, gen_len: int,
-                 keep_logits: bool = False, use_graph: bool = True, fused: bool = True):
+                 keep_logits: bool = False, use_graph: bool = True):
         self.cfg = cfg
-        self.dev = params.device
+        self.dev = torch.device(params.device)
         B = cache.batch
         self.B = B
         self.cache = cache
@@ -104,18 +81,20 @@ class GreedyDecoder:
             else None
         )
         self.step_idx = torch.zeros((1,), dtype=torch.int64, device=self.dev)
-        self.bar = torch.zeros((2,), dtype=torch.int32, device=self.dev)  # grid-barrier state
         self.graph = None
         self.use_graph = use_graph
-        self.fused = fused
+
+    def nbytes(self) -> int:
+        """Device bytes this decoder keeps alive (cache + token / logits buffers)."""
+        n = self.cache.nbytes + self.tokens.numel() * 8 + self.logits.numel() * self.logits.element_size()
+        if self.kept is not None:
+            n += self.kept.numel() * self.kept.element_size()
+        return n
 
     def _body(self):
         cfg = self.cfg
-        done = self.fused and _fused_step(self.runner, cfg, self.tok, self.cache, self.logits,
-                                          self.tok, self.bar)
-        if not done:
-            _step_into(self.runner, cfg, self.tok, self.cache, self.cache, logits=self.logits,
-                       argmax=self.tok)
+        _step_into(self.runner, cfg, self.tok, self.cache, self.cache, logits=self.logits,
+                   argmax=self.tok)
         # bookkeeping: tokens[:, step] = tok; step += 1
         self.tokens.index_copy_(1, self.step_idx, self.tok.view(-1, 1))
         if self.kept is not None:
@@ -123,26 +102,27 @@ class GreedyDecoder:
         self.step_idx.add_(1)
 
     def capture(self):
-        # warm up once on a side stream (workspace allocation, attributes)
-        saved = (self.cache.copy(), self.tok.clone(), self.tokens.clone(), self.step_idx.clone())
-        s = torch.cuda.Stream(device=self.dev)
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            self.runner.stream = _abi.stream_handle(s)
-            self._body()
-        torch.cuda.current_stream().wait_stream(s)
-        # restore the state the warm-up step consumed
-        self.cache.ssm_all.copy_(saved[0].ssm_all)
-        self.cache.conv_all.copy_(saved[0].conv_all)
-        self.tok.copy_(saved[1])
-        self.tokens.copy_(saved[2])
-        self.step_idx.copy_(saved[3])
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self.runner.stream = _abi.stream_handle()
-            self._body()
-        self.graph = g
-        self.runner.stream = _abi.stream_handle()
+        with torch.cuda.device(self.dev):
+            # warm up once on a side stream (workspace allocation, attributes)
+            saved = (self.cache.copy(), self.tok.clone(), self.tokens.clone(), self.step_idx.clone())
+            s = torch.cuda.Stream(device=self.dev)
+            s.wait_stream(torch.cuda.current_stream(self.dev))
+            with torch.cuda.stream(s):
+                self.runner.stream = _abi.stream_handle(s)
+                self._body()
+            torch.cuda.current_stream(self.dev).wait_stream(s)
+            # restore the state the warm-up step consumed
+            self.cache.ssm_all.copy_(saved[0].ssm_all)
+            self.cache.conv_all.copy_(saved[0].conv_all)
+            self.tok.copy_(saved[1])
+            self.tokens.copy_(saved[2])
+            self.step_idx.copy_(saved[3])
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.runner.stream = _abi.stream_handle(torch.cuda.current_stream(self.dev))
+                self._body()
+            self.graph = g
+            self.runner.stream = _abi.stream_handle(torch.cuda.current_stream(self.dev))
 
     def step(self):
         if self.use_graph:
@@ -150,15 +130,21 @@ class GreedyDecoder:
                 self.capture()
             self.graph.replay()
         else:
-            self.runner.stream = _abi.stream_handle()
+            self.runner.stream = _abi.stream_handle(torch.cuda.current_stream(self.dev))
             self._body()
 
 
-# captured decode graphs kept across generate() calls (a capture costs ~100x a token step);
-# keyed by the parameters' identity, config, batch and length; only modest caches are kept
+# Captured decode graphs kept across generate() calls (a capture costs ~100x a
+# token step).  Keyed by the parameters' identity, config, batch and length;
+# the parameters are held weakly (an entry dies with its params).  Only
+# modest decoders are kept: each holds its own cache copy and token buffers
+# (counted against _GRAPH_CACHE_MAX_BYTES per entry and _GRAPH_CACHE_TOTAL_BYTES
+# overall); keep_logits runs are never cached (their (B, G, V) buffer is the
+# caller's result).  clear_graph_cache() drops everything.
 _GRAPH_CACHE: dict = {}
 _GRAPH_CACHE_MAX = 2
-_GRAPH_CACHE_MAX_BYTES = 8 << 30  # per entry: the decoder keeps its own copy of the cache
+_GRAPH_CACHE_MAX_BYTES = 8 << 30
+_GRAPH_CACHE_TOTAL_BYTES = 12 << 30
 
 
 def clear_graph_cache() -> None:
@@ -168,24 +154,27 @@ def clear_graph_cache() -> None:
 
 def _decoder_for(params: ModelParams, cfg: ModelConfig, cache: Mamba2Cache, gen_len: int,
                  keep_logits: bool, use_graph: bool) -> "GreedyDecoder":
-    nbytes = cache.ssm_all.numel() * cache.ssm_all.element_size() + \
-        cache.conv_all.numel() * cache.conv_all.element_size()
-    if not use_graph or nbytes > _GRAPH_CACHE_MAX_BYTES:
+    B = cache.batch
+    need = cache.nbytes + B * gen_len * 8 + B * cfg.vocab_size * 4
+    if not use_graph or keep_logits or need > _GRAPH_CACHE_MAX_BYTES:
         return GreedyDecoder(params, cfg, cache, gen_len, keep_logits=keep_logits,
                              use_graph=use_graph)
-    key = (id(params), cfg, cache.batch, gen_len, keep_logits, str(params.device))
+    key = (id(params), cfg, B, gen_len, str(params.device))
     hit = _GRAPH_CACHE.get(key)
-    if hit is not None and hit[0] is params:
+    if hit is not None and hit[0]() is params:
         dec = hit[1]
         dec.cache.ssm_all.copy_(cache.ssm_all)  # the graph's buffers take this prefill's state
         dec.cache.conv_all.copy_(cache.conv_all)
         dec.tokens.zero_()
         return dec
-    dec = GreedyDecoder(params, cfg, cache.copy(), gen_len, keep_logits=keep_logits,
-                        use_graph=True)
-    if len(_GRAPH_CACHE) >= _GRAPH_CACHE_MAX:
+    for k in [k for k, (ref, _) in _GRAPH_CACHE.items() if ref() is None]:
+        del _GRAPH_CACHE[k]  # entries whose params are gone
+    dec = GreedyDecoder(params, cfg, cache.copy(), gen_len, use_graph=True)
+    while _GRAPH_CACHE and (len(_GRAPH_CACHE) >= _GRAPH_CACHE_MAX or
+                            sum(d.nbytes() for _, d in _GRAPH_CACHE.values()) + dec.nbytes()
+                            > _GRAPH_CACHE_TOTAL_BYTES):
         _GRAPH_CACHE.pop(next(iter(_GRAPH_CACHE)))
-    _GRAPH_CACHE[key] = (params, dec)
+    _GRAPH_CACHE[key] = (weakref.ref(params), dec)
     return dec
 
 
@@ -195,7 +184,11 @@ def generate(params: ModelParams, prompt, gen_len: int, mode: str = "cached",
     """decode.py:147-194 — greedy generation of gen_len tokens after (B, P)
     prompt.  cached: one prefill then gen_len-1 in-place steps (graph
     replays); non_cached: re-prefill the whole prefix per token (the
-    quadratic baseline).  Ties resolve to the lowest id."""
+    quadratic baseline).  Ties resolve to the lowest id.
+
+    The captured decode graph is kept for the next call with the same params,
+    config, batch and gen_len (not for keep_logits runs; see _GRAPH_CACHE);
+    ``decode.clear_graph_cache()`` releases it."""
     if cfg is None:
         raise ValueError("cfg is required")
     if gen_len < 1:

@@ -5,6 +5,8 @@ calls onto one CUDA stream; every FLOP runs in libssd200.so.
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -28,10 +30,13 @@ class PolicyAudit:
 
 
 def dims_struct(cfg: ModelConfig) -> _abi.Dims:
+    """ssd200_dims_t for cfg; carries the implementation choices in scope
+    (``_abi.tuning(...)``), or NULL for the library defaults."""
     lo, hi = cfg.dt_limits
     if not (0 <= lo < hi):
         raise ValueError(f"need 0 <= dt_min < dt_max, got {cfg.dt_limits}")
-    return _abi.Dims(
+    tune = _abi.current_tuning()
+    d = _abi.Dims(
         dtype=_abi.DTYPE_CODE[cfg.policy.compute],
         d_model=cfg.d_model,
         d_inner=cfg.d_inner,
@@ -44,7 +49,10 @@ def dims_struct(cfg: ModelConfig) -> _abi.Dims:
         norm_eps=float(cfg.norm_eps),
         dt_min=float(lo),
         dt_max=float(hi),
+        tuning=ctypes.pointer(tune) if tune is not None else None,
     )
+    d._keep = tune  # the struct points at it
+    return d
 
 
 def layer_struct(lp: LayerParams) -> _abi.Layer:
@@ -61,18 +69,6 @@ def layer_struct(lp: LayerParams) -> _abi.Layer:
     )
 
 
-def layer_table(params: ModelParams) -> torch.Tensor:
-    """Device array of ssd200_layer_t (one per layer) for the fused decode
-    step; built once per ModelParams."""
-    tab = getattr(params, "_layer_table", None)
-    if tab is None:
-        arr = (_abi.Layer * len(params.layers))(*[layer_struct(lp) for lp in params.layers])
-        raw = bytes(arr)
-        tab = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(params.device)
-        params._layer_table = tab
-    return tab
-
-
 def _audit(audit, cfg):
     if audit is not None:
         audit.record("decay_exp", "bf16e" if cfg.policy.bf16_decay else cfg.dtype)
@@ -80,7 +76,12 @@ def _audit(audit, cfg):
 
 
 def check_tokens(tokens, cfg: ModelConfig, ndim: int, device) -> torch.Tensor:
-    """model.py:191-195 / decode.py:88-92 validation, then upload as int64."""
+    """model.py:191-195 / decode.py:88-92 validation, then upload as int64.
+
+    Host ids (numpy, lists, CPU tensors) are range-checked here and raise
+    ValueError like the reference.  Ids already on the device are not read
+    back (no host sync on the hot path): the embedding kernel checks them and
+    an id outside [0, vocab) yields a NaN row instead of an out-of-bounds read."""
     if isinstance(tokens, torch.Tensor):
         t = tokens
     else:
@@ -92,9 +93,15 @@ def check_tokens(tokens, cfg: ModelConfig, ndim: int, device) -> torch.Tensor:
         raise ValueError(f"token must be (B,), got shape {shape}")
     if t.numel() == 0:
         raise ValueError("empty token array")
-    lo, hi = int(t.min()), int(t.max())
-    if lo < 0 or hi >= cfg.vocab_size:
-        raise ValueError("token id out of range")
+    if t.dtype.is_floating_point or t.dtype == torch.bool:
+        raise ValueError(f"token ids must be integers, got {t.dtype}")
+    if not t.is_cuda:
+        lo, hi = int(t.min()), int(t.max())
+        if lo < 0 or hi >= cfg.vocab_size:
+            raise ValueError("token id out of range")
+        if t.dtype != torch.int64:
+            t = t.to(torch.int64)
+        return t.contiguous().to(device=device, non_blocking=t.is_pinned())
     return t.to(device=device, dtype=torch.int64).contiguous()
 
 
@@ -108,10 +115,12 @@ class _Runner:
             )
         self.cfg = cfg
         self.params = params
-        self.dev = params.device
+        self.dev = torch.device(params.device)
         self.dims = dims_struct(cfg)
         self.lib = _abi.lib()
-        self.stream = _abi.stream_handle()
+        # the caller's current stream ON THE PARAMS' DEVICE; every ABI call runs
+        # under a device guard so the library's per-device state matches
+        self.stream = _abi.stream_handle(torch.cuda.current_stream(self.dev))
         self.sdt = state_dtype(cfg)
         self._ws = None
         self._layers = [layer_struct(lp) for lp in params.layers]
@@ -132,58 +141,39 @@ class _Runner:
             if cfg.policy.compute == "bf16"
             else None
         )
-        _abi.check(
-            self.lib.ssd200_embed(
-                self.dims, tok.data_ptr(), rows, self.params.embedding.data_ptr(),
-                hidden.data_ptr(), _abi.ptr(lp), self.stream,
-            ),
-            "ssd200_embed",
-        )
+        self._call("ssd200_embed", self.lib.ssd200_embed, self.dims, tok.data_ptr(), rows,
+                   cfg.vocab_size, self.params.embedding.data_ptr(), hidden.data_ptr(),
+                   _abi.ptr(lp), self.stream)
         return hidden, lp
 
+    def _call(self, what, fn, *args):
+        with torch.cuda.device(self.dev):
+            _abi.check(fn(*args), what)
+
     def prefill_layer(self, i, hidden, hidden_lp, ssm_out, conv_out, B, T):
-        need = self.lib.ssd200_prefill_layer_workspace(self.dims, B, T)
-        ws = self.workspace(need)
-        _abi.check(
-            self.lib.ssd200_prefill_layer(
-                self.dims, self._layers[i], hidden.data_ptr(), _abi.ptr(hidden_lp),
-                ssm_out.data_ptr(), _abi.ptr(conv_out) if conv_out.numel() else None,
-                B, T, ws.data_ptr(), ws.numel(), self.stream,
-            ),
-            "ssd200_prefill_layer",
-        )
+        ws = self.workspace(self.lib.ssd200_prefill_layer_workspace(self.dims, B, T))
+        self._call("ssd200_prefill_layer", self.lib.ssd200_prefill_layer, self.dims,
+                   self._layers[i], hidden.data_ptr(), _abi.ptr(hidden_lp), ssm_out.data_ptr(),
+                   _abi.ptr(conv_out) if conv_out.numel() else None, B, T, ws.data_ptr(),
+                   ws.numel(), self.stream)
 
     def decode_layer(self, i, hidden, hidden_lp, ssm_in, ssm_out, conv_in, conv_out, B):
-        need = self.lib.ssd200_decode_layer_workspace(self.dims, B)
-        ws = self.workspace(need)
+        ws = self.workspace(self.lib.ssd200_decode_layer_workspace(self.dims, B))
         has_conv = conv_in.numel() > 0
-        if i + 1 < len(self.params.layers):  # L2 warm-up hint (used when option 22 has bit 2)
-            nxt = self.params.layers[i + 1].W_in
-            self.lib.ssd200_decode_prefetch_next(nxt.data_ptr(), nxt.numel() * nxt.element_size())
-        _abi.check(
-            self.lib.ssd200_decode_layer(
-                self.dims, self._layers[i], hidden.data_ptr(), _abi.ptr(hidden_lp),
-                ssm_in.data_ptr(), ssm_out.data_ptr(),
-                conv_in.data_ptr() if has_conv else None,
-                conv_out.data_ptr() if has_conv else None,
-                B, ws.data_ptr(), ws.numel(), self.stream,
-            ),
-            "ssd200_decode_layer",
-        )
+        self._call("ssd200_decode_layer", self.lib.ssd200_decode_layer, self.dims,
+                   self._layers[i], hidden.data_ptr(), _abi.ptr(hidden_lp), ssm_in.data_ptr(),
+                   ssm_out.data_ptr(), conv_in.data_ptr() if has_conv else None,
+                   conv_out.data_ptr() if has_conv else None, B, ws.data_ptr(), ws.numel(),
+                   self.stream)
 
     def head(self, hidden, row_stride, rows, logits=None, argmax=None, base_offset=0):
         cfg = self.cfg
-        need = self.lib.ssd200_head_workspace(self.dims, cfg.vocab_size, rows)
-        ws = self.workspace(need)
+        ws = self.workspace(self.lib.ssd200_head_workspace(self.dims, cfg.vocab_size, rows))
         hptr = hidden.data_ptr() + base_offset * hidden.element_size()
-        _abi.check(
-            self.lib.ssd200_head(
-                self.dims, cfg.vocab_size, hptr, row_stride,
-                self.params.final_norm_w.data_ptr(), self.params.embedding.data_ptr(),
-                _abi.ptr(logits), _abi.ptr(argmax), rows, ws.data_ptr(), ws.numel(), self.stream,
-            ),
-            "ssd200_head",
-        )
+        self._call("ssd200_head", self.lib.ssd200_head, self.dims, cfg.vocab_size, hptr,
+                   row_stride, self.params.final_norm_w.data_ptr(),
+                   self.params.embedding.data_ptr(), _abi.ptr(logits), _abi.ptr(argmax), rows,
+                   ws.data_ptr(), ws.numel(), self.stream)
 
 
 def _as_hidden(hidden, cfg, dev):

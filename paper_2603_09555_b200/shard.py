@@ -310,6 +310,11 @@ class HeadShardedDecoder:
         self.buf = torch.empty((self.B, self.ld), dtype=torch.float32, device=r.dev)
         self.ws = r.workspace(r.lib.ssd200_decode_layer_workspace(self.dims_l, self.B))
         self.hidden = self.lp = None
+        # fixed buffers for the graph-captured step (HeadShardedGraphDecoder)
+        self.tok = torch.zeros((self.B,), dtype=torch.int64, device=r.dev)
+        self.logits = torch.empty((self.B, cfg.vocab_size), dtype=torch.float32, device=r.dev)
+        self._hid = torch.empty((self.B, cfg.d_model), dtype=torch.float32, device=r.dev)
+        self._lp = torch.empty((self.B, cfg.d_model), dtype=torch.bfloat16, device=r.dev)
 
     @classmethod
     def from_prefill(cls, run: "HeadShardedPrefill"):
@@ -318,6 +323,18 @@ class HeadShardedDecoder:
     def begin(self, tok: torch.Tensor):
         """Embed this step's tokens (B,) — replicated on every rank."""
         self.hidden, self.lp = self.r.embed(tok.reshape(-1))
+
+    def begin_fixed(self):
+        """Embed ``self.tok`` into the decoder's fixed hidden buffers (graph step)."""
+        cfg, r = self.cfg, self.r
+        r._call("ssd200_embed", r.lib.ssd200_embed, r.dims, self.tok.data_ptr(), self.B,
+                cfg.vocab_size, self.params.embedding.data_ptr(), self._hid.data_ptr(),
+                self._lp.data_ptr(), r.stream)
+        self.hidden, self.lp = self._hid, self._lp
+
+    def head_fixed(self):
+        """Final norm + tied head into ``self.logits``, greedy pick into ``self.tok``."""
+        self.r.head(self.hidden, self.cfg.d_model, self.B, logits=self.logits, argmax=self.tok)
 
     def partial(self, i: int) -> torch.Tensor:
         from . import _abi
@@ -354,30 +371,138 @@ class HeadShardedDecoder:
         return out, pick
 
 
-def generate_head_sharded(shard_params, prompt, gen_len: int, cfg: ModelConfig, group=None):
+def sum_reduce(bufs) -> None:
+    """The all-reduce of simulated ranks living in one process: every buffer
+    becomes the sum over the ranks, added in rank order (a fixed order, so the
+    result is deterministic)."""
+    total = bufs[0].clone()
+    for b in bufs[1:]:
+        total.add_(b)
+    for b in bufs:
+        b.copy_(total)
+
+
+def nccl_reduce(group=None):
+    """The all-reduce of one rank per process: NCCL (sum) on the caller's
+    stream, capturable in a CUDA graph."""
+    import torch.distributed as dist
+
+    def reduce(bufs):
+        for b in bufs:
+            dist.all_reduce(b, op=dist.ReduceOp.SUM, group=group)
+
+    return reduce
+
+
+class HeadShardedGraphDecoder:
+    """Head-group-sharded greedy decoding with the WHOLE token step captured as
+    one CUDA graph: embed -> per layer [every local rank's
+    ``ssd200_decode_layer_partial`` -> reduce of ``[partial | sum u^2]`` ->
+    ``ssd200_resid_norm_finish``] -> final norm + tied head + argmax -> token
+    feedback, replayed once per token with no return to Python in between
+    (the collective stays inside the captured step).
+
+    ``ranks``: the HeadShardedDecoder(s) this process drives — one per GPU in
+    a real run (``reduce = nccl_reduce(group)``; NCCL kernels are captured
+    into the graph) or several on one device to simulate ranks (``reduce =
+    sum_reduce``).  ``reduce=None`` is the single-rank case (no collective)."""
+
+    def __init__(self, ranks, gen_len: int, reduce=None, use_graph: bool = True):
+        self.ranks = list(ranks)
+        self.reduce = reduce
+        d0 = self.ranks[0]
+        self.cfg, self.B, self.dev = d0.cfg, d0.B, d0.r.dev
+        self.tokens = torch.zeros((self.B, gen_len), dtype=torch.int64, device=self.dev)
+        self.step_idx = torch.zeros((1,), dtype=torch.int64, device=self.dev)
+        self.use_graph = use_graph
+        self.graph = None
+
+    def set_token(self, tok: torch.Tensor) -> None:
+        for d in self.ranks:
+            d.tok.copy_(tok)
+
+    def _set_stream(self, stream):
+        for d in self.ranks:
+            d.r.stream = stream
+
+    def _body(self):
+        for d in self.ranks:
+            d.begin_fixed()
+        for i in range(self.cfg.n_layers):
+            for d in self.ranks:
+                d.partial(i)
+            if self.reduce is not None:
+                self.reduce([d.buf for d in self.ranks])
+            for d in self.ranks:
+                d.finish()
+        for d in self.ranks:
+            d.head_fixed()
+        self.tokens.index_copy_(1, self.step_idx, self.ranks[0].tok.view(-1, 1))
+        self.step_idx.add_(1)
+
+    def capture(self):
+        from . import _abi
+
+        with torch.cuda.device(self.dev):
+            saved = ([(d.ssm.clone(), d.conv.clone(), d.tok.clone()) for d in self.ranks],
+                     self.tokens.clone(), self.step_idx.clone())
+            side = torch.cuda.Stream(device=self.dev)
+            side.wait_stream(torch.cuda.current_stream(self.dev))
+            with torch.cuda.stream(side):  # warm-up: workspaces, attributes, NCCL setup
+                self._set_stream(_abi.stream_handle(side))
+                self._body()
+            torch.cuda.current_stream(self.dev).wait_stream(side)
+            for d, (ssm, conv, tok) in zip(self.ranks, saved[0]):
+                d.ssm.copy_(ssm)
+                d.conv.copy_(conv)
+                d.tok.copy_(tok)
+            self.tokens.copy_(saved[1])
+            self.step_idx.copy_(saved[2])
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._set_stream(_abi.stream_handle(torch.cuda.current_stream(self.dev)))
+                self._body()
+            self.graph = g
+            self._set_stream(_abi.stream_handle(torch.cuda.current_stream(self.dev)))
+
+    def step(self):
+        from . import _abi
+
+        if not self.use_graph:
+            self._set_stream(_abi.stream_handle(torch.cuda.current_stream(self.dev)))
+            self._body()
+            return
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+
+
+def generate_head_sharded(shard_params, prompt, gen_len: int, cfg: ModelConfig, group=None,
+                          use_graph: bool = True):
     """Head-group-sharded cached ``generate`` (decode.py:147-194) for this rank:
-    a head-sharded prefill of the prompt, then gen_len - 1 decode steps; per
-    layer of every step ONE all-reduce (sum) of ``[partial | sum u^2]``.
-    Returns the (B, gen_len) greedy tokens (replicated on every rank)."""
+    a head-sharded prefill of the prompt (one all-reduce per layer), then
+    gen_len - 1 token steps replayed as ONE captured CUDA graph each
+    (HeadShardedGraphDecoder: the per-layer NCCL all-reduce is inside the
+    graph).  Returns the (B, gen_len) greedy tokens (replicated on every rank)."""
     import torch.distributed as dist
 
     if gen_len < 1:
         raise ValueError("gen_len must be >= 1")
     run = HeadShardedPrefill(shard_params, prompt, cfg)
+    multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
     for i in range(cfg.n_layers):
         buf = run.partial(i)
-        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+        if multi:
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
         run.finish()
     tok = torch.empty((run.B,), dtype=torch.int64, device=run.r.dev)
     run.logits(argmax=tok)  # greedy pick, ties -> lowest id (decode.py:72-74)
-    tokens = [tok]
-    dec = HeadShardedDecoder.from_prefill(run)
+    dec = HeadShardedGraphDecoder([HeadShardedDecoder.from_prefill(run)], gen_len,
+                                  reduce=nccl_reduce(group) if multi else None,
+                                  use_graph=use_graph)
+    dec.set_token(tok)
+    dec.tokens[:, 0] = tok
+    dec.step_idx.fill_(1)
     for _ in range(gen_len - 1):
-        dec.begin(tok)
-        for i in range(cfg.n_layers):
-            buf = dec.partial(i)
-            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
-            dec.finish()
-        _, tok = dec.logits_and_pick()
-        tokens.append(tok)
-    return torch.stack(tokens, dim=1)
+        dec.step()
+    return dec.tokens.clone()

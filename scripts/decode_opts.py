@@ -1,6 +1,8 @@
 """Decode step time under library options (tuning sweeps).
 
-    python scripts/decode_opts.py --batch 64 --set "" --set "8=0" --set "6=1,7=1"
+    python scripts/decode_opts.py --batch 64 --set "" --set "dec_pdl=0" --set "dec_split_in=1,dec_split_out=1"
+
+(fields of ssd200_tuning_t, passed per call through _abi.tuning)
 """
 
 from __future__ import annotations
@@ -27,20 +29,18 @@ def main():
     args = ap.parse_args()
     cfg = m.named_config(args.model, compute="bf16")
     params = m.synthetic_init(cfg, seed=0)
-    defaults = {6: 0, 7: 0, 8: 1, 9: 0, 11: 0, 12: 0, 13: 8, 14: 1, 15: 1, 16: 0, 17: -1, 22: 0, 23: 48}
     for B in args.batch or [64]:
         prompt = torch.randint(0, cfg.vocab_size, (B, 16), device="cuda")
         _, cache = m.prefill(params, prompt, cfg, logits=None)
         for spec in args.set or [""]:
-            opts = dict(defaults)
+            opts = {}
             for kv in filter(None, spec.split(",")):
                 k, v = kv.split("=")
-                opts[int(k)] = int(v)
-            for k, v in opts.items():
-                _abi.lib().ssd200_set_option(k, v)
-            dec = m.GreedyDecoder(params, cfg, cache, args.steps + 8)
-            for _ in range(3):
-                dec.step()
+                opts[k] = int(v)
+            with _abi.tuning(**opts):  # the graph captures the tuned launches
+                dec = m.GreedyDecoder(params, cfg, cache, args.steps + 8)
+                for _ in range(3):
+                    dec.step()
             torch.cuda.synchronize()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
@@ -53,8 +53,6 @@ def main():
             print(f"B={B:4d} opts[{spec or 'default':>12s}] {ms:8.3f} ms/step  {gbs:7.0f} GB/s",
                   flush=True)
             del dec
-        for k, v in defaults.items():
-            _abi.lib().ssd200_set_option(k, v)
 
 
 if __name__ == "__main__":

@@ -27,13 +27,16 @@ def main():
     ap.add_argument("--batch", type=int, default=4)
     ap.add_argument("--seqlen", type=int, default=8192)
     ap.add_argument("--iters", type=int, default=3)
-    ap.add_argument("--opt", action="append", default=[], help="ssd200_set_option k=v")
+    ap.add_argument("--opt", action="append", default=[], help="ssd200_tuning_t field=value")
     args = ap.parse_args()
     from paper_2603_09555_b200 import _abi
 
-    for kv in args.opt:
-        k, v = kv.split("=")
-        _abi.lib().ssd200_set_option(int(k), int(v))
+    opts = dict(kv.split("=") for kv in args.opt)
+    with _abi.tuning(**opts):
+        run(args)
+
+
+def run(args):
     cfg = m.named_config(args.model, compute="bf16", n_layers=args.layers)
     params = m.synthetic_init(cfg, seed=0)
     if args.what == "prefill":

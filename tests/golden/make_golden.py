@@ -140,6 +140,9 @@ def gen_small_model():
     np.savez_compressed(os.path.join(HERE, "small_model.npz"), **out)
 
 
+C1_TAP_ROWS = [0, 1, 127, 255, 256, 383, 510, 511]
+
+
 def c1_config() -> ModelConfig:
     return ModelConfig(vocab_size=50288, d_model=768, n_layers=24)
 
@@ -165,6 +168,28 @@ def gen_c1():
     out["layer0_hidden_rows"] = h1[0, [0, 1, 255, 256, 510, 511]].astype(np.float32)
     out["layer0_state_head0"] = s1[0, 0].astype(np.float32)
     out["layer0_conv_tail"] = c1[0].astype(np.float32)
+    # the residual stream after every layer (model.py:198-203 re-run block by
+    # block): sampled rows (chunk edges included) + full-tensor norm and sum
+    h = hidden0
+    rows, norms, sums = [], [], []
+    for lyr in params.layers:
+        h, _, _ = se.block_forward(lyr, h, cfg)
+        rows.append(h[0, C1_TAP_ROWS].astype(np.float32))
+        norms.append(float(np.linalg.norm(h)))
+        sums.append(float(h.sum(dtype=np.float64)))
+    out["tap_rows"] = np.stack(rows)
+    out["tap_norm"] = np.asarray(norms)
+    out["tap_sum"] = np.asarray(sums)
+    # bf16 mode: the reference on the SAME bf16-rounded weights,
+    # f32 compute: greedy tokens + the first step's logits
+    pb = se.random_init(cfg, 0)
+    rne = lambda a: se.numerics.bf16_round(a).astype(a.dtype)  # noqa: E731
+    for lyr in pb.layers:
+        lyr.W_in, lyr.W_out = rne(lyr.W_in), rne(lyr.W_out)
+    pb.embedding = rne(pb.embedding)
+    rb = se.generate(pb, prompt, 65, mode="cached", cfg=cfg, keep_logits=True)
+    out["bf16w_tokens"] = rb.tokens
+    out["bf16w_logits_first"] = rb.per_step_logits[0, 0].astype(np.float32)
     np.savez_compressed(os.path.join(HERE, "c1_130m.npz"), **out)
     print(f"c1 golden in {time.perf_counter() - t0:.1f}s tokens={res.tokens[0, :8]}...")
 

@@ -35,7 +35,7 @@ def test_abi_version_and_error_path_without_gpu():
     from paper_2603_09555_b200 import _abi
 
     lib = _abi.lib()
-    assert lib.ssd200_abi_version() == 1
+    assert lib.ssd200_abi_version() == 2
     # argument validation happens before any CUDA call
     rc = lib.ssd200_chunk_scan(0, None, None, None, None, None, None, None, None, None,
                                1, 1, 1, 1, 1, 1, 1, None, 0, None)
@@ -43,6 +43,33 @@ def test_abi_version_and_error_path_without_gpu():
     assert "null pointer" in _abi.last_error()
     with pytest.raises(ValueError):
         _abi.check(rc, "probe")
+
+
+def test_tuning_is_per_call_not_global():
+    """Implementation choices travel inside ssd200_dims_t (no library option
+    state): a scoped override changes only the calls made with it."""
+    from paper_2603_09555_b200 import _abi, named_config
+    from paper_2603_09555_b200.model import dims_struct
+
+    lib = _abi.lib()
+    t = _abi.default_tuning()
+    assert t.size == ctypes.sizeof(_abi.Tuning)
+    assert (t.gemm_pair, t.prefill_pdl, t.dec_small_ring, t.stream_cw) == (1, 1, -1, 8)
+    cfg = named_config("1.3b")
+    base = lib.ssd200_decode_layer_workspace(dims_struct(cfg), 8)
+    with _abi.tuning(dec_split_in=1, dec_split_out=1):
+        d1 = dims_struct(cfg)
+        assert d1.tuning and d1.tuning.contents.dec_split_in == 1
+        small = lib.ssd200_decode_layer_workspace(d1, 8)
+        # the defaults are unchanged for a call made without the override
+        assert lib.ssd200_decode_layer_workspace(dims_struct(cfg).__class__(
+            **{f: getattr(d1, f) for f, _ in d1._fields_ if f != "tuning"}), 8) == base
+    assert small < base  # split-K 1 needs fewer partial buffers
+    assert not dims_struct(cfg).tuning  # scope ended: NULL = library defaults
+    assert lib.ssd200_decode_layer_workspace(dims_struct(cfg), 8) == base
+    with pytest.raises(ValueError):
+        with _abi.tuning(no_such_field=1):
+            pass
 
 
 def test_workspace_queries_are_pure_host():
