@@ -162,6 +162,18 @@ int ssd200_decode_layer(const ssd200_dims_t *d, const ssd200_layer_t *w, void *h
                         void *conv_out, int batch, void *workspace, size_t workspace_bytes,
                         ssd200_stream_t stream);
 
+/* ---- every layer of one decode_step (decode.py:99-140) ---------------------
+ * layers: HOST array of n_layers ssd200_layer_t.  ssm (n_layers, batch, H, P, N)
+ * and conv (n_layers, batch, conv_dim, k-1) contiguous; out may alias in.
+ * hidden / hidden_lp hold the embedded tokens on entry and the residual stream
+ * after the last layer on return (ssd200_decode_layer per layer, one ABI call
+ * per token step).  Workspace: ssd200_decode_layers_workspace. */
+size_t ssd200_decode_layers_workspace(const ssd200_dims_t *d, int batch);
+int ssd200_decode_layers(const ssd200_dims_t *d, const ssd200_layer_t *layers, int n_layers,
+                         void *hidden, void *hidden_lp, const void *ssm_in, void *ssm_out,
+                         const void *conv_in, void *conv_out, int batch, void *workspace,
+                         size_t workspace_bytes, ssd200_stream_t stream);
+
 /* ---- final RMSNorm + tied head (+ greedy argmax) (model.py:204-205,
  * decode.py:72-74,142-143) -------------------------------------------------
  * Reads `rows` rows of hidden spaced hidden_row_stride elements apart.

@@ -106,6 +106,12 @@ SIGNATURES = [
         c_int,
         [ctypes.POINTER(Dims), ctypes.POINTER(Layer)] + [c_void_p] * 6 + [c_int, c_void_p, c_size_t, c_void_p],
     ),
+    ("ssd200_decode_layers_workspace", c_size_t, [ctypes.POINTER(Dims), c_int]),
+    (
+        "ssd200_decode_layers",
+        c_int,
+        [ctypes.POINTER(Dims), ctypes.POINTER(Layer), c_int] + [c_void_p] * 6 + [c_int, c_void_p, c_size_t, c_void_p],
+    ),
     ("ssd200_head_workspace", c_size_t, [ctypes.POINTER(Dims), c_int, c_int]),
     (
         "ssd200_head",

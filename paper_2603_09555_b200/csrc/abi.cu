@@ -1058,6 +1058,7 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   fa.H = d->n_heads;
   fa.inv_d = 1.f / (float)d->d_inner;
   fa.eps = (float)d->norm_eps;
+  fa.hidden_in = hidden;
   fa.hidden = hidden;
   fa.lp = hidden_lp;
   fa.d_model = d->d_model;
@@ -1467,6 +1468,36 @@ int ssd200_decode_layer(const ssd200_dims_t *d, const ssd200_layer_t *w, void *h
                                   (const float *)ssm_in, (float *)ssm_out,
                                   (const float *)conv_in, (float *)conv_out, batch, workspace,
                                   workspace_bytes, st);
+}
+
+size_t ssd200_decode_layers_workspace(const ssd200_dims_t *d, int batch) {
+  return ssd200_decode_layer_workspace(d, batch);
+}
+
+int ssd200_decode_layers(const ssd200_dims_t *d, const ssd200_layer_t *layers, int n_layers,
+                         void *hidden, void *hidden_lp, const void *ssm_in, void *ssm_out,
+                         const void *conv_in, void *conv_out, int batch, void *workspace,
+                         size_t workspace_bytes, ssd200_stream_t stream) {
+  TuneScope scope(d);
+  int rc = check_dims(d);
+  if (rc) return rc;
+  REQUIRE(layers && n_layers >= 1 && hidden && ssm_in && ssm_out && batch >= 1, SSD200_EINVAL,
+          "decode_layers: bad arguments");
+  REQUIRE(d->conv_kernel == 1 || (conv_in && conv_out), SSD200_EINVAL,
+          "decode_layers: conv state is null");
+  const Widths wd = widths(d);
+  const size_t esz = d->dtype == SSD200_F64 ? 8 : 4;
+  const size_t ss = (size_t)batch * d->n_heads * d->head_dim * d->d_state * esz;
+  const size_t cs = (size_t)batch * wd.conv_dim * (d->conv_kernel - 1) * esz;
+  const char *si = static_cast<const char *>(ssm_in), *ci = static_cast<const char *>(conv_in);
+  char *so = static_cast<char *>(ssm_out), *co = static_cast<char *>(conv_out);
+  for (int i = 0; i < n_layers; ++i) {
+    rc = ssd200_decode_layer(d, &layers[i], hidden, hidden_lp, si + i * ss, so + i * ss,
+                             ci ? ci + i * cs : nullptr, co ? co + i * cs : nullptr, batch,
+                             workspace, workspace_bytes, stream);
+    if (rc) return rc;
+  }
+  return SSD200_OK;
 }
 
 size_t ssd200_head_workspace(const ssd200_dims_t *d, int vocab, int rows) {

@@ -392,6 +392,7 @@ struct DecFinishArgs {
   const float *ssq;   // (B, H)
   int H;
   float inv_d, eps;
+  const float *hidden_in;  // residual before this update (may alias hidden)
   float *hidden;
   bf16 *lp;
   int d_model;
@@ -412,10 +413,9 @@ __global__ __launch_bounds__(256) void dec_out_finish(DecFinishArgs a) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = (int)blockIdx.x < nb_h && n < a.d_model;
   const long i = (long)b * a.d_model + n;
-  // the residual was written a layer ago (every PDL predecessor has completed it)
-  const float hold = (live && !a.pout) ? a.hidden[i] : 0.f;
-  griddep_wait();
+  griddep_wait();  // the residual, the partials and sum u^2 are all predecessor outputs
   griddep_launch();
+  const float hold = (live && !a.pout) ? a.hidden_in[i] : 0.f;
   if ((int)blockIdx.x >= nb_h) {
     const int c = a.d_inner + ((int)blockIdx.x - nb_h) * 256 + threadIdx.x;  // B / C channel
     if (c >= a.conv_dim) return;

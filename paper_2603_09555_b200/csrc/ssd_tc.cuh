@@ -503,17 +503,20 @@ __global__ void __launch_bounds__(CHUNKSCAN_THREADS, 1)
       const int l = tid;
       const __nv_bfloat162 w2 = __float2bfloat162_rn(f.dt * ex2((f.cend - f.cs) * kLog2e));
       uint4 *row = reinterpret_cast<uint4 *>(xb + l * 128);
+      // every 16-byte chunk of the row gets the same weight, so visit them in a
+      // lane-rotated order (the 8 lanes of a shared-memory phase hit 8 bank
+      // groups); all 8 loads are issued before the first multiply
+      uint4 v[8];
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) v[ch] = row[(ch + l) & 7];
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {  // packed bf16 multiply (X is a bf16 MMA operand)
-        // every 16-byte chunk of the row gets the same weight, so visit them in a
-        // lane-rotated order: the 8 lanes of a shared-memory phase hit 8 bank groups
-        const int pc = (ch + l) & 7;
-        uint4 v = row[pc];
-        __nv_bfloat162 *e = reinterpret_cast<__nv_bfloat162 *>(&v);
+        __nv_bfloat162 *e = reinterpret_cast<__nv_bfloat162 *>(&v[ch]);
 #pragma unroll
         for (int j = 0; j < 4; ++j) e[j] = __hmul2(e[j], w2);
-        row[pc] = v;
       }
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) row[(ch + l) & 7] = v[ch];
       sm100::fence_proxy_async();
       sm100::mbar_arrive(&xsd[st]);
     };
@@ -529,7 +532,10 @@ __global__ void __launch_bounds__(CHUNKSCAN_THREADS, 1)
     load_w(1, wb);
     scale(0, wa);
     load_w(2, wa);
+    float dnext = ceg[0];  // e^{cs_end} decay of the next chunk, loaded one chunk ahead
     for (int c = 0; c < Nc; ++c) {
+      const float dlog = dnext;
+      if (c + 1 < Nc) dnext = ceg[c + 1];
       if (c + 1 < Nc) {
         const int k = c + 1;
         if (k & 1) {
@@ -541,7 +547,7 @@ __global__ void __launch_bounds__(CHUNKSCAN_THREADS, 1)
         }
       }
       const int st = c & 1;
-      const float decay = expf(ceg[c]);
+      const float decay = expf(dlog);
       sm100::mbar_wait(&sfull[st], (c >> 1) & 1);
       sm100::tc_fence_after();
       uint32_t r0[32];

@@ -30,14 +30,18 @@ def cache_init(cfg: ModelConfig, batch: int, device="cuda") -> Mamba2Cache:
 
 
 def _step_into(r: _Runner, cfg, tok, cache_in: Mamba2Cache, cache_out: Mamba2Cache,
-               logits=None, argmax=None):
+               logits=None, argmax=None, chained: bool = True):
     B = tok.shape[0]
     hidden, lp = r.embed(tok)
-    for i in range(cfg.n_layers):
-        r.decode_layer(
-            i, hidden, lp, cache_in.ssm_all[i], cache_out.ssm_all[i],
-            cache_in.conv_all[i], cache_out.conv_all[i], B,
-        )
+    if chained:  # all layers in one call (bf16: each in_proj applies the previous update)
+        r.decode_layers(hidden, lp, cache_in.ssm_all, cache_out.ssm_all, cache_in.conv_all,
+                        cache_out.conv_all, B)
+    else:
+        for i in range(cfg.n_layers):
+            r.decode_layer(
+                i, hidden, lp, cache_in.ssm_all[i], cache_out.ssm_all[i],
+                cache_in.conv_all[i], cache_out.conv_all[i], B,
+            )
     r.head(hidden, cfg.d_model, B, logits=logits, argmax=argmax)
 
 

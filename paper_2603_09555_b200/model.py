@@ -124,6 +124,7 @@ class _Runner:
         self.sdt = state_dtype(cfg)
         self._ws = None
         self._layers = [layer_struct(lp) for lp in params.layers]
+        self._layer_arr = (_abi.Layer * len(self._layers))(*self._layers)
 
     def workspace(self, nbytes: int) -> torch.Tensor:
         if self._ws is None or self._ws.numel() < nbytes:
@@ -163,6 +164,17 @@ class _Runner:
         self._call("ssd200_decode_layer", self.lib.ssd200_decode_layer, self.dims,
                    self._layers[i], hidden.data_ptr(), _abi.ptr(hidden_lp), ssm_in.data_ptr(),
                    ssm_out.data_ptr(), conv_in.data_ptr() if has_conv else None,
+                   conv_out.data_ptr() if has_conv else None, B, ws.data_ptr(), ws.numel(),
+                   self.stream)
+
+    def decode_layers(self, hidden, hidden_lp, ssm_in, ssm_out, conv_in, conv_out, B):
+        """Every layer of one decode step (ssd200_decode_layers: chained layers)."""
+        ws = self.workspace(self.lib.ssd200_decode_layers_workspace(self.dims, B))
+        has_conv = conv_in.numel() > 0
+        self._call("ssd200_decode_layers", self.lib.ssd200_decode_layers, self.dims,
+                   self._layer_arr, len(self._layers), hidden.data_ptr(), _abi.ptr(hidden_lp),
+                   ssm_in.data_ptr(), ssm_out.data_ptr(),
+                   conv_in.data_ptr() if has_conv else None,
                    conv_out.data_ptr() if has_conv else None, B, ws.data_ptr(), ws.numel(),
                    self.stream)
 

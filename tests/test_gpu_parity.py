@@ -676,3 +676,35 @@ def test_bf16_head_sharded_generate_over_nccl_world1():
     ref = m.generate(m.from_reference(host, cfg), prompt, 6, cfg=cfg)
     assert torch.equal(got, ref.tokens)
     assert torch.equal(via_api, ref.tokens)
+
+
+@pytest.mark.parametrize("B", [1, 9, 64])
+def test_bf16_chained_decode_layers_bitwise(B):
+    """ssd200_decode_layers (every layer of a token step in one ABI call, the
+    (n_layers, ...) caches addressed by the library) against one
+    ssd200_decode_layer call per layer: logits, greedy tokens and both caches
+    agree bitwise over 4 steps."""
+    import paper_2603_09555_b200 as m
+    from paper_2603_09555_b200.decode import _step_into
+    from paper_2603_09555_b200.model import _Runner
+
+    cfg = m.named_config("1.3b", compute="bf16", vocab_size=512, n_layers=3)
+    params = m.from_reference(m.random_init_host(cfg, 71), cfg)
+    prompt = np.random.default_rng(72 + B).integers(0, cfg.vocab_size, size=(B, 12))
+    _, c0 = m.prefill(params, prompt, cfg, logits=None)
+    runs = []
+    for chained in (True, False):
+        c = c0.copy()
+        r = _Runner(params, cfg)
+        tok = torch.as_tensor(prompt[:, -1], device="cuda")
+        lgs = []
+        for _ in range(4):
+            lg = torch.empty((B, cfg.vocab_size), dtype=torch.float32, device="cuda")
+            _step_into(r, cfg, tok, c, c, logits=lg, argmax=tok, chained=chained)
+            lgs.append(lg)
+        runs.append((torch.stack(lgs), tok.clone(), c))
+    (la, ta, ca), (lb, tb, cb) = runs
+    assert torch.equal(la, lb)
+    assert torch.equal(ta, tb)
+    assert torch.equal(ca.ssm_all, cb.ssm_all)
+    assert torch.equal(ca.conv_all, cb.conv_all)
