@@ -85,9 +85,13 @@ typedef struct ssd200_dims {
 
 typedef struct ssd200_layer {
   const void *W_in, *conv_w, *conv_b, *dt_bias, *a, *D, *norm_w, *W_out;
-  /* optional: W_out with norm_w folded in, reference (d_inner, d_model)
-   * layout.  Reserved for a K-split decode out_proj; may be NULL. */
-  const void *W_out_t;
+  /* optional (d_model) weight of a residual pre-norm, compute dtype (f32 in
+   * bf16 mode): the block then runs in_proj on rmsnorm(hidden) * pre_norm_w
+   * (norm_eps) and adds its output to the un-normalised hidden — the layout
+   * of real state-spaces/mamba2 checkpoints (backbone.layers.N.norm), which
+   * the reference block drops (converter/mapping.json:75-78).  NULL = the
+   * reference block (model.py:124-174). */
+  const void *pre_norm_w;
 } ssd200_layer_t;
 
 int ssd200_abi_version(void);

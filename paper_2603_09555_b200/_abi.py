@@ -61,7 +61,7 @@ class Dims(ctypes.Structure):
 class Layer(ctypes.Structure):
     _fields_ = [
         (n, c_void_p)
-        for n in ("W_in", "conv_w", "conv_b", "dt_bias", "a", "D", "norm_w", "W_out", "W_out_t")
+        for n in ("W_in", "conv_w", "conv_b", "dt_bias", "a", "D", "norm_w", "W_out", "pre_norm_w")
     ]
 
 

@@ -145,6 +145,18 @@ def _config_from_dict(raw: dict, policy: ElemPolicy | None = None) -> ModelConfi
     )
 
 
+PRE_NORM = "layers.{i}.pre_norm.weight"  # optional residual pre-norm (not in the reference format)
+
+
+def pre_norm_names(cfg: ModelConfig) -> list[str]:
+    """The optional per-layer residual pre-norm tensors (d_model,) that a bundle
+    converted from a real state-spaces/mamba2 checkpoint may carry
+    (``convert(..., keep_pre_norm=True)``).  The reference's reader ignores
+    them with a warning (bundle.py:186-225 tolerates unknown tensors); this
+    one loads them into ``LayerParams.pre_norm_w`` when every layer has one."""
+    return [PRE_NORM.format(i=i) for i in range(cfg.n_layers)]
+
+
 def _host_tensors(params, cfg: ModelConfig) -> dict:
     def arr(x):
         if isinstance(x, torch.Tensor):
@@ -155,6 +167,8 @@ def _host_tensors(params, cfg: ModelConfig) -> dict:
     for i, layer in enumerate(params.layers):
         for leaf, attr in _ATTR.items():
             out[f"layers.{i}.{leaf}"] = arr(getattr(layer, attr))
+        if getattr(layer, "pre_norm_w", None) is not None:
+            out[PRE_NORM.format(i=i)] = arr(layer.pre_norm_w)
     return out
 
 
@@ -167,11 +181,12 @@ def save_bundle(params, cfg: ModelConfig, path) -> None:
         path.mkdir(parents=True, exist_ok=True)
         tensors = _host_tensors(params, cfg)
         entries, payload = [], bytearray()
-        for name in tensor_names(cfg):
+        extra = [n for n in pre_norm_names(cfg) if n in tensors]
+        for name in tensor_names(cfg) + extra:
+            shape = (cfg.d_model,) if name in extra else tensor_shape(name, cfg)
             a = np.ascontiguousarray(tensors[name], dtype="<f4")
-            if a.shape != tensor_shape(name, cfg):
-                raise TensorShapeError(
-                    f"{name}: shape {a.shape} != expected {tensor_shape(name, cfg)}")
+            if a.shape != shape:
+                raise TensorShapeError(f"{name}: shape {a.shape} != expected {shape}")
             if len(payload) % ALIGNMENT:
                 payload.extend(b"\x00" * (ALIGNMENT - len(payload) % ALIGNMENT))
             entries.append({"name": name, "dtype": "f32", "shape": list(a.shape),
@@ -213,7 +228,9 @@ def _validate(manifest, payload_len: int, policy: ElemPolicy | None):
     if len(entries) != len(manifest["tensors"]):
         raise BundleError("duplicate tensor names in manifest")
     expected = tensor_names(cfg)
-    for extra in sorted(set(entries) - set(expected)):
+    pre = pre_norm_names(cfg)
+    has_pre = all(n in entries for n in pre)
+    for extra in sorted(set(entries) - set(expected) - (set(pre) if has_pre else set())):
         warnings.warn(f"ignoring unknown tensor {extra!r} in bundle", stacklevel=3)
     prev_end, table = 0, []
     for name in expected:
@@ -237,12 +254,21 @@ def _validate(manifest, payload_len: int, policy: ElemPolicy | None):
                 f"{name}: payload truncated (need {offset + length} bytes, have {payload_len})")
         prev_end = offset + length
         table.append((name, shape, offset, nelems))
+    for name in pre if has_pre else []:  # optional residual pre-norm, after the canonical set
+        entry = entries[name]
+        shape = tuple(entry["shape"])
+        if shape != (cfg.d_model,) or entry["dtype"] != "f32" or entry["length"] != 4 * cfg.d_model:
+            raise TensorShapeError(f"{name}: expected f32 ({cfg.d_model},), got {entry}")
+        if entry["offset"] % ALIGNMENT or entry["offset"] + entry["length"] > payload_len:
+            raise PayloadError(f"{name}: offset {entry['offset']} misaligned or truncated")
+        table.append((name, shape, entry["offset"], cfg.d_model))
     return cfg, table
 
 
 def _assemble(tensors: dict, cfg: ModelConfig) -> SimpleNamespace:
     layers = [SimpleNamespace(**{attr: tensors[f"layers.{i}.{leaf}"]
-                                 for leaf, attr in _ATTR.items()})
+                                 for leaf, attr in _ATTR.items()},
+                              pre_norm_w=tensors.get(PRE_NORM.format(i=i)))
               for i in range(cfg.n_layers)]
     return SimpleNamespace(embedding=tensors["embedding"], layers=layers,
                            final_norm_w=tensors["final_norm.weight"])
@@ -304,6 +330,7 @@ def load_bundle(path, device="cuda", compute: str = "f32"):
             W_out=big(p + "out_proj.weight", transpose=True,
                       row_scale=norm_w if compute == "bf16" else None),
             a=torch.as_tensor(decay_coefficient(host[p + "A_log"], cfg), dtype=wd).to(dev),
+            pre_norm_w=small(PRE_NORM.format(i=i)) if PRE_NORM.format(i=i) in host else None,
         ))
     params = ModelParams(embedding=big("embedding"), layers=layers,
                          final_norm_w=small("final_norm.weight"), mode=compute)

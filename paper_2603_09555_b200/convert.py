@@ -9,8 +9,11 @@ mapping.json (HF ``backbone.*`` names -> canonical names, torch Linear
 (``time_step_limit`` infinity -> null), every tensor cast to float32 from F32 /
 BF16 / F16 / F64 storage, deterministic output.  Source tensors without an
 engine slot are reported, never silently dropped: the per-block residual
-pre-norm (the engine block has none, mapping.json "known_unmapped") and the
-tied ``lm_head``.
+pre-norm (the reference block has none, mapping.json "known_unmapped") and the
+tied ``lm_head``.  ``keep_pre_norm=True`` (``--keep-pre-norm``) instead carries
+the pre-norm weights into the bundle as ``layers.N.pre_norm.weight``, which
+this package's block applies (``LayerParams.pre_norm_w``), so real
+state-spaces/mamba2 checkpoints compute what they were trained to.
 
     python -m paper_2603_09555_b200.convert --source <hf dir> --out <bundle dir>
 """
@@ -135,16 +138,19 @@ def _read_checkpoint(source: str):
     return raw_cfg, tensors
 
 
-def convert(source: str, out: str):
+PRE_NORM_RULE = ("backbone.layers.{i}.norm.weight", "layers.{i}.pre_norm.weight", "none")
+
+
+def convert(source: str, out: str, keep_pre_norm: bool = False):
     """convert.ts convert: HF checkpoint dir -> bundle dir.  Returns
     (cfg, converted canonical names, unmapped source names)."""
     raw_cfg, tensors = _read_checkpoint(source)
     cfg = translate_config(raw_cfg)
     rules = {}
-    for src, dst, tr in TENSOR_RULES:
+    for src, dst, tr in TENSOR_RULES + ((PRE_NORM_RULE,) if keep_pre_norm else ()):
         for s_name, d_name in zip(_expand(src, cfg.n_layers), _expand(dst, cfg.n_layers)):
             rules[s_name] = (d_name, tr)
-    known = {n for p in KNOWN_UNMAPPED for n in _expand(p, cfg.n_layers)}
+    known = {n for p in KNOWN_UNMAPPED for n in _expand(p, cfg.n_layers)} - set(rules)
     produced, unmapped = {}, []
     for name in sorted(tensors):
         if name not in rules:
@@ -154,18 +160,19 @@ def convert(source: str, out: str):
         if target in produced:
             raise BundleError(f"duplicate production of canonical tensor {target}")
         arr = apply_transform(np.asarray(tensors[name], dtype=np.float32), tr)
-        if tuple(arr.shape) != tensor_shape(target, cfg):
-            raise TensorShapeError(
-                f"{target}: shape {list(arr.shape)} != expected {list(tensor_shape(target, cfg))}")
+        want = (cfg.d_model,) if target.endswith("pre_norm.weight") else tensor_shape(target, cfg)
+        if tuple(arr.shape) != tuple(want):
+            raise TensorShapeError(f"{target}: shape {list(arr.shape)} != expected {list(want)}")
         produced[target] = arr
-    for _, dst, _ in TENSOR_RULES:
+    for _, dst, _ in TENSOR_RULES + ((PRE_NORM_RULE,) if keep_pre_norm else ()):
         for d_name in _expand(dst, cfg.n_layers):
             if d_name not in produced:
                 raise MissingTensorError(f"missing canonical tensor {d_name}")
     layers = []
     for i in range(cfg.n_layers):
         layers.append(SimpleNamespace(**{attr: produced[f"layers.{i}.{leaf}"]
-                                         for leaf, attr in _LEAF_ATTR.items()}))
+                                         for leaf, attr in _LEAF_ATTR.items()},
+                                      pre_norm_w=produced.get(f"layers.{i}.pre_norm.weight")))
     params = SimpleNamespace(embedding=produced["embedding"], layers=layers,
                              final_norm_w=produced["final_norm.weight"])
     save_bundle(params, cfg, out)
@@ -178,8 +185,10 @@ def main(argv=None) -> int:
     ap = argparse.ArgumentParser(description="HF Mamba-2 checkpoint -> bundle")
     ap.add_argument("--source", required=True)
     ap.add_argument("--out", required=True)
+    ap.add_argument("--keep-pre-norm", action="store_true",
+                    help="carry backbone.layers.N.norm into the bundle (applied by this engine)")
     args = ap.parse_args(argv)
-    cfg, converted, unmapped = convert(args.source, args.out)
+    cfg, converted, unmapped = convert(args.source, args.out, keep_pre_norm=args.keep_pre_norm)
     print(f"converted {len(converted)} tensors ({cfg.n_layers} layers, d_model={cfg.d_model}) "
           f"-> {args.out}")
     for name in unmapped:

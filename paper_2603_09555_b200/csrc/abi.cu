@@ -564,6 +564,7 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
 // ------------------------------------------------------------ prefill layer
 // workspace carve (identical in sizing and launch)
 template <typename T> struct PrefillWs {
+  void *xn;    // pre-norm only: rmsnorm(hidden) * pre_norm_w, (rows, d_model) T or bf16
   void *u;     // f32/f64: (rows, d_in_proj) T;  bf16: (rows, d_inner+conv_dim) bf16
   void *act;   // post-conv xBC: T or bf16 (rows, conv_dim); reused for the normed y
   T *dt;       // (rows, H)
@@ -579,6 +580,7 @@ bool carve_prefill(const ssd200_dims_t *d, int B, int Tn, void *ws, size_t cap, 
   const long rows = (long)B * Tn;
   const bool lp = d->dtype == SSD200_BF16;
   Carve cv(ws, cap);
+  o.xn = lp ? (void *)cv.take<bf16>(rows * d->d_model) : (void *)cv.take<T>(rows * d->d_model);
   if (lp) {
     o.u = cv.take<bf16>(rows * (d->d_inner + w.conv_dim));
     o.act = cv.take<bf16>(rows * w.conv_dim);
@@ -609,9 +611,19 @@ int prefill_layer_simt(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidde
   T *u = static_cast<T *>(o.u);
   T *act = static_cast<T *>(o.act);
   const int k = d->conv_kernel;
+  // optional residual pre-norm (ssd200_layer_t.pre_norm_w): in_proj reads the normed copy
+  const T *xin = hidden;
+  if (w->pre_norm_w) {
+    rmsnorm_rows<T, T><<<(unsigned)rows, 256, 0, st>>>(hidden, d->d_model,
+                                                      static_cast<const T *>(w->pre_norm_w),
+                                                      static_cast<T *>(o.xn), d->d_model,
+                                                      d->d_model, (T)d->norm_eps);
+    LAUNCH_CHECK("pre_norm");
+    xin = static_cast<const T *>(o.xn);
+  }
   // in_proj: u = hidden . W_in   (model.py:141)
   gemm_simt<T, false, EPI_STORE><<<dim3(blocks_for(wd.d_in_proj, 64), blocks_for(rows, 64)),
-                                   256, 0, st>>>(hidden, d->d_model,
+                                   256, 0, st>>>(xin, d->d_model,
                                                  static_cast<const T *>(w->W_in), wd.d_in_proj,
                                                  u, wd.d_in_proj, (int)rows, (int)wd.d_in_proj,
                                                  d->d_model);
@@ -724,8 +736,18 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
   ep.dt_bias = static_cast<const float *>(w->dt_bias);
   ep.dt_lo = (float)d->dt_min;
   ep.dt_hi = (float)d->dt_max;
+  REQUIRE(!(partial && w->pre_norm_w), SSD200_EUNSUPPORTED,
+          "head-sharded prefill has no residual pre-norm");
   phase_mark(PH_IN_PROJ, 0, st);
-  int rc = tc_gemm<TC_EPI_INPROJ>(hidden_lp, d->d_model, static_cast<const bf16 *>(w->W_in),
+  const bf16 *xin = hidden_lp;
+  if (w->pre_norm_w) {  // optional residual pre-norm: in_proj reads rmsnorm(hidden) * w (bf16)
+    rmsnorm_rows<float, bf16><<<(unsigned)rows, 256, 0, st>>>(
+        hidden, d->d_model, static_cast<const float *>(w->pre_norm_w), static_cast<bf16 *>(o.xn),
+        d->d_model, d->d_model, (float)d->norm_eps);
+    LAUNCH_CHECK("pre_norm");
+    xin = static_cast<const bf16 *>(o.xn);
+  }
+  int rc = tc_gemm<TC_EPI_INPROJ>(xin, d->d_model, static_cast<const bf16 *>(w->W_in),
                                   d->d_model, (int)rows, (int)wd.d_in_proj, d->d_model, ep, st);
   if (rc) return rc;
   phase_mark(PH_IN_PROJ, 1, st);
@@ -846,6 +868,7 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
 
 // ------------------------------------------------------------- decode layer
 template <typename T> struct DecodeWs {
+  void *xn;          // pre-norm only: (B, d_model) T (bf16 in bf16 mode)
   T *u, *act, *y, *normed_T;
   bf16 *normed_lp;
   float *part;       // wide-batch bf16: out_proj split-K partials
@@ -900,6 +923,7 @@ bool carve_decode(const ssd200_dims_t *d, int B, void *ws, size_t cap, DecodeWs<
   const bool big = std::is_same<T, float>::value && d->dtype == SSD200_BF16 &&
                    dec_big_eligible(d);
   const DecSplits sp = big ? dec_splits(d, B) : DecSplits{1, 1};
+  o.xn = cv.take<T>((size_t)B * d->d_model);
   o.u = cv.take<T>((size_t)sp.in * B * w.d_in_proj);
   o.part = big ? cv.take<float>((size_t)sp.out * B * d->d_model) : nullptr;
   o.ssq = big ? cv.take<float>((size_t)B * d->n_heads) : nullptr;
@@ -983,7 +1007,17 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   const DecSplits sp = dec_splits(d, B);
   const long s_in = (long)B * wd.d_in_proj, s_out = (long)B * d->d_model;
   {
-    int rc = dec_gemm(static_cast<const bf16 *>(w->W_in), (int)wd.d_in_proj, d->d_model, hidden_lp,
+    const bf16 *xin = hidden_lp;
+    if (w->pre_norm_w) {  // optional residual pre-norm
+      REQUIRE(hidden, SSD200_EUNSUPPORTED, "head-sharded decode has no residual pre-norm");
+      rmsnorm_rows<float, bf16><<<B, 256, 0, st>>>(hidden, d->d_model,
+                                                   static_cast<const float *>(w->pre_norm_w),
+                                                   static_cast<bf16 *>(o.xn), d->d_model,
+                                                   d->d_model, (float)d->norm_eps);
+      LAUNCH_CHECK("pre_norm");
+      xin = static_cast<const bf16 *>(o.xn);
+    }
+    int rc = dec_gemm(static_cast<const bf16 *>(w->W_in), (int)wd.d_in_proj, d->d_model, xin,
                       B, o.u, wd.d_in_proj, sp.in, s_in, st);
     if (rc) return rc;
   }
@@ -1097,6 +1131,25 @@ int decode_layer_impl(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidden
                               st);
     }
   }
+  // optional residual pre-norm: in_proj reads rmsnorm(hidden) * pre_norm_w
+  const T *xin = hidden;
+  const bf16 *xin_lp = hidden_lp;
+  if (w->pre_norm_w) {
+    if (lp) {
+      rmsnorm_rows<T, bf16><<<B, 256, 0, st>>>(hidden, d->d_model,
+                                              static_cast<const T *>(w->pre_norm_w),
+                                              static_cast<bf16 *>(o.xn), d->d_model, d->d_model,
+                                              (T)d->norm_eps);
+      xin_lp = static_cast<const bf16 *>(o.xn);
+    } else {
+      rmsnorm_rows<T, T><<<B, 256, 0, st>>>(hidden, d->d_model,
+                                           static_cast<const T *>(w->pre_norm_w),
+                                           static_cast<T *>(o.xn), d->d_model, d->d_model,
+                                           (T)d->norm_eps);
+      xin = static_cast<const T *>(o.xn);
+    }
+    LAUNCH_CHECK("pre_norm");
+  }
   // in_proj
   if (lp) {
     REQUIRE(hidden_lp, SSD200_EINVAL, "bf16 mode needs the hidden_lp shadow");
@@ -1104,14 +1157,14 @@ int decode_layer_impl(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidden
     if (B <= GEMV_BF16_MAX_ROWS) {
       gemv_nk<float, bf16, bf16, EPI_STORE>
           <<<dim3(blocks_for(wd.d_in_proj, 32), blocks_for(B, 4)), 256, 0, st>>>(
-              hidden_lp, d->d_model, Win, d->d_model, (float *)o.u, wd.d_in_proj, nullptr, B,
+              xin_lp, d->d_model, Win, d->d_model, (float *)o.u, wd.d_in_proj, nullptr, B,
               (int)wd.d_in_proj, d->d_model);
       LAUNCH_CHECK("gemv_nk in_proj");
     } else {
       TcEpilogue ep{};
       ep.C = o.u;
       ep.ldc = wd.d_in_proj;
-      int rc = tc_gemm<TC_EPI_F32>(hidden_lp, d->d_model, Win, d->d_model, B, (int)wd.d_in_proj,
+      int rc = tc_gemm<TC_EPI_F32>(xin_lp, d->d_model, Win, d->d_model, B, (int)wd.d_in_proj,
                                    d->d_model, ep, st);
       if (rc) return rc;
     }
@@ -1119,11 +1172,11 @@ int decode_layer_impl(const ssd200_dims_t *d, const ssd200_layer_t *w, T *hidden
     const T *Win = static_cast<const T *>(w->W_in);
     if (B <= GEMV_MAX_ROWS) {
       gemv_kn<T, EPI_STORE><<<dim3(blocks_for(wd.d_in_proj, 32), blocks_for(B, 8)), dim3(32, 8),
-                              0, st>>>(hidden, d->d_model, Win, wd.d_in_proj, o.u, wd.d_in_proj,
+                              0, st>>>(xin, d->d_model, Win, wd.d_in_proj, o.u, wd.d_in_proj,
                                        B, (int)wd.d_in_proj, d->d_model);
     } else {
       gemm_simt<T, false, EPI_STORE><<<dim3(blocks_for(wd.d_in_proj, 64), blocks_for(B, 64)),
-                                       256, 0, st>>>(hidden, d->d_model, Win, wd.d_in_proj, o.u,
+                                       256, 0, st>>>(xin, d->d_model, Win, wd.d_in_proj, o.u,
                                                      wd.d_in_proj, B, (int)wd.d_in_proj,
                                                      d->d_model);
     }
@@ -1260,7 +1313,7 @@ int head_bf16(const ssd200_dims_t *d, int V, const float *hidden, long hrs, cons
 // =============================================================== C ABI
 extern "C" {
 
-int ssd200_abi_version(void) { return 2; }
+int ssd200_abi_version(void) { return 3; }
 
 void ssd200_tuning_defaults(ssd200_tuning_t *t) {
   if (t) *t = kDefaultTuning;

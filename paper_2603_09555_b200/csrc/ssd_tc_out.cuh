@@ -295,20 +295,19 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
       else sm100::tmem_st4_if(taddr, *reinterpret_cast<const uint32_t(*)[4]>(pk), on);
     };
     // M = G * decay * dt for this warp's slice of head hh -> TMEM M buffer hh & 1.
-    // JD = this warp's diagonal chunk (4 R + lane quarter, warp-uniform) is a
-    // compile-time constant: exactly the JD chunks left of the diagonal are
-    // computed (branch-free, so their loads and math interleave) — none of the
-    // chunks at or past the diagonal (zero for every head, written once).
-    auto build_m = [&](auto jdc, int hh, float csl) {
-      constexpr int JD = decltype(jdc)::value;
+    // The off-diagonal chunks are computed branch-free (NJ is a compile-time
+    // constant per row tile) so their loads and math interleave; chunks at or
+    // past the diagonal are computed but not stored.
+    auto build_m = [&](auto rt, int hh, float csl) {
+      constexpr int NJ = 4 * (decltype(rt)::value + 1);
       const uint32_t mt = tmem + lane_off + TM_M + (hh & 1) * 128 + (CW / 2) * kw;
       {  // diagonal chunk: per-element decay, causal mask
         uint32_t gw[CW / 2], pd[CW / 2];
         float cs[CW], dt[CW];
-        ld_g(JD, gw);
-        ld_table(wcs, JD, cs);
-        ld_table(wdt, JD, dt);
-        const int s0 = 32 * JD + CW * kw;
+        ld_g(jd, gw);
+        ld_table(wcs, jd, cs);
+        ld_table(wdt, jd, dt);
+        const int s0 = 32 * jd + CW * kw;
 #pragma unroll
         for (int e = 0; e < CW / 2; ++e) {
           const int s = s0 + 2 * e;
@@ -319,12 +318,12 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
           __nv_bfloat162 v = __floats2bfloat162_rn(m0, m1);
           pd[e] = *reinterpret_cast<uint32_t *>(&v);
         }
-        st_m(mt + 16 * JD, pd, true);
+        st_m(mt + 16 * jd, pd, true);
       }
       // off-diagonal chunks: M = (G * cf) * rf on packed bf16 pairs (M is bf16 anyway)
       const uint32_t *wcfb = reinterpret_cast<const uint32_t *>(wcf);
 #pragma unroll
-      for (int j = 0; j < JD; ++j) {
+      for (int j = 0; j < NJ - 1; ++j) {
         uint32_t gw[CW / 2], cw[CW / 2], pk[CW / 2];
         ld_g(j, gw);
 #pragma unroll
@@ -340,7 +339,7 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
                                            rf2);
           pk[e] = *reinterpret_cast<const uint32_t *>(&m);
         }
-        st_m(mt + 16 * j, pk, true);
+        st_m(mt + 16 * j, pk, j < jd);
       }
       sm100::tmem_st_wait();
       sm100::tc_fence_before();
@@ -348,16 +347,8 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
       if (lane == 0) sm100::mbar_arrive(&mrdy[hh & 1]);
     };
     auto build = [&](int hh, float csl) {
-      switch (jd) {
-        case 0: build_m(std::integral_constant<int, 0>{}, hh, csl); break;
-        case 1: build_m(std::integral_constant<int, 1>{}, hh, csl); break;
-        case 2: build_m(std::integral_constant<int, 2>{}, hh, csl); break;
-        case 3: build_m(std::integral_constant<int, 3>{}, hh, csl); break;
-        case 4: build_m(std::integral_constant<int, 4>{}, hh, csl); break;
-        case 5: build_m(std::integral_constant<int, 5>{}, hh, csl); break;
-        case 6: build_m(std::integral_constant<int, 6>{}, hh, csl); break;
-        default: build_m(std::integral_constant<int, 7>{}, hh, csl); break;
-      }
+      if (R) build_m(std::integral_constant<int, 1>{}, hh, csl);
+      else build_m(std::integral_constant<int, 0>{}, hh, csl);
     };
 
     Pref nxt;

@@ -65,7 +65,7 @@ def layer_struct(lp: LayerParams) -> _abi.Layer:
         D=lp.D.data_ptr(),
         norm_w=lp.norm_w.data_ptr(),
         W_out=lp.W_out.data_ptr(),
-        W_out_t=lp.W_out_t.data_ptr() if lp.W_out_t is not None else None,
+        pre_norm_w=lp.pre_norm_w.data_ptr() if lp.pre_norm_w is not None else None,
     )
 
 

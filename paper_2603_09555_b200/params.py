@@ -36,9 +36,10 @@ class LayerParams:
     norm_w: torch.Tensor
     W_out: torch.Tensor
     a: torch.Tensor = field(default=None)  # -exp(A_log), compute dtype (f32 in bf16 mode)
-    # optional norm_w-folded W_out in the reference (d_inner, d_model) layout
-    # (ssd200_layer_t.W_out_t; unused by the current kernels)
-    W_out_t: torch.Tensor = field(default=None)
+    # optional residual pre-norm weight (d_model), compute dtype (f32 in bf16 mode):
+    # real state-spaces/mamba2 checkpoints' backbone.layers.N.norm, which the
+    # reference block drops (converter/mapping.json:75-78); None = the reference block
+    pre_norm_w: torch.Tensor = field(default=None)
 
 
 @dataclass
@@ -116,6 +117,8 @@ def from_reference(params, cfg: ModelConfig, device="cuda") -> ModelParams:
                 norm_w=small(lp.norm_w),
                 W_out=big(W_out, transpose=True),
                 a=small(decay_coefficient(_np(lp.A_log), cfg)),
+                pre_norm_w=(small(lp.pre_norm_w)
+                            if getattr(lp, "pre_norm_w", None) is not None else None),
             )
         )
     return ModelParams(

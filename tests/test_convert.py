@@ -102,3 +102,40 @@ def test_finite_time_step_limit(tmp_path):
     _hf_checkpoint(tmp_path / "hf", limit=(0.001, 0.1))
     cfg, _, _ = convert.convert(str(tmp_path / "hf"), str(tmp_path / "out"))
     assert cfg.dt_limits == (0.001, 0.1)
+
+
+def test_keep_pre_norm_round_trip_and_oracle(tmp_path):
+    """--keep-pre-norm: backbone.layers.N.norm.weight lands in the bundle as
+    layers.N.pre_norm.weight (instead of being reported unmapped), the bundle
+    reader returns it as pre_norm_w, and the oracle block with the pre-norm is
+    residual + mixer(rmsnorm(hidden) * w) — the real state-spaces/mamba2 block."""
+    import warnings
+
+    import oracle as orc
+
+    src = _hf_checkpoint(tmp_path / "hf")
+    cfg, converted, unmapped = convert.convert(str(tmp_path / "hf"), str(tmp_path / "b"),
+                                               keep_pre_norm=True)
+    assert not any("layers.0.norm.weight" in u for u in unmapped)
+    assert "layers.1.pre_norm.weight" in converted
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")  # the pre-norm tensors are not "unknown"
+        host, cfg2 = bundle.load_bundle_host(tmp_path / "b")
+    for i in range(cfg.n_layers):
+        assert np.array_equal(host.layers[i].pre_norm_w, src[f"backbone.layers.{i}.norm.weight"])
+    # without the flag the reference behaviour is unchanged
+    _, _, unmapped0 = convert.convert(str(tmp_path / "hf"), str(tmp_path / "b0"))
+    assert any("backbone.layers.0.norm.weight" in u for u in unmapped0)
+    host0, _ = bundle.load_bundle_host(tmp_path / "b0")
+    assert host0.layers[0].pre_norm_w is None
+    # oracle block with the pre-norm = manual composition
+    rng = np.random.default_rng(3)
+    hid = rng.standard_normal((2, 20, cfg.d_model)).astype(np.float32)
+    lyr = host.layers[0]
+    out, _, _ = orc.block(lyr, hid, cfg)
+    from types import SimpleNamespace
+
+    plain = SimpleNamespace(**{k: v for k, v in vars(lyr).items() if k != "pre_norm_w"})
+    normed = orc.rms_norm(hid, lyr.pre_norm_w, cfg.norm_eps)
+    mix, _, _ = orc.block(plain, normed, cfg)
+    assert np.allclose(out, hid + (mix - normed), atol=1e-5, rtol=1e-5)

@@ -708,3 +708,46 @@ def test_bf16_chained_decode_layers_bitwise(B):
     assert torch.equal(ta, tb)
     assert torch.equal(ca.ssm_all, cb.ssm_all)
     assert torch.equal(ca.conv_all, cb.conv_all)
+
+
+@pytest.mark.parametrize("comp", ["f32", "bf16"])
+def test_pre_norm_block_vs_oracle(comp):
+    """The optional residual pre-norm (ssd200_layer_t.pre_norm_w; real
+    state-spaces/mamba2 checkpoints' backbone.layers.N.norm, which the reference
+    block drops): prefill, a cached decode step and greedy tokens against the
+    oracle with the same pre-norm — f32 at the reference gates, bf16 on
+    bf16-rounded weights within the stated bound."""
+    import paper_2603_09555_b200 as m
+
+    if comp == "f32":
+        cfg = small_config(d_model=64, n_layers=2)
+    else:
+        cfg = _bf16_cfg(d_model=512)
+    host = m.random_init_host(cfg, 51)
+    rng = np.random.default_rng(52)
+    for lp in host.layers:
+        lp.pre_norm_w = (1.0 + 0.3 * rng.standard_normal(cfg.d_model)).astype(np.float32)
+    params = m.from_reference(host, cfg)
+    assert params.layers[0].pre_norm_w is not None
+    toks = rng.integers(0, cfg.vocab_size, size=(2, 300))
+    ref_host = orc.round_weights_bf16(host) if comp == "bf16" else host
+    rcfg = cfg.with_policy(compute="f32")
+    rl, rs, rc = orc.prefill(ref_host, toks, rcfg)
+    logits, cache = m.prefill(params, toks[:, :299], cfg)
+    sl, _ = m.decode_step(params, cache, toks[:, 299], cfg)
+    got_p, got_d = _np(logits), _np(sl)
+    if comp == "f32":
+        for got, ref in ((got_p, rl[:, :299]), (got_d, rl[:, 299])):
+            assert np.abs(got - ref).max() <= 2e-5 * max(1.0, np.abs(ref).max())
+        gen = m.generate(params, toks[:1, :40], 12, cfg=cfg)
+        assert np.array_equal(_np(gen.tokens), orc.generate(host, toks[:1, :40], 12, cfg))
+    else:
+        r1 = np.linalg.norm(got_p[:, -1] - rl[:, 298]) / np.linalg.norm(rl[:, 298])
+        r2 = np.linalg.norm(got_d - rl[:, 299]) / np.linalg.norm(rl[:, 299])
+        report("pre_norm_bf16", prefill=float(r1), decode=float(r2))
+        assert r1 <= BF16_BOUND and r2 <= BF16_BOUND, (r1, r2)
+    # and without the pre-norm the outputs differ (the weights are non-unit)
+    for lp in params.layers:
+        lp.pre_norm_w = None
+    plain, _ = m.prefill(params, toks[:, :299], cfg)
+    assert (plain - logits).abs().max().item() > 1e-3

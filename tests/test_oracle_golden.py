@@ -123,3 +123,21 @@ def test_c1_golden_fixture_sane():
     assert z["tokens"].shape == (1, 65)
     assert int(np.argmax(z["logits_first"])) == int(z["tokens"][0, 0])
     assert int(np.argmax(z["logits_last"])) == int(z["tokens"][0, -1])
+
+
+def test_verify_sequential_recurrence_matches_reference_golden():
+    """verify.py's oracle suite compares the device scan with a host f64 time
+    loop; that loop reproduces the reference's own sequential_ssm outputs
+    (ssd_cases.npz, written by the real reference) to f64 rounding."""
+    from paper_2603_09555_b200.ssd import SsdInputs
+    from paper_2603_09555_b200.verify import sequential_recurrence
+
+    z = golden("ssd_cases.npz")
+    n = sum(1 for k in z.files if k.endswith(".Y_seq"))
+    for i in range(n):
+        g = lambda k: z[f"{i}.{k}"]  # noqa: E731
+        if int(g("has_init")):
+            continue  # the verify suite runs from a zero state
+        y = sequential_recurrence(SsdInputs(X=g("X"), dt=g("dt"), a=g("a"), Bmat=g("B"),
+                                            Cmat=g("C")))
+        assert np.abs(y - g("Y_seq")).max() <= 1e-12 * max(1.0, np.abs(g("Y_seq")).max())
