@@ -237,14 +237,16 @@ def peaks():
                 "source": "fallback (B200_PROFILING.md)"}
 
 
-def traffic_from_profiles(kernel_key):
-    """dram bytes per launch of the dominant kernel from the committed ncu
-    --set full capture (profiles/traffic.json), or None."""
+def traffic_from_profiles(model, kernel_key, batch):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/traffic.json, keyed by model; captured at
+    C4's per-GPU batch of 32 rows x 8192), or None for another shape."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(kernel_key)
+            table = json.load(f).get(model.lower(), {})
     except (OSError, ValueError):
         return None
+    return table.get(kernel_key) if batch == 32 else None
 
 
 # ---------------------------------------------------------------- CPU legs
@@ -433,14 +435,18 @@ def run_prefill(args, rank, world, local):
     peak = pk["bf16_tflops_sustained"]
     kernel_key = {0: "tc_gemm_kernel<256,2>", 1: "conv_silu_tma", 2: "ssd_scan",
                   3: "gated_norm_kernel", 4: "tc_gemm_kernel<256,4>"}[dom]
+    kernel_name = {0: "tc_gemm_kernel<256, INPROJ, CTA pair>", 1: "conv_silu_tma",
+                   2: "ssd_tc_cumsum + ssd_tc_chunkscan + ssd_tc_out", 3: "-",
+                   4: "tc_gemm_kernel<256, RESID_NORM, CTA pair>"}[dom]
     roof = {
-        "kernel": f"{PHASES[dom]} ({kernel_key})",
+        "kernel": f"{PHASES[dom]} ({kernel_name})",
         "bound": "tensor",
         "achieved": achieved,
         "peak": peak,
         "unit": "TFLOP/s",
         "frac": (achieved / peak) if achieved else None,
-        "traffic": traffic_from_profiles(kernel_key),
+        "traffic": traffic_from_profiles(args.model, kernel_key, B),
+        "traffic_source": "profiles/traffic.json (ncu --set full, one launch at B=32, T=8192)",
         "algorithmic_flops_per_launch": phase_flops[dom],
         "avg_launch_ms": launch_ms,
         "peak_source": pk["source"] + ", sustained (kernel timed inside a long step)",

@@ -70,6 +70,7 @@ typedef struct ssd200_tuning {
   int stream_cps;          /* decode state stream: CTAs per SM (0 auto, 1, 2) */
   int stream_cw;           /* decode state stream: consumer warps (8 or 16) */
   int out_interleave;      /* SSD output kernel: the two row tiles of a chunk run side by side (1) */
+  int gemm_group_m;        /* prefill GEMM tile order: row blocks per group (0 auto, 1 row-major) */
 } ssd200_tuning_t;
 
 void ssd200_tuning_defaults(ssd200_tuning_t *t);
