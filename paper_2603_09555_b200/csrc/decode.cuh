@@ -194,8 +194,10 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
     // ---------------- producer warp: loads, write-back, refills
     if (lane == 0) {
       for (int li = 0; li < S && li < cnt; ++li) issue_state(li);
-      griddep_wait();  // the in_proj partials
+      // let the out_proj launch now: its CTAs take the SMs this grid leaves free and
+      // stream W_out into their rings (they wait for this grid before reading u / ssq)
       griddep_launch();
+      griddep_wait();  // the in_proj partials
       for (int li = 0; li < S && li < cnt; ++li) issue_rest(li);
       for (int li = 0; li < cnt; ++li) {
         const int s = li % S;
@@ -413,8 +415,10 @@ __global__ __launch_bounds__(256) void dec_out_finish(DecFinishArgs a) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = (int)blockIdx.x < nb_h && n < a.d_model;
   const long i = (long)b * a.d_model + n;
-  griddep_wait();  // the residual, the partials and sum u^2 are all predecessor outputs
+  // the next layer's in_proj may launch at once and prefetch its weights while the
+  // out_proj drains (it waits for this grid before reading hidden_lp)
   griddep_launch();
+  griddep_wait();  // the residual, the partials and sum u^2 are all predecessor outputs
   const float hold = (live && !a.pout) ? a.hidden_in[i] : 0.f;
   if ((int)blockIdx.x >= nb_h) {
     const int c = a.d_inner + ((int)blockIdx.x - nb_h) * 256 + threadIdx.x;  // B / C channel
