@@ -516,8 +516,10 @@ def run_prefill_heads(args, rank, world, local):
     dev_tok = host_tok.cuda()
     lib = _abi.lib()
 
+    run = shard.HeadShardedPrefill(params, dev_tok, cfg)  # buffers allocated once
+
     def step(tok):
-        run = shard.HeadShardedPrefill(params, tok, cfg)
+        run.restart(tok)
         for i in range(cfg.n_layers):
             buf = run.partial(i)
             if world > 1:

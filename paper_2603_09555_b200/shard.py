@@ -230,6 +230,20 @@ class HeadShardedPrefill:
                                 dtype=torch.float32, device=r.dev)
         self.ws = r.workspace(r.lib.ssd200_prefill_layer_workspace(self.dims_l, self.B, self.T))
 
+    def restart(self, tokens) -> None:
+        """Embed a new (B, T) token batch of the same shape into the existing
+        buffers (no allocation: a benchmark loop reuses one object)."""
+        from . import _abi
+        from .model import check_tokens
+
+        r, cfg = self.r, self.cfg
+        tok = check_tokens(tokens, cfg, 2, r.dev)
+        if tuple(tok.shape) != (self.B, self.T):
+            raise ValueError(f"restart needs tokens of shape {(self.B, self.T)}, got {tuple(tok.shape)}")
+        r._call("ssd200_embed", r.lib.ssd200_embed, r.dims, tok.data_ptr(), self.rows,
+                cfg.vocab_size, self.params.embedding.data_ptr(), self.hidden.data_ptr(),
+                _abi.ptr(self.lp), r.stream)
+
     def partial(self, i: int) -> torch.Tensor:
         from . import _abi
 

@@ -671,11 +671,21 @@ def test_bf16_head_sharded_generate_over_nccl_world1():
             gd.step()
         got = gd.tokens.clone()
         via_api = shard.generate_head_sharded(shards[0], prompt, 6, cfg, group=group)
+        lg, ssm = shard.prefill_head_sharded(shards[0], prompt, cfg, group=group)
+        # restart(): the same object re-run on new tokens equals a fresh one
+        run2 = shard.HeadShardedPrefill(shards[0], prompt, cfg)
+        run2.restart(prompt[::-1].copy())
+        fresh = shard.HeadShardedPrefill(shards[0], prompt[::-1].copy(), cfg)
+        assert torch.equal(run2.hidden, fresh.hidden) and torch.equal(run2.lp, fresh.lp)
     finally:
         dist.destroy_process_group()
-    ref = m.generate(m.from_reference(host, cfg), prompt, 6, cfg=cfg)
+    full = m.from_reference(host, cfg)
+    ref = m.generate(full, prompt, 6, cfg=cfg)
     assert torch.equal(got, ref.tokens)
     assert torch.equal(via_api, ref.tokens)
+    want, cache = m.prefill(full, prompt, cfg, logits="last")
+    assert ((lg - want).norm() / want.norm()).item() <= BF16_BOUND
+    assert ((ssm - cache.ssm_all).norm() / cache.ssm_all.norm()).item() <= BF16_STATE_BOUND
 
 
 @pytest.mark.parametrize("B", [1, 9, 64])
