@@ -17,18 +17,20 @@
 
 using namespace ssd200;
 
-constexpr int N = 8512, K = 2048, BM = 128, BK = 64, STAGES = 5, KSPLIT = 4;
+constexpr int N = 8512, K = 2048, BM = 128, BK = 64, MAXSTAGES = 12;
 constexpr uint32_t TILE = BM * BK * 2;  // 16 KB
 
 template <bool TILED>
-__global__ void __launch_bounds__(64, 2) stream(const __grid_constant__ CUtensorMap tm,
-                                                 const uint8_t *tiled, float *sink) {
+__global__ void __launch_bounds__(64) stream(const __grid_constant__ CUtensorMap tm,
+                                             const uint8_t *tiled, float *sink, int STAGES,
+                                             int KSPLIT) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *sm = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  __shared__ __align__(8) uint64_t full[MAXSTAGES], empty[MAXSTAGES];
   const int ntn = N / BM + (N % BM ? 1 : 0);
   const int n_blk = blockIdx.x % ntn, ks = blockIdx.x / ntn;
   const int nkb = K / BK, kb0 = ks * nkb / KSPLIT, kb1 = (ks + 1) * nkb / KSPLIT;
+  if (blockIdx.x >= ntn * KSPLIT) return;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       sm100::mbar_init(&full[s], 1);
@@ -99,9 +101,8 @@ int main() {
   ((EncodeFn)fn)(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, strides, box, es,
                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  const size_t smem = STAGES * TILE + 1024;
-  cudaFuncSetAttribute(stream<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(stream<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(stream<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(stream<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   // flush buffer larger than L2 between iterations
   uint8_t *flush;
   const size_t fb = 512ull << 20;
@@ -109,27 +110,33 @@ int main() {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  const int grid = ntn * KSPLIT;
-  for (int variant = 0; variant < 4; ++variant) {
-    const bool tiledv = variant & 1;
-    float tot = 0.f;
-    const int iters = 50;
-    for (int it = 0; it < iters; ++it) {
-      cudaMemsetAsync(flush, it, fb);
-      cudaEventRecord(a);
-      if (tiledv)
-        stream<true><<<grid, 64, smem>>>(tm, tiled, sink);
-      else
-        stream<false><<<grid, 64, smem>>>(tm, tiled, sink);
-      cudaEventRecord(b);
-      cudaEventSynchronize(b);
-      float ms;
-      cudaEventElapsedTime(&ms, a, b);
-      tot += ms;
+  // (stages, k-split): smem per CTA = stages x 16 KB; CTAs per SM follow from it
+  const int cfgs[][2] = {{5, 4}, {5, 8}, {3, 8}, {2, 16}, {3, 16}, {10, 2}, {12, 4}, {6, 4}, {4, 8}};
+  for (auto &c : cfgs) {
+    const int stages = c[0], ksplit = c[1];
+    const size_t smem = stages * TILE + 1024;
+    const int grid = ntn * ksplit;
+    for (int tiledv = 0; tiledv < 2; ++tiledv) {
+      float tot = 0.f;
+      const int iters = 30;
+      for (int it = 0; it < iters; ++it) {
+        cudaMemsetAsync(flush, it, fb);
+        cudaEventRecord(a);
+        if (tiledv)
+          stream<true><<<grid, 64, smem>>>(tm, tiled, sink, stages, ksplit);
+        else
+          stream<false><<<grid, 64, smem>>>(tm, tiled, sink, stages, ksplit);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        tot += ms;
+      }
+      const double us = tot / iters * 1e3;
+      printf("stages %2d ksplit %2d grid %4d smem %3zu KB  %-22s %8.2f us  %7.0f GB/s\n", stages,
+             ksplit, grid, smem >> 10, tiledv ? "tile-major 1-D bulk" : "row-major 2-D TMA", us,
+             bytes / (us * 1e3));
     }
-    const double us = tot / iters * 1e3;
-    printf("%-28s %8.2f us  %7.0f GB/s\n", tiledv ? "(b) tile-major 1-D bulk" : "(a) row-major 2-D TMA", us,
-           bytes / (us * 1e3));
   }
   cudaError_t e = cudaDeviceSynchronize();
   printf("status %s\n", cudaGetErrorString(e));
