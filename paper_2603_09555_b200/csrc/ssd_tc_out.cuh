@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
     sm100::mbar_init(bar_g, 1);
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&bar_x[i], 1);
-      sm100::mbar_init(&xfree[i], 1 + OUT_MW);  // MMA commit + every math warp's D-skip read
+      sm100::mbar_init(&xfree[i], 1 + 4);  // MMA commit + each lane quarter's u store (it reuses the tile)
       sm100::mbar_init(&bar_p[i], 1);
       sm100::mbar_init(&pfree[i], 1);
       sm100::mbar_init(&bar_y[i], 1);
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
       sm100::mbar_init(&mrdy[i], OUT_MW);
     }
     sm100::mbar_init(bar_z, 1);
-    sm100::mbar_init(zfree, 4);  // one arrival per lane quarter once its u store has read smem
+    sm100::mbar_init(zfree, OUT_MW);  // one arrival per math warp once it has read its z
     sm100::fence_barrier_init();
   }
   if (warp == 1) sm100::tmem_alloc<512>(tslot);
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
         for (int q = 0; q <= R; ++q)
           sm100::tma_load_3d(sm + OutSmem::X0 + buf * 32768 + q * 16384, &tm_act, &bar_x[buf],
                              h * TC_P, c * TC_L + q * 128, b);
-        sm100::mbar_wait(zfree, (i & 1) ^ 1);  // single buffer: head i-1's epilogue read it
+        sm100::mbar_wait(zfree, (i & 1) ^ 1);  // single buffer: every warp has read head i-1's z
         sm100::mbar_arrive_expect_tx(bar_z, 16384);
         sm100::tma_load_3d(sm + OutSmem::Z0, &tm_z, bar_z, h * TC_P, c * TC_L + R * 128, b);
       }
@@ -409,15 +409,16 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
 #pragma unroll
       for (int cc = 0; cc < EW / 8; ++cc)
         zv[cc] = *reinterpret_cast<const uint4 *>(sm + OutSmem::Z0 + sw128_off(row, pc / 8 + cc));
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(zfree);  // the next head's z may land now
       sm100::mbar_wait(&bar_y[buf], (i >> 1) & 1);  // MMA(i) done
-      {  // D-skip x from the X tile the MMA just consumed (row l of the chunk), then release it
-        const uint8_t *xt = sm + OutSmem::X0 + buf * 32768 + R * 16384;
+      // D-skip x from the X tile the MMA just consumed (row l of the chunk); u later
+      // overwrites the same positions and leaves from there, so the tile is released
+      // only once that store has read it
+      uint8_t *xt = sm + OutSmem::X0 + buf * 32768 + R * 16384;
 #pragma unroll
-        for (int cc = 0; cc < EW / 8; ++cc)
-          xv[cc] = *reinterpret_cast<const uint4 *>(xt + sw128_off(row, pc / 8 + cc));
-        __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(&xfree[buf]);
-      }
+      for (int cc = 0; cc < EW / 8; ++cc)
+        xv[cc] = *reinterpret_cast<const uint4 *>(xt + sw128_off(row, pc / 8 + cc));
       sm100::tc_fence_after();
       // ---- epilogue(i) on columns [pc, pc+EW) in 16-column steps, overlapping MMA(i+1)
       const uint32_t ydt = tmem + lane_off + TM_Y + buf * 128 + pc;
@@ -446,22 +447,21 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
           __nv_bfloat162 v = __floats2bfloat162_rn(u0, u1);
           out[j] = *reinterpret_cast<uint32_t *>(&v);
         }
-        // u overwrites this thread's own z positions of the tile (read above)
+        // u overwrites this thread's own x positions of the X tile (read above)
 #pragma unroll
         for (int k = 0; k < 2; ++k)
-          *reinterpret_cast<uint4 *>(sm + OutSmem::Z0 + sw128_off(row, pc / 8 + 2 * hs + k)) =
+          *reinterpret_cast<uint4 *>(xt + sw128_off(row, pc / 8 + 2 * hs + k)) =
               make_uint4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
       }
       // the quarter's 32 x 64 u tile leaves through TMA (rows past T are clipped);
-      // the z buffer is released once the store has read it
+      // the X buffer is released once the store has read it
       sm100::fence_proxy_async();
       named_bar(4 + q, 32 * OUT_KW);
       if (kw == 0 && lane == 0) {
-        sm100::tma_store_3d(&tm_u, sm + OutSmem::Z0 + q * 4096, h * TC_P,
-                            c * TC_L + R * 128 + q * 32, b);
+        sm100::tma_store_3d(&tm_u, xt + q * 4096, h * TC_P, c * TC_L + R * 128 + q * 32, b);
         sm100::bulk_commit();
         sm100::bulk_wait_read0();
-        sm100::mbar_arrive(zfree);
+        sm100::mbar_arrive(&xfree[buf]);
       }
       // sum u^2 of this warp's columns over the 8-head slice that ends here:
       // one partial per (slice, column half), slice-major (n_slices * OUT_KW, rows),
