@@ -554,16 +554,16 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
     LAUNCH_CHECK("ssd_tc_pass");
   }
   // outputs (+ D skip + gate)
-  // head groups of whole 8-head slices: sum u^2 leaves per slice, so the grouping
+  // head groups of whole SSQ_SLICE-head slices: sum u^2 leaves per slice, so the grouping
   // (which depends on B) does not change any row's result
   a.interleave = tune().out_interleave;
-  a.NG = pick_groups(H, (long)B * a.Nc * 2, (tune().out_waves > 0 ? tune().out_waves : 1) * sms, OutSmem::MAX_HG, 8);
+  a.NG = pick_groups(H, (long)B * a.Nc * 2, (tune().out_waves > 0 ? tune().out_waves : 1) * sms, OutSmem::MAX_HG, SSQ_SLICE);
   a.HG = H / a.NG;
   REQUIRE(launch_pf(ssd_tc_out, dim3(B * a.Nc * 2 * a.NG), dim3(OUT_THREADS), OutSmem::TOTAL, st,
                      tm_act, tm_prev, tm_z, tm_u, a) == cudaSuccess,
           SSD200_ELAUNCH, "ssd_tc_out launch");
   LAUNCH_CHECK("ssd_tc_out");
-  *ng_out = (H / 8) * OUT_KW;  // sum u^2 partials per row, (8-head slice, column half)
+  *ng_out = (H / SSQ_SLICE) * OUT_KW;  // sum u^2 partials per row, (slice, column half)
   return SSD200_OK;
 }
 

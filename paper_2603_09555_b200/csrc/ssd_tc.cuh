@@ -40,7 +40,7 @@ struct TcSsdArgs {
   bf16 *prev;         // (B, Nc, H, N, P) bf16: state entering each chunk (transposed)
   float *final_state; // (B, H, P, N)
   bf16 *u_out;        // (rows, d_inner)
-  float *ssq;         // (H/8 * OUT_KW, rows) partial sums of u^2 per (8-head slice, column half)
+  float *ssq;         // (H/SSQ_SLICE * OUT_KW, rows) partial sums of u^2 per (head slice, column half)
 };
 
 __device__ __forceinline__ unsigned long long clk64() {

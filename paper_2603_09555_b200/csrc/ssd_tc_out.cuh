@@ -12,7 +12,7 @@
 //     Ydiag = M . X_h        (K = 128(R+1)), A operand read from TMEM   ssd.py:149
 //     Yoff  = C_R . prev_h^T (K = N = 128)                               ssd.py:196
 //     y = Ydiag + e^{cs_l} Yoff + D_h x;  u = y * silu(z);  sum u^2       model.py:166-167
-//   sum u^2 leaves as one partial per (8-head slice, column half) — independent of
+//   sum u^2 leaves as one partial per (SSQ_SLICE-head slice, column half) — independent of
 //   the head grouping, so the norm's row scale is batch-invariant.
 //
 // M lives in TMEM (tcgen05.st by the math warps, consumed as the A operand of
@@ -43,6 +43,10 @@ namespace ssd200 {
 #define SSD200_OUT_KW 2
 #endif
 constexpr int OUT_KW = SSD200_OUT_KW;  // math warps per TMEM lane quarter (2 or 4)
+// heads per sum-u^2 slice: head groups are whole slices, so the smallest group (and
+// hence the output kernel's parallelism at small B) is one slice — 2 keeps B = 1,
+// T = 2K at 256 CTAs for 32 heads; the out_proj then sums H / 2 * OUT_KW partials
+constexpr int SSQ_SLICE = 2;
 constexpr int OUT_CW = 32 / OUT_KW;    // columns of every 32-column M chunk per warp
 constexpr int OUT_MW = 4 * OUT_KW;     // math warps
 constexpr int OUT_EW = TC_P / OUT_KW;  // epilogue head columns per warp
@@ -409,8 +413,6 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
 #pragma unroll
       for (int cc = 0; cc < EW / 8; ++cc)
         zv[cc] = *reinterpret_cast<const uint4 *>(sm + OutSmem::Z0 + sw128_off(row, pc / 8 + cc));
-      __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(zfree);  // the next head's z may land now
       sm100::mbar_wait(&bar_y[buf], (i >> 1) & 1);  // MMA(i) done
       // D-skip x from the X tile the MMA just consumed (row l of the chunk); u later
       // overwrites the same positions and leaves from there, so the tile is released
@@ -453,9 +455,14 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
           *reinterpret_cast<uint4 *>(xt + sw128_off(row, pc / 8 + 2 * hs + k)) =
               make_uint4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
       }
+      // z is consumed (every zv register fed the math above, so the loads are done):
+      // the next head's z may land.  Releasing right after the loads let the TMA
+      // overwrite the tile before a delayed LDS had read it (1 in ~15 runs differed).
+      sm100::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(zfree);
       // the quarter's 32 x 64 u tile leaves through TMA (rows past T are clipped);
       // the X buffer is released once the store has read it
-      sm100::fence_proxy_async();
       named_bar(4 + q, 32 * OUT_KW);
       if (kw == 0 && lane == 0) {
         sm100::tma_store_3d(&tm_u, xt + q * 4096, h * TC_P, c * TC_L + R * 128 + q * 32, b);
@@ -463,13 +470,13 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
         sm100::bulk_wait_read0();
         sm100::mbar_arrive(&xfree[buf]);
       }
-      // sum u^2 of this warp's columns over the 8-head slice that ends here:
+      // sum u^2 of this warp's columns over the SSQ_SLICE-head slice that ends here:
       // one partial per (slice, column half), slice-major (n_slices * OUT_KW, rows),
       // so the out_proj's row scale sums the same partials in the same order
       // whatever head grouping (and hence batch) this launch used
-      if ((i & 7) == 7) {
+      if (i % SSQ_SLICE == SSQ_SLICE - 1) {
         if (valid)
-          p.ssq[(long)(((h0 + i) >> 3) * OUT_KW + kw) * ((long)p.B * p.T) + (long)b * p.T + t] = ssq;
+          p.ssq[(long)(((h0 + i) / SSQ_SLICE) * OUT_KW + kw) * ((long)p.B * p.T) + (long)b * p.T + t] = ssq;
         ssq = 0.f;
       }
     }

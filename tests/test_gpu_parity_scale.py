@@ -184,3 +184,22 @@ def test_bf16_prefill_batch_invariance_production_width():
         assert torch.equal(part, full[lo:hi]), (lo, hi)
         assert torch.equal(pc.ssm_all, cache.ssm_all[:, lo:hi]), (lo, hi)
         assert torch.equal(pc.conv_all, cache.conv_all[:, lo:hi]), (lo, hi)
+
+
+def test_bf16_prefill_is_deterministic():
+    """Race detector: the same bf16 prefill repeated gives bitwise the same
+    residual stream and states.  (It caught a shared-memory buffer released by
+    an mbarrier arrive issued before the warp's loads from it had completed.)"""
+    import paper_2603_09555_b200 as m
+
+    cfg = m.named_config("370m", compute="bf16", vocab_size=512, n_layers=1)
+    params = m.from_reference(m.random_init_host(cfg, 91), cfg)
+    toks = torch.as_tensor(np.random.default_rng(92).integers(0, cfg.vocab_size, size=(4, 2048)),
+                           device="cuda")
+    _, c0, h0 = m.prefill(params, toks, cfg, logits="last", return_hidden=True)
+    h0, s0 = h0.clone(), c0.ssm_all.clone()
+    bad = 0
+    for _ in range(40):
+        _, c, h = m.prefill(params, toks, cfg, logits="last", return_hidden=True)
+        bad += int(not (torch.equal(h, h0) and torch.equal(c.ssm_all, s0)))
+    assert bad == 0, f"{bad} of 40 repeats differ"
