@@ -1282,8 +1282,12 @@ int head_bf16(const ssd200_dims_t *d, int V, const float *hidden, long hrs, cons
   float *pv = cv.take<float>((size_t)rows * nparts);
   int *pi = cv.take<int>((size_t)rows * nparts);
   REQUIRE(cv.ok(), SSD200_EWORKSPACE, "head workspace %zu < %zu", ws_bytes, cv.used);
-  rmsnorm_rows<float, bf16><<<rows, 256, 0, st>>>(hidden, hrs, fw, normed, d->d_model,
-                                                  d->d_model, (float)d->norm_eps);
+  {  // PDL: the norm's launch overlaps the last layer's finish (it waits for it)
+    cudaError_t e = launch_pdl(rmsnorm_rows<float, bf16>, dim3(rows), dim3(256), 0, st, hidden,
+                               (long)hrs, fw, normed, (long)d->d_model, d->d_model,
+                               (float)d->norm_eps);
+    REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "rmsnorm_rows: %s", cudaGetErrorString(e));
+  }
   LAUNCH_CHECK("rmsnorm_rows");
   if (rows <= 256 && tune().dec_swap && d->d_model % 8 == 0) {
     // decode batches: the embedding streamed once as the UMMA M side (decode_gemm.cuh)

@@ -599,6 +599,8 @@ __global__ __launch_bounds__(256) void gated_norm_kernel(const T *__restrict__ y
                                                          TO *__restrict__ out, long ldo, int D,
                                                          T eps) {
   __shared__ T red[32];
+  griddep_wait();  // no-op unless launched as a programmatic dependent (the bf16 head)
+  griddep_launch();
   const long r = blockIdx.x;
   T ss = T(0);
   for (int c = threadIdx.x; c < D; c += blockDim.x) {
@@ -619,6 +621,8 @@ __global__ __launch_bounds__(256) void rmsnorm_rows(const T *__restrict__ x, lon
                                                     const T *__restrict__ w,
                                                     TO *__restrict__ out, long ldo, int D, T eps) {
   __shared__ T red[32];
+  griddep_wait();  // no-op unless launched as a programmatic dependent (the bf16 head)
+  griddep_launch();
   const long r = blockIdx.x;
   T ss = T(0);
   for (int c = threadIdx.x; c < D; c += blockDim.x) {
