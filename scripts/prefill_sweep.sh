@@ -4,9 +4,9 @@
 set -u
 for T in 2048 4096 8192 16384; do
   for B in 1 2 4 8; do
-    timeout 300 python bench.py --model 370m --batch $B --seqlen $T --no-decode --no-cpu \
+    timeout 300 python bench.py --model 370m --batch $B --seqlen $T --no-decode --no-cpu --no-c2 \
       --steps 5 --warmup 3 > gpurun_out/sweep_370m_B${B}_T${T}.json 2>/dev/null
   done
 done
-timeout 600 python bench.py --model 2.7b --batch 4 --seqlen 8192 --no-decode --no-cpu \
+timeout 600 python bench.py --model 2.7b --batch 4 --seqlen 8192 --no-decode --no-cpu --no-c2 \
   --steps 5 --warmup 3 > gpurun_out/sweep_2p7b_B4_T8192.json 2>/dev/null
