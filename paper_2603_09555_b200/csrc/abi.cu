@@ -232,7 +232,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
                        cudaStream_t st, Args... args) {
   return launch_ex(tune().dec_pdl, kern, grid, block, smem, st, args...);
 }
-// prefill kernels: PDL per option 5
+// prefill kernels: PDL per ssd200_tuning_t.prefill_pdl
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pf(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                       cudaStream_t st, Args... args) {

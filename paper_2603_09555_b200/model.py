@@ -203,7 +203,10 @@ def block_forward(layer: LayerParams, hidden, cfg: ModelConfig, audit: PolicyAud
     if h.dim() != 3 or h.shape[-1] != cfg.d_model:
         raise ValueError(f"hidden must be (B, T, {cfg.d_model}), got {tuple(h.shape)}")
     B, T, _ = h.shape
-    params = ModelParams(embedding=layer.W_in, layers=[layer], final_norm_w=layer.norm_w, mode=cfg.policy.compute)
+    # the layer's own upload mode (its W_in dtype), so a layer/cfg mismatch raises in
+    # _Runner instead of running kernels on the wrong layout; only the layer is used
+    mode = {torch.bfloat16: "bf16", torch.float32: "f32", torch.float64: "f64"}[layer.W_in.dtype]
+    params = ModelParams(embedding=layer.W_in, layers=[layer], final_norm_w=layer.norm_w, mode=mode)
     r = _Runner(params, cfg)
     lp = h.to(torch.bfloat16) if cfg.policy.compute == "bf16" else None
     sdt = state_dtype(cfg)
