@@ -481,6 +481,8 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
       }
     }
   }
+  if (warp >= 2 && (warp - 2) < 4 && lane == 0)  // kw == 0: the u stores have completed
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
     __syncwarp();
