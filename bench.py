@@ -451,6 +451,28 @@ def run_prefill(args, rank, world, local):
         "avg_launch_ms": launch_ms,
         "peak_source": pk["source"] + ", sustained (kernel timed inside a long step)",
     }
+    # every phase against its own roofline: the GEMMs against the tensor peak, conv
+    # and the SSD scan against HBM by their algorithmic bytes (cost.bytes_prefill_layer),
+    # the scan also by the reference FLOP formula (what round 1 reported)
+    pb = m.cost.bytes_prefill_layer(cfg, T, B)
+    per_phase = {}
+    for p_, name in enumerate(PHASES):
+        t_launch = phase_ms[p_] / L / 1e3
+        if t_launch <= 0 or name == "gated_norm":
+            continue
+        e = {"ms_per_launch": t_launch * 1e3}
+        if name in ("in_proj", "out_proj"):
+            tf = phase_flops[p_] / t_launch / 1e12
+            e.update(bound="tensor", achieved=tf, unit="TFLOP/s", frac=tf / peak)
+        else:
+            gb = pb[name] / t_launch / 1e9
+            e.update(bound="hbm", achieved=gb, unit="GB/s", frac=gb / pk["hbm_gbs"],
+                     algorithmic_bytes_per_launch=pb[name])
+            if name == "scan":
+                tf = phase_flops[p_] / t_launch / 1e12
+                e.update(formula_tflops=tf, formula_frac_of_tensor=tf / peak)
+        per_phase[name] = e
+    roof["phases"] = per_phase
     step_tflops = flops_step / (ms / 1e3) / 1e12  # this rank's work / its own time
     del params, dev_tok
     return {

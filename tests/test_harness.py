@@ -64,3 +64,19 @@ def test_harness_runs_on_device(tmp_path):
     harness.write_csv(rows, tmp_path / "r.csv")
     lines = (tmp_path / "r.csv").read_text().splitlines()
     assert lines[0] == cost.CostReport.CSV_HEADER_B200 and len(lines) == 5
+
+
+def test_prefill_phase_bytes():
+    """Algorithmic bytes of the HBM-bound prefill phases (bench.py's per-phase
+    rooflines): conv reads + writes xBC once; the scan reads x, z, B, C, dt and
+    writes u and the final state."""
+    from paper_2603_09555_b200 import cost, named_config
+
+    cfg = named_config("2.7b")
+    rows = 32 * 8192
+    b = cost.bytes_prefill_layer(cfg, 8192, 32)
+    assert b["conv"] == 2 * rows * cfg.conv_dim * 2
+    want = (rows * (2 * cfg.d_inner + 2 * cfg.d_state) * 2 + rows * cfg.n_heads * 4
+            + rows * cfg.d_inner * 2 + 32 * cfg.n_heads * cfg.head_dim * cfg.d_state * 4)
+    assert b["scan"] == want
+    assert cost.bytes_prefill_layer(cfg, 8192, 1)["conv"] * 32 == b["conv"]
