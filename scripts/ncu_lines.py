@@ -2,7 +2,7 @@
 line (needs -lineinfo and --import-source on), with each line's top stall
 reasons:
 
-    python scripts/ncu_lines.py report.ncu-rep kernel_regex [n]
+    python scripts/ncu_lines.py report.ncu-rep kernel_regex [n] [launch_skip]
 """
 import csv
 import io
@@ -12,8 +12,10 @@ from collections import defaultdict
 
 rep, kern = sys.argv[1], sys.argv[2]
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 25
+skip = sys.argv[4] if len(sys.argv) > 4 else "0"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass",
-                      "-k", f"regex:{kern}", "-c", "1"], capture_output=True, text=True).stdout
+                      "-k", f"regex:{kern}", "--launch-skip", skip, "-c", "1"],
+                     capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 fname, hdr, line, acc = None, None, None, {}
 reasons = defaultdict(lambda: defaultdict(int))
