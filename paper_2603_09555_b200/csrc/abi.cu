@@ -375,6 +375,9 @@ int check_dims(const ssd200_dims_t *d) {
   REQUIRE(d->n_heads * d->head_dim == d->d_inner, SSD200_EINVAL, "n_heads*head_dim != d_inner");
   REQUIRE(d->n_heads % d->n_groups == 0, SSD200_EINVAL, "n_heads %% n_groups != 0");
   REQUIRE(d->conv_kernel <= 16, SSD200_EUNSUPPORTED, "conv_kernel > 16");
+  REQUIRE(!d->tuning || d->tuning->size == (int)sizeof(ssd200_tuning_t), SSD200_EINVAL,
+          "tuning.size %d != sizeof(ssd200_tuning_t) %d (header / library mismatch)",
+          d->tuning->size, (int)sizeof(ssd200_tuning_t));
   return SSD200_OK;
 }
 

@@ -33,7 +33,7 @@ def _step_into(r: _Runner, cfg, tok, cache_in: Mamba2Cache, cache_out: Mamba2Cac
                logits=None, argmax=None, chained: bool = True):
     B = tok.shape[0]
     hidden, lp = r.embed(tok)
-    if chained:  # all layers in one call (bf16: each in_proj applies the previous update)
+    if chained:  # all layers in one ABI call
         r.decode_layers(hidden, lp, cache_in.ssm_all, cache_out.ssm_all, cache_in.conv_all,
                         cache_out.conv_all, B)
     else:

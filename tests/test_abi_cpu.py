@@ -70,6 +70,13 @@ def test_tuning_is_per_call_not_global():
     with pytest.raises(ValueError):
         with _abi.tuning(no_such_field=1):
             pass
+    # a tuning struct from another header version is refused, not silently ignored
+    bad = _abi.default_tuning()
+    bad.size = ctypes.sizeof(_abi.Tuning) - 4
+    d2 = dims_struct(cfg)
+    d2.tuning = ctypes.pointer(bad)
+    assert lib.ssd200_decode_layer_workspace(d2, 8) == 0
+    assert "tuning.size" in _abi.last_error()
 
 
 def test_workspace_queries_are_pure_host():
