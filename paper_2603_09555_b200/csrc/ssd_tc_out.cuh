@@ -39,10 +39,9 @@
 
 namespace ssd200 {
 
-#ifndef SSD200_OUT_KW
-#define SSD200_OUT_KW 2
-#endif
-constexpr int OUT_KW = SSD200_OUT_KW;  // math warps per TMEM lane quarter (2 or 4)
+// math warps per TMEM lane quarter: 8 math warps at 168 registers fill most of the
+// register file (16 would leave 113 registers per thread)
+constexpr int OUT_KW = 2;
 // heads per sum-u^2 slice: head groups are whole slices, so the smallest group (and
 // hence the output kernel's parallelism at small B) is one slice — 2 keeps B = 1,
 // T = 2K at 256 CTAs for 32 heads; the out_proj then sums H / 2 * OUT_KW partials
@@ -247,17 +246,10 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
       const int h = h0 + i;
       const float *csg = p.cs + ((long)b * p.H + h) * csb + (long)c * TC_L;
       const float *dtg = p.dtT + ((long)b * p.H + h) * csb + (long)c * TC_L;
-      if constexpr (CL == 4) {
-        const float4 a = *reinterpret_cast<const float4 *>(csg + fcol);
-        const float4 d = *reinterpret_cast<const float4 *>(dtg + fcol);
-        f.cs[0] = a.x, f.cs[1] = a.y, f.cs[2] = a.z, f.cs[3] = a.w;
-        f.dt[0] = d.x, f.dt[1] = d.y, f.dt[2] = d.z, f.dt[3] = d.w;
-      } else {
-        const float2 a = *reinterpret_cast<const float2 *>(csg + fcol);
-        const float2 d = *reinterpret_cast<const float2 *>(dtg + fcol);
-        f.cs[0] = a.x, f.cs[1] = a.y;
-        f.dt[0] = d.x, f.dt[1] = d.y;
-      }
+      const float4 a = *reinterpret_cast<const float4 *>(csg + fcol);
+      const float4 d = *reinterpret_cast<const float4 *>(dtg + fcol);
+      f.cs[0] = a.x, f.cs[1] = a.y, f.cs[2] = a.z, f.cs[3] = a.w;
+      f.dt[0] = d.x, f.dt[1] = d.y, f.dt[2] = d.z, f.dt[3] = d.w;
       f.cr = csg[32 * fj + 31];
       f.csl = csg[l];
     };
@@ -295,8 +287,7 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
       }
     };
     auto st_m = [&](uint32_t taddr, const uint32_t (&pk)[CW / 2], bool on) {
-      if constexpr (CW == 16) sm100::tmem_st8_if(taddr, pk, on);
-      else sm100::tmem_st4_if(taddr, *reinterpret_cast<const uint32_t(*)[4]>(pk), on);
+      sm100::tmem_st8_if(taddr, pk, on);
     };
     // M = G * decay * dt for this warp's slice of head hh -> TMEM M buffer hh & 1.
     // The off-diagonal chunks are computed branch-free (NJ is a compile-time
@@ -366,9 +357,7 @@ __global__ void __launch_bounds__(OUT_THREADS, 1)
     for (int j = 0; j < 8; ++j) {
       if (j < nj && j <= jd) {
         uint32_t r[CW];
-        if constexpr (CW == 16) sm100::tmem_ld16(tmem + lane_off + TM_M + 32 * j + CW * kw, r);
-        else sm100::tmem_ld8(tmem + lane_off + TM_M + 32 * j + CW * kw,
-                             *reinterpret_cast<uint32_t(*)[8]>(r));
+        sm100::tmem_ld16(tmem + lane_off + TM_M + 32 * j + CW * kw, r);
         sm100::tmem_ld_wait();
 #pragma unroll
         for (int k = 0; k < CP; ++k) {
