@@ -16,7 +16,8 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libssd200.so")
+# SSD200_LIBRARY: another build of the same library (A/B of compile-time variants)
+LIB_PATH = os.environ.get("SSD200_LIBRARY") or os.path.join(_HERE, "libssd200.so")
 
 F32, F64, BF16 = 0, 1, 2
 DTYPE_CODE = {"f32": F32, "f64": F64, "bf16": BF16}
