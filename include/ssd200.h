@@ -71,6 +71,9 @@ typedef struct ssd200_tuning {
   int stream_cw;           /* decode state stream: consumer warps (8 or 16) */
   int out_interleave;      /* SSD output kernel: the two row tiles of a chunk run side by side (1) */
   int gemm_group_m;        /* prefill GEMM tile order: row blocks per group (0 auto, 1 row-major) */
+  int gemm_stream;         /* prefill GEMM epilogues: outputs and residual with evict-first (.cs)
+                              accesses, so they do not evict the operands' L2 reuse: 0 off,
+                              1 when the output exceeds 1 GB as f32 (1), 2 always */
 } ssd200_tuning_t;
 
 void ssd200_tuning_defaults(ssd200_tuning_t *t);

@@ -51,6 +51,7 @@ ssd200_tuning_t make_default_tuning() {
   t.stream_cw = 8;
   t.out_interleave = 1;
   t.gemm_group_m = 0;
+  t.gemm_stream = 1;
   return t;
 }
 const ssd200_tuning_t kDefaultTuning = make_default_tuning();
@@ -301,6 +302,12 @@ int tc_gemm(const bf16 *A, long lda, const bf16 *B, long ldb, int M, int N, int 
   // 24.8 -> 13.6 GB of DRAM traffic; row-major for narrow ones (out_proj)
   const int gm = tune().gemm_group_m;
   ep.group_m = gm > 0 ? gm : ((N + 255) / 256 > 16 ? 16 : 1);
+  // evict-first epilogue accesses once the output dwarfs L2 (>= 1 GB as f32): 2.7B at
+  // C4 +0.8 %, in_proj / out_proj DRAM reads 10.7 -> 9.9 / 12.2 -> 11.5 GB per launch;
+  // at 370M B = 4 (0.1-0.6 GB) the next kernel still finds part of the output in L2
+  // and evict-first measured -1 % (profiles/r02_prefill_ab_gemm_stream.txt)
+  ep.stream = tune().gemm_stream == 2 ||
+              (tune().gemm_stream == 1 && (double)M * N * 4.0 >= 1024.0 * 1024 * 1024);
   pdl = pdl && tune().dec_pdl;
   REQUIRE(M > 0 && N > 0 && K > 0, SSD200_EINVAL, "tc_gemm: empty problem");
   REQUIRE(K % 8 == 0, SSD200_EINVAL, "tc_gemm: K must be a multiple of 8");

@@ -57,7 +57,27 @@ struct TcEpilogue {
   int ksplit;
   long split_stride;
   int group_m;  // tile order: row blocks per group (<= 1: row-major), see tile_mn
+  int stream;   // outputs / residual with evict-first (.cs) accesses: at prefill sizes they
+                // have no L2 reuse, and plain ones evict the weight / activation tiles
+                // the other CTAs are about to re-read (2.7B out_proj: 16.2 GB DRAM per
+                // launch for 9.4 GB of operands and outputs)
 };
+
+__device__ __forceinline__ float4 ld_f4(const float *p, bool cs) {
+  return cs ? __ldcs(reinterpret_cast<const float4 *>(p)) : *reinterpret_cast<const float4 *>(p);
+}
+__device__ __forceinline__ void st_f4(float *p, float4 v, bool cs) {
+  if (cs) __stcs(reinterpret_cast<float4 *>(p), v);
+  else *reinterpret_cast<float4 *>(p) = v;
+}
+__device__ __forceinline__ void st_u2(void *p, uint2 v, bool cs) {
+  if (cs) __stcs(reinterpret_cast<uint2 *>(p), v);
+  else *reinterpret_cast<uint2 *>(p) = v;
+}
+__device__ __forceinline__ void st_u4(void *p, uint4 v, bool cs) {
+  if (cs) __stcs(reinterpret_cast<uint4 *>(p), v);
+  else *reinterpret_cast<uint4 *>(p) = v;
+}
 
 
 // PAIR: a CTA pair (cluster of 2, cta_group::2) computes a 256 x BN tile; each
@@ -367,8 +387,8 @@ __global__ void __launch_bounds__(320, 1)
                 const int mr = m_w + 8 * i + vr, n = n0 + 16 * h + vc;
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (mr < M && n < N)
-                  v = *reinterpret_cast<const float4 *>(
-                      reinterpret_cast<const float *>(ep.C) + (size_t)mr * ep.ldc + n);
+                  v = ld_f4(reinterpret_cast<const float *>(ep.C) + (size_t)mr * ep.ldc + n,
+                            ep.stream);
                 dst[16 * h + 4 * i + 0] = v.x;
                 dst[16 * h + 4 * i + 1] = v.y;
                 dst[16 * h + 4 * i + 2] = v.z;
@@ -419,11 +439,11 @@ __global__ void __launch_bounds__(320, 1)
                   o.y = hv[16 * h + 4 * i + 1] + __uint_as_float(xpb[rr * 17 + vc + 1]);
                   o.z = hv[16 * h + 4 * i + 2] + __uint_as_float(xpb[rr * 17 + vc + 2]);
                   o.w = hv[16 * h + 4 * i + 3] + __uint_as_float(xpb[rr * 17 + vc + 3]);
-                  *reinterpret_cast<float4 *>(C + (size_t)mr * ep.ldc + n) = o;
+                  st_f4(C + (size_t)mr * ep.ldc + n, o, ep.stream);
                   uint2 pk;
                   pk.x = pack_bf16x2(o.x, o.y);
                   pk.y = pack_bf16x2(o.z, o.w);
-                  *reinterpret_cast<uint2 *>(ep.C_lp + (size_t)mr * ep.ldc + n) = pk;
+                  st_u2(ep.C_lp + (size_t)mr * ep.ldc + n, pk, ep.stream);
                 }
               }
               __syncwarp();
@@ -463,7 +483,7 @@ __global__ void __launch_bounds__(320, 1)
               v.y = xpb[rr * 17 + vc + 1];
               v.z = xpb[rr * 17 + vc + 2];
               v.w = xpb[rr * 17 + vc + 3];
-              *reinterpret_cast<uint4 *>(C + (size_t)mr * ep.ldc + n0 + 2 * vc) = v;
+              st_u4(C + (size_t)mr * ep.ldc + n0 + 2 * vc, v, ep.stream);
             }
           }
           __syncwarp();
