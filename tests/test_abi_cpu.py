@@ -54,7 +54,8 @@ def test_tuning_is_per_call_not_global():
     lib = _abi.lib()
     t = _abi.default_tuning()
     assert t.size == ctypes.sizeof(_abi.Tuning)
-    assert (t.gemm_pair, t.prefill_pdl, t.dec_small_ring, t.stream_cw) == (1, 1, -1, 8)
+    assert (t.gemm_pair, t.prefill_pdl, t.dec_small_ring, t.stream_cw, t.gemm_stream) == \
+        (1, 1, -1, 8, 1)
     cfg = named_config("1.3b")
     base = lib.ssd200_decode_layer_workspace(dims_struct(cfg), 8)
     with _abi.tuning(dec_split_in=1, dec_split_out=1):

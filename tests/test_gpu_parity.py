@@ -513,6 +513,25 @@ def test_bf16_prefill_cta_pair_gemms_match(B, T):
     assert ((sa - sb).norm() / sa.norm()).item() <= 1e-3
 
 
+def test_bf16_prefill_gemm_cache_hints_are_bitwise_neutral():
+    """The GEMM epilogues' evict-first accesses (tuning gemm_stream: 0 off, 2
+    always) change only where lines live in L2, never the arithmetic: logits,
+    states and the residual stream bitwise equal."""
+    import paper_2603_09555_b200 as m
+    from paper_2603_09555_b200 import _abi
+
+    cfg = _bf16_cfg(vocab_size=2048, d_model=1024, n_layers=2)
+    params = m.from_reference(m.random_init_host(cfg, 75), cfg)
+    toks = np.random.default_rng(76).integers(0, cfg.vocab_size, size=(2, 1024))
+    outs = []
+    for hint in (0, 2):
+        with _abi.tuning(gemm_stream=hint):
+            lg, cache, hid = m.prefill(params, toks, cfg, logits="last", return_hidden=True)
+        outs.append((lg, cache.ssm_all.clone(), hid.clone()))
+    (la, sa, ha), (lb, sb, hb) = outs
+    assert torch.equal(la, lb) and torch.equal(sa, sb) and torch.equal(ha, hb)
+
+
 def test_generate_graph_cache_reuse_is_exact():
     """generate() keeps captured decode graphs across calls (decode._GRAPH_CACHE):
     a second call with another prompt through the cached graph must equal an
