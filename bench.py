@@ -53,7 +53,10 @@ import numpy as np  # noqa: E402
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-PHASES = ("in_proj", "conv", "scan", "gated_norm", "out_proj")
+# prefill layer phases as the library marks them (abi.cu PH_*): scan_states = chunk
+# cumsum + chunk walk, scan_out = the output kernel (intra + cross-chunk outputs, D
+# skip, gate; the gated norm's row scale is in the out_proj epilogue)
+PHASES = ("in_proj", "conv", "scan_states", "scan_out", "out_proj")
 
 
 def parse():
@@ -423,20 +426,22 @@ def run_prefill(args, rank, world, local):
     # dominant kernel: the phase with the largest share
     dom = int(np.argmax(phase_ms))
     per_layer = m.cost.flops_prefill_layer(cfg, T)
+    scan_flops = B * (per_layer["ssd_intra"] + per_layer["ssd_states"] + per_layer["ssd_inter"]
+                      + per_layer["ssd_cross"])
     phase_flops = {
         0: B * per_layer["in_proj"],
         1: B * per_layer["conv"],
-        2: B * (per_layer["ssd_intra"] + per_layer["ssd_states"] + per_layer["ssd_inter"] + per_layer["ssd_cross"]),
-        3: 0,
+        2: B * (per_layer["ssd_states"] + per_layer["ssd_inter"]),
+        3: B * (per_layer["ssd_intra"] + per_layer["ssd_cross"]),
         4: B * per_layer["out_proj"],
     }
     launch_ms = phase_ms[dom] / L
     achieved = phase_flops[dom] / (launch_ms / 1e3) / 1e12 if phase_flops[dom] else None
     peak = pk["bf16_tflops_sustained"]
-    kernel_key = {0: "tc_gemm_kernel<256,2>", 1: "conv_silu_tma", 2: "ssd_scan",
-                  3: "gated_norm_kernel", 4: "tc_gemm_kernel<256,4>"}[dom]
+    kernel_key = {0: "tc_gemm_kernel<256,2>", 1: "conv_silu_tma", 2: "ssd_tc_chunkscan",
+                  3: "ssd_tc_out", 4: "tc_gemm_kernel<256,4>"}[dom]
     kernel_name = {0: "tc_gemm_kernel<256, INPROJ, CTA pair>", 1: "conv_silu_tma",
-                   2: "ssd_tc_cumsum + ssd_tc_chunkscan + ssd_tc_out", 3: "-",
+                   2: "ssd_tc_cumsum + ssd_tc_chunkscan", 3: "ssd_tc_out",
                    4: "tc_gemm_kernel<256, RESID_NORM, CTA pair>"}[dom]
     roof = {
         "kernel": f"{PHASES[dom]} ({kernel_name})",
@@ -451,27 +456,36 @@ def run_prefill(args, rank, world, local):
         "avg_launch_ms": launch_ms,
         "peak_source": pk["source"] + ", sustained (kernel timed inside a long step)",
     }
-    # every phase against its own roofline: the GEMMs against the tensor peak, conv
-    # and the SSD scan against HBM by their algorithmic bytes (cost.bytes_prefill_layer),
-    # the scan also by the reference FLOP formula (what round 1 reported)
-    pb = m.cost.bytes_prefill_layer(cfg, T, B)
+    # every phase against its own roofline: the GEMMs against the tensor peak; conv and
+    # the two scan kernels against HBM by their operand bytes (cost.bytes_prefill_layer,
+    # cost.bytes_scan_kernels); the whole scan (both kernels) by its algorithmic bytes
+    # and the reference FLOP formula (what round 1 reported)
+    pb = dict(m.cost.bytes_prefill_layer(cfg, T, B))
+    pb.update(m.cost.bytes_scan_kernels(cfg, T, B))
     per_phase = {}
+
+    def hbm_entry(t_launch, nbytes):
+        gb = nbytes / t_launch / 1e9
+        return {"ms_per_launch": t_launch * 1e3, "bound": "hbm", "achieved": gb, "unit": "GB/s",
+                "frac": gb / pk["hbm_gbs"], "bytes_per_launch": nbytes}
+
     for p_, name in enumerate(PHASES):
         t_launch = phase_ms[p_] / L / 1e3
-        if t_launch <= 0 or name == "gated_norm":
+        if t_launch <= 0:
             continue
-        e = {"ms_per_launch": t_launch * 1e3}
         if name in ("in_proj", "out_proj"):
             tf = phase_flops[p_] / t_launch / 1e12
-            e.update(bound="tensor", achieved=tf, unit="TFLOP/s", frac=tf / peak)
+            per_phase[name] = {"ms_per_launch": t_launch * 1e3, "bound": "tensor",
+                               "achieved": tf, "unit": "TFLOP/s", "frac": tf / peak}
         else:
-            gb = pb[name] / t_launch / 1e9
-            e.update(bound="hbm", achieved=gb, unit="GB/s", frac=gb / pk["hbm_gbs"],
-                     algorithmic_bytes_per_launch=pb[name])
-            if name == "scan":
-                tf = phase_flops[p_] / t_launch / 1e12
-                e.update(formula_tflops=tf, formula_frac_of_tensor=tf / peak)
-        per_phase[name] = e
+            per_phase[name] = hbm_entry(t_launch, pb[name])
+    t_scan = (phase_ms[2] + phase_ms[3]) / L / 1e3
+    if t_scan > 0:
+        e = hbm_entry(t_scan, pb["scan"])
+        e.update(formula_tflops=scan_flops / t_scan / 1e12,
+                 formula_frac_of_tensor=scan_flops / t_scan / 1e12 / peak,
+                 note="both scan kernels; algorithmic bytes (x, z, B, C, dt in; u, state out)")
+        per_phase["scan"] = e
     roof["phases"] = per_phase
     step_tflops = flops_step / (ms / 1e3) / 1e12  # this rank's work / its own time
     del params, dev_tok

@@ -66,7 +66,11 @@ struct TuneScope {
   ~TuneScope() { g_tune = prev; }
 };
 
-enum { PH_IN_PROJ = 0, PH_CONV = 1, PH_SCAN = 2, PH_NORM = 3, PH_OUT_PROJ = 4 };
+// bench phases of a prefill layer.  PH_SCAN: the chunk states (tensor-core path:
+// cumsum + chunk walk) or the whole SIMT scan; PH_GATE: the gated output — the
+// tensor-core output kernel (intra-chunk + cross-chunk outputs, D skip, gate) or
+// the SIMT gated norm
+enum { PH_IN_PROJ = 0, PH_CONV = 1, PH_SCAN = 2, PH_GATE = 3, PH_OUT_PROJ = 4 };
 
 inline void phase_mark(int p, int end, cudaStream_t st) {
   if (g_phase_ev && p < g_nphase)
@@ -522,6 +526,7 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
   if (rc) return rc;
   const long sms = num_sms();
   // chunk cumsums
+  phase_mark(PH_SCAN, 0, st);
   REQUIRE(launch_pf(ssd_tc_cumsum, dim3(B * a.Nc, (H + 7) / 8), dim3(256), 0, st, a) ==
               cudaSuccess,
           SSD200_ELAUNCH, "ssd_tc_cumsum launch");
@@ -563,16 +568,19 @@ int run_tc_scan(const ssd200_dims_t *d, const ssd200_layer_t *w, const bf16 *act
             SSD200_ELAUNCH, "ssd_tc_pass launch");
     LAUNCH_CHECK("ssd_tc_pass");
   }
+  phase_mark(PH_SCAN, 1, st);
   // outputs (+ D skip + gate)
   // head groups of whole SSQ_SLICE-head slices: sum u^2 leaves per slice, so the grouping
   // (which depends on B) does not change any row's result
   a.interleave = tune().out_interleave;
   a.NG = pick_groups(H, (long)B * a.Nc * 2, (tune().out_waves > 0 ? tune().out_waves : 1) * sms, OutSmem::MAX_HG, SSQ_SLICE);
   a.HG = H / a.NG;
+  phase_mark(PH_GATE, 0, st);
   REQUIRE(launch_pf(ssd_tc_out, dim3(B * a.Nc * 2 * a.NG), dim3(OUT_THREADS), OutSmem::TOTAL, st,
                      tm_act, tm_prev, tm_z, tm_u, a) == cudaSuccess,
           SSD200_ELAUNCH, "ssd_tc_out launch");
   LAUNCH_CHECK("ssd_tc_out");
+  phase_mark(PH_GATE, 1, st);
   *ng_out = (H / SSQ_SLICE) * OUT_KW;  // sum u^2 partials per row, (slice, column half)
   return SSD200_OK;
 }
@@ -806,13 +814,9 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
     float *ssq = reinterpret_cast<float *>(reinterpret_cast<char *>(o.y) +
                                            align_up((size_t)rows * d->d_inner * 2));
     int ng = 1;
-    phase_mark(PH_SCAN, 0, st);
     rc = run_tc_scan(d, w, act, wd.conv_dim, u, n_split, o.dt, ssm_out, u_gated, ssq, &ng, o.scan,
-                     B, Tn, st);
+                     B, Tn, st);  // marks PH_SCAN and PH_GATE
     if (rc) return rc;
-    phase_mark(PH_SCAN, 1, st);
-    phase_mark(PH_NORM, 0, st);
-    phase_mark(PH_NORM, 1, st);
     TcEpilogue er{};
     phase_mark(PH_OUT_PROJ, 0, st);
     if (partial) {  // this rank's share: unscaled partial + local sum u^2
@@ -864,13 +868,13 @@ int prefill_layer_bf16(const ssd200_dims_t *d, const ssd200_layer_t *w, float *h
   rc = run_scan<float, bf16>(sa, o.scan, o.scan_bytes, st);
   if (rc) return rc;
   phase_mark(PH_SCAN, 1, st);
-  phase_mark(PH_NORM, 0, st);
+  phase_mark(PH_GATE, 0, st);
   bf16 *normed = act;  // act is dead after the scan
   gated_norm_kernel<float, bf16, bf16><<<(unsigned)rows, 256, 0, st>>>(
       o.y, d->d_inner, u, n_split, nullptr /* norm_w folded into W_out */, normed, d->d_inner,
       d->d_inner, (float)d->norm_eps);
   LAUNCH_CHECK("gated_norm");
-  phase_mark(PH_NORM, 1, st);
+  phase_mark(PH_GATE, 1, st);
   TcEpilogue er{};
   er.C = hidden;
   er.ldc = d->d_model;

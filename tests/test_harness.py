@@ -80,3 +80,9 @@ def test_prefill_phase_bytes():
             + rows * cfg.d_inner * 2 + 32 * cfg.n_heads * cfg.head_dim * cfg.d_state * 4)
     assert b["scan"] == want
     assert cost.bytes_prefill_layer(cfg, 8192, 1)["conv"] * 32 == b["conv"]
+    # the two scan kernels' own operands: every algorithmic operand once, plus the
+    # split's intermediates (x read by both kernels, the bf16 chunk states, cs / dt^T)
+    k = cost.bytes_scan_kernels(cfg, 8192, 32)
+    prev = 32 * 32 * cfg.n_heads * cfg.head_dim * cfg.d_state * 2
+    assert k["scan_states"] + k["scan_out"] > b["scan"] + 2 * prev
+    assert 4.5e9 < k["scan_states"] < 4.7e9 and 9.7e9 < k["scan_out"] < 9.9e9  # ncu: 4.58 / 10.04 GB
