@@ -997,8 +997,9 @@ def run(args):
         del dparams
         torch.cuda.empty_cache()
     if rank == 0 and world == 1 and not args.no_cpu:
+        # two blocks: ~10 s of host work at 2.7B (one block took 4.8 s on the box)
         v, secs, desc = cpu_prefill_sample(args.model, T=min(args.cpu_seqlen, args.seqlen),
-                                           layers=1)
+                                           layers=2)
         cpu = {"value": v, "unit": "tok/s", "cores": _NCPU, "kind": "port", "sample": desc,
                "seconds": secs}
     if rank == 0:
