@@ -30,6 +30,8 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 # bench.py roofline keys -> kernel-name prefixes whose launches make up one unit
 GROUPS = {
     "ssd_scan": ("ssd_tc_cumsum", "ssd_tc_chunkscan", "ssd_tc_out"),
+    "ssd_tc_chunkscan": ("ssd_tc_cumsum", "ssd_tc_chunkscan"),  # bench phase scan_states
+    "ssd_tc_out": ("ssd_tc_out",),                                # bench phase scan_out
     "tc_gemm_kernel<256,2>": ("void tc_gemm_kernel<256, 2",),
     "tc_gemm_kernel<256,4>": ("void tc_gemm_kernel<256, 4",),
     "conv_silu_tma": ("conv_silu_tma",),

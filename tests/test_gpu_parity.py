@@ -493,7 +493,7 @@ def test_verify_suites_pass():
 
 @pytest.mark.parametrize("B,T", [(4, 4096)])
 def test_bf16_prefill_cta_pair_gemms_match(B, T):
-    """CTA-pair (cta_group::2) GEMMs for in_proj / out_proj (option 20) against
+    """CTA-pair (cta_group::2) GEMMs for in_proj / out_proj (tuning gemm_pair) against
     the single-CTA GEMMs on a production-width layer at a size where both
     take 256 x 256 pair tiles; the single-CTA path is the one pinned to the
     oracle above."""
