@@ -74,6 +74,9 @@ typedef struct ssd200_tuning {
   int gemm_stream;         /* prefill GEMM epilogues: outputs and residual with evict-first (.cs)
                               accesses, so they do not evict the operands' L2 reuse: 0 off,
                               1 when the output exceeds 1 GB as f32 (1), 2 always */
+  int stream_chunk;        /* decode state stream tile hand-out: 0 auto (once a CTA's fair share
+                              is >= 4 tiles, chunks of 1/12 of it, 1..8 tiles, from an atomic
+                              counter), -1 static contiguous ranges, > 0 tiles per chunk */
 } ssd200_tuning_t;
 
 void ssd200_tuning_defaults(ssd200_tuning_t *t);

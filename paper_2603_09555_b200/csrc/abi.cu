@@ -5,6 +5,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstring>
 #include <atomic>
 #include <mutex>
 #include <set>
@@ -29,6 +30,25 @@ thread_local uint64_t g_launches = 0;
 thread_local void *const *g_phase_ev = nullptr;  // bench instrumentation only
 thread_local int g_nphase = 0;
 
+// launch-timeline slots (SSD200_TRACE diagnostic builds; -1 otherwise)
+#ifdef SSD200_TRACE
+std::mutex g_trace_mu;
+int g_trace_next = 0;
+char g_trace_name[TRACE_SLOTS][32];
+int trace_slot(const char *name) {
+  std::lock_guard<std::mutex> lk(g_trace_mu);
+  if (g_trace_next >= TRACE_SLOTS) return -1;
+  snprintf(g_trace_name[g_trace_next], 32, "%s", name);
+  return g_trace_next++;
+}
+__global__ void trace_init_kernel() {
+  for (int i = threadIdx.x; i < TRACE_SLOTS; i += blockDim.x)
+    for (int k = 0; k < 6; ++k) g_trace[i][k] = (k & 1) ? 0ull : ~0ull;
+}
+#else
+inline int trace_slot(const char *) { return -1; }
+#endif
+
 // Implementation choices come with each call (ssd200_dims_t.tuning); TuneScope
 // makes them visible to the launch helpers for the duration of that call only.
 ssd200_tuning_t make_default_tuning() {
@@ -52,6 +72,7 @@ ssd200_tuning_t make_default_tuning() {
   t.out_interleave = 1;
   t.gemm_group_m = 0;
   t.gemm_stream = 1;
+  t.stream_chunk = 0;
   return t;
 }
 const ssd200_tuning_t kDefaultTuning = make_default_tuning();
@@ -893,6 +914,7 @@ template <typename T> struct DecodeWs {
   bf16 *normed_lp;
   float *part;       // wide-batch bf16: out_proj split-K partials
   float *ssq;        // wide-batch bf16: (B, H) sum u^2
+  unsigned *ctr;     // wide-batch bf16: the state stream's chunk counter
 };
 
 // split-K factors of the bf16 decode GEMMs: enough
@@ -947,6 +969,7 @@ bool carve_decode(const ssd200_dims_t *d, int B, void *ws, size_t cap, DecodeWs<
   o.u = cv.take<T>((size_t)sp.in * B * w.d_in_proj);
   o.part = big ? cv.take<float>((size_t)sp.out * B * d->d_model) : nullptr;
   o.ssq = big ? cv.take<float>((size_t)B * d->n_heads) : nullptr;
+  o.ctr = big ? cv.take<unsigned>(4) : nullptr;
   o.act = cv.take<T>((size_t)B * w.conv_dim);
   o.y = cv.take<T>((size_t)B * d->d_inner);
   o.normed_T = cv.take<T>((size_t)B * d->d_inner);
@@ -964,7 +987,7 @@ constexpr int GEMV_BF16_MAX_ROWS = 8;
 // weight-streaming swapped-operand GEMM (decode_gemm.cuh) for B <= 256, else tc_gemm
 template <int BNB, bool SMALL>
 int launch_dec_gemm_cfg(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long ldo,
-                        int ksplit, long split_stride, cudaStream_t st) {
+                        int ksplit, long split_stride, cudaStream_t st, unsigned *zero_ctr) {
   using Cfg = DgCfg<BNB, SMALL>;
   CUtensorMap tw, tx;
   int rc = make_map_2d(&tw, W, N, K, K, 128);
@@ -972,7 +995,7 @@ int launch_dec_gemm_cfg(const bf16 *W, int N, int K, const bf16 *X, int B, float
   rc = make_map_2d(&tx, X, B, K, K, BNB);
   if (rc) return rc;
   smem_attr(dec_gemm_swap<BNB, SMALL>, (int)Cfg::SMEM);
-  DgArgs a{N, K, B, ksplit, out, ldo, split_stride};
+  DgArgs a{N, K, B, ksplit, out, ldo, split_stride, zero_ctr, trace_slot("dec_gemm")};
   const int grid = ((N + 127) / 128) * ksplit;
   cudaError_t e =
       launch_pdl(dec_gemm_swap<BNB, SMALL>, dim3(grid), dim3(192), Cfg::SMEM, st, tw, tx, a);
@@ -982,25 +1005,27 @@ int launch_dec_gemm_cfg(const bf16 *W, int N, int K, const bf16 *X, int B, float
 }
 template <int BNB>
 int launch_dec_gemm_bnb(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long ldo,
-                        int ksplit, long split_stride, cudaStream_t st) {
+                        int ksplit, long split_stride, cudaStream_t st, unsigned *zero_ctr) {
   // the small ring (two CTAs per SM) measured faster up to B = 32 (B = 1: 1.18 -> 1.06 ms
   // with the in_proj split 4), slower from B = 64 (3.37 vs 3.47 ms) and at B = 256
   const bool small = tune().dec_small_ring < 0 ? B <= tune().dec_small_max : tune().dec_small_ring != 0;
   return small
-             ? launch_dec_gemm_cfg<BNB, true>(W, N, K, X, B, out, ldo, ksplit, split_stride, st)
-             : launch_dec_gemm_cfg<BNB, false>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
+             ? launch_dec_gemm_cfg<BNB, true>(W, N, K, X, B, out, ldo, ksplit, split_stride, st,
+                                              zero_ctr)
+             : launch_dec_gemm_cfg<BNB, false>(W, N, K, X, B, out, ldo, ksplit, split_stride, st,
+                                               zero_ctr);
 }
 
 int dec_gemm(const bf16 *W, int N, int K, const bf16 *X, int B, float *out, long ldo, int ksplit,
-             long split_stride, cudaStream_t st) {
+             long split_stride, cudaStream_t st, unsigned *zero_ctr = nullptr) {
   REQUIRE(ksplit >= 1 && ksplit <= (K + 63) / 64, SSD200_EINVAL, "dec_gemm: bad split");
   if (B <= 256 && tune().dec_swap) {
-    if (B <= 16) return launch_dec_gemm_bnb<16>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
-    if (B <= 32) return launch_dec_gemm_bnb<32>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
-    if (B <= 64) return launch_dec_gemm_bnb<64>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
+    if (B <= 16) return launch_dec_gemm_bnb<16>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, zero_ctr);
+    if (B <= 32) return launch_dec_gemm_bnb<32>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, zero_ctr);
+    if (B <= 64) return launch_dec_gemm_bnb<64>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, zero_ctr);
     if (B <= 128)
-      return launch_dec_gemm_bnb<128>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
-    return launch_dec_gemm_bnb<256>(W, N, K, X, B, out, ldo, ksplit, split_stride, st);
+      return launch_dec_gemm_bnb<128>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, zero_ctr);
+    return launch_dec_gemm_bnb<256>(W, N, K, X, B, out, ldo, ksplit, split_stride, st, zero_ctr);
   }
   TcEpilogue ep{};
   ep.C = out;
@@ -1037,8 +1062,10 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
       LAUNCH_CHECK("pre_norm");
       xin = static_cast<const bf16 *>(o.xn);
     }
+    // the in_proj zeroes the state stream's chunk counter after its own dependency
+    // wait (every earlier grab of it is then complete)
     int rc = dec_gemm(static_cast<const bf16 *>(w->W_in), (int)wd.d_in_proj, d->d_model, xin,
-                      B, o.u, wd.d_in_proj, sp.in, s_in, st);
+                      B, o.u, wd.d_in_proj, sp.in, s_in, st, o.ctr);
     if (rc) return rc;
   }
   DecStreamArgs sa{};
@@ -1068,6 +1095,8 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   sa.ssq = o.ssq;
   const DssLayout lay(d->head_dim, d->d_state, sp.in);
   sa.stage_bytes = lay.total;
+  sa.trace = trace_slot("dec_ssm_stream");
+  sa.trace2 = trace_slot("  stream phases");
   // CTAs per SM: two independent pipelines per SM (measured at 1.3B with the
   // small-ring decode GEMMs: B = 8 1.42 -> 1.29, B = 64 3.97 -> 3.51, B = 256
   // 12.1 -> 10.9 ms/step; neutral at B = 1, where there are fewer tiles than SMs)
@@ -1075,16 +1104,29 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   const int cps = tune().stream_cps == 1 ? 1
                   : tune().stream_cps == 2 ? 2
                   : (ntiles_all >= 2 * num_sms() ? 2 : 1);
-  int stages = (int)((cps == 2 ? 105u * 1024u : 214u * 1024u) / lay.total);
+  const uint32_t par_bytes = dss_par_bytes(d->n_heads, d->n_groups, d->d_state);
+  int stages = (int)((cps == 2 ? 105u * 1024u : 214u * 1024u) - par_bytes) / (int)lay.total;
   if (tune().stream_stages > 0 && tune().stream_stages < stages) stages = tune().stream_stages;
-  sa.stages = stages > DSS_MAX_STAGES ? DSS_MAX_STAGES : stages;
-  REQUIRE(sa.stages >= 2, SSD200_EUNSUPPORTED, "decode state tile too large for the smem ring");
-  const size_t smem = (size_t)sa.stages * lay.total;
-  cudaError_t e;
+  REQUIRE(stages >= 2, SSD200_EUNSUPPORTED, "decode state tile too large for the smem ring");
   const int ntiles = B * d->n_heads;
   const int grid = ntiles < cps * num_sms() ? ntiles : cps * num_sms();
-  REQUIRE((ntiles + grid - 1) / grid <= DSS_MAX_TILES, SSD200_EUNSUPPORTED,
-          "decode: %d state tiles per CTA exceed %d", (ntiles + grid - 1) / grid, DSS_MAX_TILES);
+  // no more stages than a CTA has tiles: at small batches (one tile per CTA) the
+  // ring then leaves the SM's shared memory to the out_proj CTAs that launch
+  // early and stream W_out while this grid runs
+  const int per_cta = (ntiles + grid - 1) / grid;
+  if (stages > per_cta) stages = per_cta;
+  sa.stages = stages > DSS_MAX_STAGES ? DSS_MAX_STAGES : stages;
+  const size_t smem = (size_t)sa.stages * lay.total + par_bytes;
+  cudaError_t e;
+  // tile hand-out: static ranges, or (wide batches) chunks from a counter the
+  // in_proj zeroes — only dec_gemm_swap does (B <= 256)
+  const bool can_dyn = B <= 256 && tune().dec_swap;
+  int chunk = 0;
+  if (tune().stream_chunk > 0) chunk = tune().stream_chunk;
+  else if (tune().stream_chunk == 0 && per_cta >= 4)  // 1.3B B = 256: 11.1 (static) -> 10.45 ms
+    chunk = per_cta / 12 < 1 ? 1 : (per_cta / 12 > 8 ? 8 : per_cta / 12);
+  sa.chunk = can_dyn ? chunk : 0;
+  sa.ctr = o.ctr;
   const int cw = tune().stream_cw == 16 ? 16 : 8;  // consumer warps
   const int nq = d->d_state <= 128 ? 1 : 2, rpw = d->head_dim / cw;
   e = cudaErrorInvalidValue;
@@ -1127,6 +1169,7 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   fa.pout = pout;
   fa.pld = pld;
   const int gbx = (d->d_model + 255) / 256 + (int)((wd.conv_dim - d->d_inner + 255) / 256);
+  fa.trace = trace_slot("dec_out_finish");
   e = launch_pdl(dec_out_finish, dim3(gbx, B), dim3(256), 0, st, fa);
   REQUIRE(e == cudaSuccess, SSD200_ELAUNCH, "dec_out_finish: %s", cudaGetErrorString(e));
   LAUNCH_CHECK("dec_out_finish");
@@ -1337,7 +1380,7 @@ int head_bf16(const ssd200_dims_t *d, int V, const float *hidden, long hrs, cons
 // =============================================================== C ABI
 extern "C" {
 
-int ssd200_abi_version(void) { return 3; }
+int ssd200_abi_version(void) { return 4; }
 
 void ssd200_tuning_defaults(ssd200_tuning_t *t) {
   if (t) *t = kDefaultTuning;
@@ -1630,5 +1673,33 @@ int ssd200_set_phase_events(void *const *events, int n_phases) {
   g_nphase = events ? n_phases : 0;
   return SSD200_OK;
 }
+
+#ifdef SSD200_TRACE
+// diagnostic builds: reset the device timeline (and, with reset_slots, the
+// slot counter: call before capturing / issuing the launches to trace)
+int ssd200_trace_reset(int reset_slots, ssd200_stream_t stream) {
+  if (reset_slots) {
+    std::lock_guard<std::mutex> lk(g_trace_mu);
+    g_trace_next = 0;
+  }
+  trace_init_kernel<<<1, 256, 0, (cudaStream_t)stream>>>();
+  return cudaGetLastError() == cudaSuccess ? SSD200_OK : SSD200_ELAUNCH;
+}
+// copies n = min(max_slots, used slots) rows of 6 timestamps (ns) and names
+// (32 chars each); returns n or < 0
+int ssd200_trace_read(unsigned long long *out, char *names, int max_slots) {
+  int n;
+  {
+    std::lock_guard<std::mutex> lk(g_trace_mu);
+    n = g_trace_next < max_slots ? g_trace_next : max_slots;
+    memcpy(names, g_trace_name, (size_t)n * 32);
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return SSD200_ELAUNCH;
+  if (cudaMemcpyFromSymbol(out, g_trace, (size_t)n * 6 * sizeof(unsigned long long)) !=
+      cudaSuccess)
+    return SSD200_ELAUNCH;
+  return n;
+}
+#endif
 
 }  // extern "C"

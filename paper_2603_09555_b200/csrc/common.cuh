@@ -76,6 +76,25 @@ __device__ __forceinline__ void griddep_launch() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Launch timeline probe (diagnostic builds only, -DSSD200_TRACE): per launch
+// slot, the earliest / latest %globaltimer at which a CTA entered (k = 0),
+// passed its dependency wait (k = 1) and left (k = 2).  Slots are handed out by
+// the host at launch time (ssd200_trace_*); -1 = not traced.
+#ifdef SSD200_TRACE
+constexpr int TRACE_SLOTS = 2048;
+__device__ unsigned long long g_trace[TRACE_SLOTS][6];
+__device__ __forceinline__ void trace_mark(int slot, int k) {
+  if (slot < 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  atomicMin(&g_trace[slot][2 * k], t);
+  atomicMax(&g_trace[slot][2 * k + 1], t);
+}
+#define SSD200_TRACE_MARK(slot, k) trace_mark((slot), (k))
+#else
+#define SSD200_TRACE_MARK(slot, k) ((void)0)
+#endif
+
 template <typename T> __device__ __forceinline__ T clamp_(T v, T lo, T hi) {
   return v < lo ? lo : (v > hi ? hi : v);
 }

@@ -58,23 +58,37 @@ __device__ __forceinline__ void mbar_wait_s(uint64_t *bar, uint32_t parity) {
 // weights), so the layer's middle is one streaming kernel.
 //
 // dec_ssm_stream: a persistent TMA pipeline over the (row, head) state tiles
-// (P x N f32 = 32 KB, contiguous in the cache).  One CTA per SM takes a
-// contiguous range of tiles.  A producer warp keeps S-1 tiles in flight with
-// cp.async.bulk — per tile: the state tile, the raw in_proj x / z / B / C
-// slices of every split-K partial, and the conv windows of the tile's x and
-// B / C channels — writes each updated tile back with a bulk store (in place)
-// and refills its stage.  Eight consumer warps, per tile:
+// (P x N f32 = 32 KB, contiguous in the cache).  A producer warp keeps S tiles
+// in flight with cp.async.bulk — per tile: the state tile, the raw in_proj
+// x / z / B / C slices of every split-K partial, the conv windows of the tile's
+// x and B / C channels and its x conv taps; the tile index, whether B / C are
+// new and the raw dt (summed over the partials by the producer's lanes) go in
+// the stage's header — and refills a stage as soon as its tile is done.  Tiles
+// come either as a contiguous static range per CTA or, at wide batches, as
+// chunks of consecutive tiles handed out by an atomic counter (the first chunk
+// of each CTA is static, so its state is requested before the dependency
+// wait): a static split leaves the CTAs that started late or share their SM
+// with a slower neighbour finishing up to ~18 % after the others (1.3B,
+// B = 256).  Which CTA updates a tile does not change its arithmetic.  Eight
+// consumer warps, per tile:
 //   conv taps + SiLU for the tile's x channels and its row's B / C channels
 //     (decode.py:103-108; the x windows are rolled here, each is owned by one
 //     tile; the shared B / C windows are rolled by dec_out_finish, after every
 //     tile has read them),
 //   h <- e^{a dt} h + dt x B ; y = C.h + D x ; u = y silu(z)      decode.py:111-133
-// all from shared memory.  dt = clip(softplus(dt_raw + dt_bias)) of all the
-// CTA's tiles is computed once up front.
+// all from shared memory; h leaves straight from registers (streaming stores).
+// The layer's per-head scalars and B / C conv taps are copied once per CTA.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
                "r"(static_cast<uint32_t>(__cvta_generic_to_shared(src))), "r"(bytes)
+               : "memory");
+}
+// expect tx bytes on the current phase without arriving
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+               "r"(bytes)
                : "memory");
 }
 
@@ -93,13 +107,19 @@ struct DecStreamArgs {
   float *ssq;      // (B, H)
   int stages;
   uint32_t stage_bytes;
+  // dynamic tile hand-out: chunk > 0 tiles per chunk, ctr = chunk counter (zeroed
+  // by this layer's in_proj after its own dependency wait); chunk = 0: static ranges
+  int chunk;
+  unsigned *ctr;
+  int trace;  // launch-timeline slot (SSD200_TRACE builds), -1 = none
+  int trace2; // consumer sub-phases: first tile landed, B / C conv done, last tile done
 };
 constexpr int DSS_MAX_STAGES = 8;
-constexpr int DSS_MAX_TILES = 512;  // tiles per CTA (dt table)
 
-// byte offsets inside a stage (nsplit raw partials of x, z, B, C; conv windows)
+// byte offsets inside a stage (nsplit raw partials of x, z, B, C; conv windows;
+// the x conv taps and biases of the tile's head)
 struct DssLayout {
-  uint32_t xr, zr, br, cr, xw, bw, cw, total;
+  uint32_t xr, zr, br, cr, xw, bw, cw, xcw, xcb, total;
   __host__ __device__ DssLayout(int P, int N, int ns) {
     xr = (uint32_t)P * N * 4;
     zr = xr + ns * P * 4;
@@ -108,9 +128,17 @@ struct DssLayout {
     xw = cr + ns * N * 4;
     bw = xw + P * 12;
     cw = bw + N * 12;
-    total = (cw + N * 12 + 127) & ~127u;
+    xcw = cw + N * 12;
+    xcb = xcw + P * 16;
+    total = (xcb + P * 4 + 127) & ~127u;
   }
 };
+// per-CTA parameter block behind the ring: dt_bias | a | D (H floats each,
+// padded to 16 B), then the B / C conv taps (2 G N float4) and biases (2 G N)
+__host__ __device__ inline uint32_t dss_par_scalars(int H) { return (3u * H * 4u + 15u) & ~15u; }
+__host__ __device__ inline uint32_t dss_par_bytes(int H, int G, int N) {
+  return dss_par_scalars(H) + 2u * G * N * 20u;
+}
 
 // sum_j p[j * stride] for j = 0 .. n-1, added in j order (the split-K partials'
 // fixed reduction order), with the first 16 loads issued together: a dependent
@@ -132,148 +160,222 @@ template <int NQ, int RPW, int CW>
 __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(DecStreamArgs a) {
   constexpr int CT = CW * 32;
   extern __shared__ __align__(128) uint8_t dsm[];
-  __shared__ __align__(8) uint64_t full[DSS_MAX_STAGES], done[DSS_MAX_STAGES];
+  __shared__ __align__(8) uint64_t full[DSS_MAX_STAGES], done[DSS_MAX_STAGES], pbar;
   __shared__ float red[DSS_MAX_STAGES][CW];
-  __shared__ float2 hdr[DSS_MAX_TILES];                   // (dt, e^{a dt}) per local tile
-  __shared__ __align__(16) float bcact[2][2 * 256];     // [B N | C N] per (row, group), double buffered
+  __shared__ int s_tile[DSS_MAX_STAGES];    // tile index (-1: no more tiles)
+  __shared__ int s_nbc[DSS_MAX_STAGES];     // the stage carries a new (row, group)'s B / C
+  __shared__ float s_raw[DSS_MAX_STAGES];   // dt_raw summed over the split-K partials
+  __shared__ __align__(16) float bcact[2][2 * 256];  // [B N | C N] per (row, group), double buffered
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int P = a.P, N = a.N, N4 = N >> 2, H = a.H, ns = a.nsplit;
+  if (threadIdx.x == 0) SSD200_TRACE_MARK(a.trace, 0);
+  const int P = a.P, N = a.N, N4 = N >> 2, H = a.H, G = a.G, ns = a.nsplit;
   const int ntiles = a.B * H;
-  const int t0 = (int)((long)ntiles * blockIdx.x / gridDim.x);
-  const int t1 = (int)((long)ntiles * (blockIdx.x + 1) / gridDim.x);
-  const int cnt = t1 - t0;
   const int S = a.stages;
   const DssLayout L(P, N, ns);
   const uint32_t tile_bytes = (uint32_t)P * N * 4;
-  // B / C (and their conv windows) only travel with the first tile of each (row, group)
-  const uint32_t in_bytes = tile_bytes + (uint32_t)ns * 2 * P * 4 + P * 12;
+  // per tile: state + x taps (requested early) and x / z partials + x windows; per new
+  // (row, group): B / C partials + windows
+  const uint32_t early_bytes = tile_bytes + P * 20;
+  const uint32_t rest_bytes = (uint32_t)ns * 2 * P * 4 + P * 12;
   const uint32_t bc_bytes = (uint32_t)ns * 2 * N * 4 + 2 * N * 12;
-  const int hpg = H / a.G;
-  auto bc_key = [&](int li) { const int t = t0 + li; return (t / H) * a.G + (t % H) / hpg; };
-  auto new_bc = [&](int li) { return li == 0 || bc_key(li) != bc_key(li - 1); };
+  const int hpg = H / G;
+  float *s_dtb = reinterpret_cast<float *>(dsm + (size_t)S * a.stage_bytes);
+  float *s_a = s_dtb + H, *s_D = s_dtb + 2 * H;
+  const float4 *s_bcw =
+      reinterpret_cast<const float4 *>(dsm + (size_t)S * a.stage_bytes + dss_par_scalars(H));
+  const float *s_bcb = reinterpret_cast<const float *>(s_bcw + 2 * G * N);
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init_s(&full[s], 1);
       mbar_init_s(&done[s], CW);
     }
+    mbar_init_s(&pbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // the state tile is independent of this step's earlier kernels (last written
-  // by this layer's previous step, which every PDL predecessor has transitively
-  // completed), so it is requested before griddepcontrol.wait ...
-  auto issue_state = [&](int li) {
-    uint64_t *bar = &full[li % S];
-    mbar_expect_s(bar, in_bytes + (new_bc(li) ? bc_bytes : 0u));
-    bulk_g2s(dsm + (size_t)(li % S) * a.stage_bytes, a.ssm_in + (size_t)(t0 + li) * P * N,
-             tile_bytes, bar);
-  };
-  // ... the in_proj partials and conv windows after it
-  auto issue_rest = [&](int li) {
-    const int t = t0 + li, b = t / H, h = t % H, g = h / (H / a.G);
-    uint8_t *st = dsm + (size_t)(li % S) * a.stage_bytes;
-    uint64_t *bar = &full[li % S];
-    const bool nbc = new_bc(li);
-    for (int j = 0; j < ns; ++j) {
-      const float *pr = a.proj + j * a.sstride + (size_t)b * a.ldp;
-      bulk_g2s(st + L.xr + j * P * 4, pr + a.d_inner + h * P, P * 4, bar);
-      bulk_g2s(st + L.zr + j * P * 4, pr + h * P, P * 4, bar);
-      if (nbc) {
-        bulk_g2s(st + L.br + j * N * 4, pr + 2 * a.d_inner + g * N, N * 4, bar);
-        bulk_g2s(st + L.cr + j * N * 4, pr + 2 * a.d_inner + a.G * N + g * N, N * 4, bar);
-      }
-    }
-    const float *cwin = a.conv_in + (size_t)b * a.conv_dim * 3;
-    bulk_g2s(st + L.xw, cwin + (size_t)h * P * 3, P * 12, bar);
-    if (nbc) {
-      bulk_g2s(st + L.bw, cwin + (size_t)(a.d_inner + g * N) * 3, N * 12, bar);
-      bulk_g2s(st + L.cw, cwin + (size_t)(a.d_inner + a.G * N + g * N) * 3, N * 12, bar);
-    }
-  };
   if (warp == CW) {
-    // ---------------- producer warp: loads, write-back, refills
+    // ---------------- producer warp: loads, refills (lane 0 issues, all lanes load dt)
+    // the tile sequence: static range [t0, t1), or chunk blockIdx.x, then grabbed chunks
+    const bool dyn = a.chunk > 0;
+    const int t0 = dyn ? blockIdx.x * a.chunk : (int)((long)ntiles * blockIdx.x / gridDim.x);
+    const int t1 = dyn ? min(ntiles, t0 + a.chunk)
+                       : (int)((long)ntiles * (blockIdx.x + 1) / gridDim.x);
+    int cur = t0, end = t1, prev_key = -1;
+    auto next_tile = [&](bool may_grab) -> int {
+      if (cur >= end) {
+        if (!dyn || !may_grab) return -1;
+        int c = 0;
+        if (lane == 0) c = (int)gridDim.x + (int)atomicAdd(a.ctr, 1u);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        cur = c * a.chunk;
+        end = min(ntiles, cur + a.chunk);
+        if (cur >= ntiles) {
+          cur = end = ntiles;
+          return -1;
+        }
+      }
+      return cur++;
+    };
+    // early part of a stage (no dependency on this step's earlier kernels): the
+    // state tile (last written by this layer's previous step) and the x taps
+    auto fill_early = [&](int s, int t) {
+      if (lane == 0) {
+        const int h = t % H;
+        uint8_t *st = dsm + (size_t)s * a.stage_bytes;
+        mbar_expect_tx_only(&full[s], early_bytes);
+        bulk_g2s(st, a.ssm_in + (size_t)t * P * N, tile_bytes, &full[s]);
+        bulk_g2s(st + L.xcw, a.conv_w + (size_t)h * P * 4, P * 16, &full[s]);
+        bulk_g2s(st + L.xcb, a.conv_b + (size_t)h * P, P * 4, &full[s]);
+      }
+    };
+    // the rest (after the dependency wait): in_proj partials, conv windows, dt_raw;
+    // the arrive publishes the stage header
+    auto fill_rest = [&](int s, int t) {
+      const int b = t / H, h = t % H, g = h / hpg, key = b * G + g;
+      const bool nbc = key != prev_key;
+      prev_key = key;
+      if (lane == 0) {
+        uint8_t *st = dsm + (size_t)s * a.stage_bytes;
+        uint64_t *bar = &full[s];
+        mbar_expect_tx_only(bar, rest_bytes + (nbc ? bc_bytes : 0u));
+        for (int j = 0; j < ns; ++j) {
+          const float *pr = a.proj + j * a.sstride + (size_t)b * a.ldp;
+          bulk_g2s(st + L.xr + j * P * 4, pr + a.d_inner + h * P, P * 4, bar);
+          bulk_g2s(st + L.zr + j * P * 4, pr + h * P, P * 4, bar);
+          if (nbc) {
+            bulk_g2s(st + L.br + j * N * 4, pr + 2 * a.d_inner + g * N, N * 4, bar);
+            bulk_g2s(st + L.cr + j * N * 4, pr + 2 * a.d_inner + G * N + g * N, N * 4, bar);
+          }
+        }
+        const float *cwin = a.conv_in + (size_t)b * a.conv_dim * 3;
+        bulk_g2s(st + L.xw, cwin + (size_t)h * P * 3, P * 12, bar);
+        if (nbc) {
+          bulk_g2s(st + L.bw, cwin + (size_t)(a.d_inner + g * N) * 3, N * 12, bar);
+          bulk_g2s(st + L.cw, cwin + (size_t)(a.d_inner + G * N + g * N) * 3, N * 12, bar);
+        }
+      }
+      // dt_raw: lane j loads split j, lane 0 adds them in split order (sum_splits' order)
+      float v = 0.f;
+      for (int j0 = 0; j0 < ns; j0 += 32) {
+        const int j = j0 + lane;
+        const float x = j < ns ? __ldcg(a.proj + (size_t)j * a.sstride + (size_t)b * a.ldp +
+                                        a.d_inner + a.conv_dim + h)
+                               : 0.f;
+        for (int q = 0; q < 32 && j0 + q < ns; ++q) v += __shfl_sync(0xffffffffu, x, q);
+      }
+      if (lane == 0) {
+        s_tile[s] = t;
+        s_nbc[s] = nbc ? 1 : 0;
+        s_raw[s] = v;
+        mbar_arrive_s(&full[s]);
+      }
+    };
+    auto fill_end = [&](int s) {
+      if (lane == 0) {
+        s_tile[s] = -1;
+        mbar_arrive_s(&full[s]);
+      }
+    };
     if (lane == 0) {
-      for (int li = 0; li < S && li < cnt; ++li) issue_state(li);
-      // let the out_proj launch now: its CTAs take the SMs this grid leaves free and
-      // stream W_out into their rings (they wait for this grid before reading u / ssq)
-      griddep_launch();
-      griddep_wait();  // the in_proj partials
-      for (int li = 0; li < S && li < cnt; ++li) issue_rest(li);
-      for (int li = 0; li < cnt; ++li) {
-        const int s = li % S;
-        mbar_wait_s(&done[s], (uint32_t)(li / S) & 1u);  // the consumer warps finished tile li
-        float tsum = 0.f;
-#pragma unroll
-        for (int w = 0; w < CW; ++w) tsum += red[s][w];  // fixed order: deterministic
-        a.ssq[t0 + li] = tsum;
-        if (li + S < cnt) {  // stage s is free: the consumers stored the tile from registers
-          issue_state(li + S);
-          issue_rest(li + S);
+      mbar_expect_s(&pbar, dss_par_bytes(H, G, N));
+      bulk_g2s(s_dtb, a.dt_bias, H * 4, &pbar);
+      bulk_g2s(s_a, a.a, H * 4, &pbar);
+      bulk_g2s(s_D, a.D, H * 4, &pbar);
+      bulk_g2s(const_cast<float4 *>(s_bcw), a.conv_w + (size_t)a.d_inner * 4, 2 * G * N * 16, &pbar);
+      bulk_g2s(const_cast<float *>(s_bcb), a.conv_b + a.d_inner, 2 * G * N * 4, &pbar);
+    }
+    int early[DSS_MAX_STAGES];
+    int npre = 0;
+    for (; npre < S; ++npre) {
+      early[npre] = next_tile(false);
+      if (early[npre] < 0) break;
+      fill_early(npre, early[npre]);
+    }
+    griddep_wait();  // the in_proj partials (and the zeroed chunk counter)
+    SSD200_TRACE_MARK(a.trace, 1);
+    int nissued = 0;
+    bool ended = false;
+    for (int s = 0; s < S && !ended; ++s) {
+      if (s < npre) {
+        fill_rest(s, early[s]);
+        ++nissued;
+      } else {
+        const int t = next_tile(true);
+        if (t < 0) {
+          fill_end(s);
+          ended = true;
+        } else {
+          fill_early(s, t);
+          fill_rest(s, t);
+          ++nissued;
         }
       }
     }
+    // let the out_proj launch once this CTA's first tile (the critical loads) has
+    // landed: its CTAs then stream W_out into their rings while this grid computes
+    // (they wait for this grid before reading u / ssq), instead of queueing their
+    // weight tiles ahead of these small loads on the same SMs
+    if (nissued > 0) mbar_wait_s(&full[0], 0);
+    griddep_launch();
+    for (int li = 0; li < nissued; ++li) {
+      const int s = li % S;
+      mbar_wait_s(&done[s], (uint32_t)(li / S) & 1u);  // the consumer warps finished tile li
+      if (lane == 0) {
+        float tsum = 0.f;
+#pragma unroll
+        for (int w = 0; w < CW; ++w) tsum += red[s][w];  // fixed order: deterministic
+        a.ssq[s_tile[s]] = tsum;
+      }
+      __syncwarp();
+      if (!ended) {  // stage s is free: the consumers stored the tile from registers
+        const int t = next_tile(true);
+        if (t < 0) {
+          fill_end(s);
+          ended = true;
+        } else {
+          fill_early(s, t);
+          fill_rest(s, t);
+          ++nissued;
+        }
+      }
+    }
+    if (lane == 0) SSD200_TRACE_MARK(a.trace, 2);
     return;
   }
   // ---------------- consumers
-  // the layer's parameters do not depend on the predecessor: pull the first tile's
-  // conv taps / biases and the per-head scalars into L1 while the in_proj drains
-  if (cnt > 0) {
-    const int h0 = t0 % H, g0 = h0 / hpg;
-    auto pf = [](const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); };
-    if (threadIdx.x < 2 * N) {
-      const int j = threadIdx.x, isc = j >= N;
-      const int ch = a.d_inner + (isc ? a.G * N : 0) + g0 * N + (isc ? j - N : j);
-      pf(a.conv_w + (size_t)ch * 4);
-      pf(a.conv_b + ch);
-    }
-    if (lane < RPW) {
-      const int ch = h0 * P + warp * RPW + lane;
-      pf(a.conv_w + (size_t)ch * 4);
-      pf(a.conv_b + ch);
-    }
-    if (threadIdx.x < cnt && threadIdx.x < CT) {
-      const int h = (t0 + threadIdx.x) % H;
-      pf(a.dt_bias + h);
-      pf(a.a + h);
-      pf(a.D + h);
-    }
-  }
-  // dt of every local tile first (decode.py:111-114)
-  griddep_wait();
-  for (int i = threadIdx.x; i < cnt; i += CT) {
-    const int t = t0 + i, b = t / H, h = t % H;
-    const float raw = sum_splits(a.proj + (size_t)b * a.ldp + a.d_inner + a.conv_dim + h,
-                                 a.sstride, ns);
-    const float dt = clamp_(softplus(raw + a.dt_bias[h]), a.dt_lo, a.dt_hi);
-    hdr[i] = make_float2(dt, expf(a.a[h] * dt));
-  }
-  named_barrier_sync(1, CT);
+  mbar_wait_s(&pbar, 0);
   int bce = 1;
-  for (int li = 0; li < cnt; ++li) {
+  for (int li = 0;; ++li) {
     const int s = li % S;
     uint8_t *st = dsm + (size_t)s * a.stage_bytes;
     mbar_wait_s(&full[s], (uint32_t)(li / S) & 1u);
-    const int t = t0 + li, b = t / H, h = t % H, g = h / hpg;
-    const bool nbc = new_bc(li);
+    if (threadIdx.x == 0 && li == 0) SSD200_TRACE_MARK(a.trace2, 0);
+    const int t = s_tile[s];
+    if (t < 0) break;
+    const int b = t / H, h = t % H, g = h / hpg;
+    const bool nbc = s_nbc[s] != 0;
     bce ^= nbc ? 1 : 0;
     float *bca = bcact[bce];
     if (nbc) {
       // the row's B / C channels (shared by every head of the group): conv taps
-      // (oldest first) + SiLU, once per (row, group) per CTA
+      // (oldest first) + SiLU, once per (row, group) in this CTA's tile sequence
       for (int j = threadIdx.x; j < 2 * N; j += CT) {
         const bool isc = j >= N;
         const int jj = isc ? j - N : j;
-        const int ch = a.d_inner + (isc ? a.G * N : 0) + g * N + jj;
+        const int pj = (isc ? G * N : 0) + g * N + jj;
         const float *rawp = reinterpret_cast<const float *>(st + (isc ? L.cr : L.br));
         float v = 0.f;
         for (int q = 0; q < ns; ++q) v += rawp[q * N + jj];
         const float *win = reinterpret_cast<const float *>(st + (isc ? L.cw : L.bw)) + jj * 3;
-        const float4 cwt = __ldg(reinterpret_cast<const float4 *>(a.conv_w) + ch);
-        bca[j] = silu(win[0] * cwt.x + win[1] * cwt.y + win[2] * cwt.z + v * cwt.w +
-                      __ldg(a.conv_b + ch));
+        const float4 cwt = s_bcw[pj];
+        bca[j] = silu(win[0] * cwt.x + win[1] * cwt.y + win[2] * cwt.z + v * cwt.w + s_bcb[pj]);
       }
       named_barrier_sync(1, CT);
     }
+    if (threadIdx.x == 0 && li == 0) SSD200_TRACE_MARK(a.trace2, 1);
+    // dt = clip(softplus(dt_raw + dt_bias)) and the decay e^{a dt} (decode.py:111-114)
+    const float dt = clamp_(softplus(s_raw[s] + s_dtb[h]), a.dt_lo, a.dt_hi);
+    const float decay = expf(s_a[h] * dt), Dh = s_D[h];
     // this warp's rows need only their own x and z: lanes 0..RPW-1 run the x conv
     // (and roll the x windows, which this tile owns: roll_and_insert, decode.py:65-69),
     // lanes 16..16+RPW-1 sum z over the split-K partials
@@ -284,9 +386,10 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
       float v = 0.f;
       for (int q = 0; q < ns; ++q) v += rawp[q * P + p];
       const float *win = reinterpret_cast<const float *>(st + L.xw) + p * 3;
-      const float4 cwt = __ldg(reinterpret_cast<const float4 *>(a.conv_w) + ch);
+      const float4 cwt = reinterpret_cast<const float4 *>(st + L.xcw)[p];
       const float w0 = win[0], w1 = win[1], w2 = win[2];
-      mine = silu(w0 * cwt.x + w1 * cwt.y + w2 * cwt.z + v * cwt.w + __ldg(a.conv_b + ch));
+      mine = silu(w0 * cwt.x + w1 * cwt.y + w2 * cwt.z + v * cwt.w +
+                  reinterpret_cast<const float *>(st + L.xcb)[p]);
       float *co = a.conv_out + ((size_t)b * a.conv_dim + ch) * 3;
       co[0] = w1;
       co[1] = w2;
@@ -303,7 +406,6 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
     float4 *ho = reinterpret_cast<float4 *>(a.ssm_out + (size_t)t * P * N);
     const float4 *bs = reinterpret_cast<const float4 *>(bca);
     const float4 *cs = reinterpret_cast<const float4 *>(bca + N);
-    const float dt = hdr[li].x, decay = hdr[li].y, Dh = __ldg(a.D + h);
     float4 bq[NQ], cq[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
@@ -317,7 +419,7 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
     for (int r = 0; r < RPW; ++r) {
       const int p = warp * RPW + r;
       const float dx = dt * xrow[r];
-      float t = 0.f;
+      float tt = 0.f;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         const int n4 = lane + 32 * q;
@@ -328,13 +430,13 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
           v.z = decay * v.z + dx * bq[q].z;
           v.w = decay * v.w + dx * bq[q].w;
           __stcs(ho + p * N4 + n4, v);  // streaming store straight from registers
-          t = fmaf(cq[q].x, v.x, t);
-          t = fmaf(cq[q].y, v.y, t);
-          t = fmaf(cq[q].z, v.z, t);
-          t = fmaf(cq[q].w, v.w, t);
+          tt = fmaf(cq[q].x, v.x, tt);
+          tt = fmaf(cq[q].y, v.y, tt);
+          tt = fmaf(cq[q].z, v.z, tt);
+          tt = fmaf(cq[q].w, v.w, tt);
         }
       }
-      acc[r] = t;
+      acc[r] = tt;
     }
     // y_p = C . h_p: reduce the RPW row sums over the 32 lanes
     float yv;
@@ -380,6 +482,7 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
     __syncwarp();
     if (lane == 0) mbar_arrive_s(&done[s]);
   }
+  if (threadIdx.x == 0) SSD200_TRACE_MARK(a.trace2, 2);
 }
 
 // hidden += rsqrt(sum_h ssq[b, h] / d_inner + eps) * sum_s part[s, b, :]
@@ -407,6 +510,7 @@ struct DecFinishArgs {
   // head-group-sharded mode: pout[b, :d_model] = partial, pout[b, d_model] = sum u^2
   float *pout;
   long pld;
+  int trace;  // launch-timeline slot (SSD200_TRACE builds), -1 = none
 };
 __global__ __launch_bounds__(256) void dec_out_finish(DecFinishArgs a) {
   __shared__ float sc;
@@ -417,8 +521,10 @@ __global__ __launch_bounds__(256) void dec_out_finish(DecFinishArgs a) {
   const long i = (long)b * a.d_model + n;
   // the next layer's in_proj may launch at once and prefetch its weights while the
   // out_proj drains (it waits for this grid before reading hidden_lp)
+  if (threadIdx.x == 0) SSD200_TRACE_MARK(a.trace, 0);
   griddep_launch();
   griddep_wait();  // the residual, the partials and sum u^2 are all predecessor outputs
+  if (threadIdx.x == 0) SSD200_TRACE_MARK(a.trace, 1);
   const float hold = (live && !a.pout) ? a.hidden_in[i] : 0.f;
   if ((int)blockIdx.x >= nb_h) {
     const int c = a.d_inner + ((int)blockIdx.x - nb_h) * 256 + threadIdx.x;  // B / C channel
@@ -452,6 +558,7 @@ __global__ __launch_bounds__(256) void dec_out_finish(DecFinishArgs a) {
   const float v = hold + sc * acc;
   a.hidden[i] = v;
   a.lp[i] = __float2bfloat16_rn(v);
+  if (threadIdx.x == 0) SSD200_TRACE_MARK(a.trace, 2);
 }
 
 // greedy pick over wide logits (decode.py:72-74, ties -> lowest id): grid

@@ -39,6 +39,8 @@ struct DgArgs {
   int ksplit;
   float *out;         // (ksplit, B, ldo)
   long ldo, split_stride;
+  unsigned *zero_ctr;  // in_proj: the state stream's chunk counter, zeroed after the wait
+  int trace;          // launch-timeline slot (SSD200_TRACE builds), -1 = none
 };
 
 template <int BNB, bool SMALL = false>
@@ -48,6 +50,7 @@ __global__ void __launch_bounds__(192, 1)
   using Cfg = DgCfg<BNB, SMALL>;
   constexpr int BK = Cfg::BK, STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
+  if (threadIdx.x == 0) SSD200_TRACE_MARK(a.trace, 0);
   uint8_t *smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sA = smem;
   uint8_t *sB = smem + STAGES * Cfg::A_BYTES;
@@ -84,7 +87,14 @@ __global__ void __launch_bounds__(192, 1)
         sm100::mbar_arrive_expect_tx(&full[i], Cfg::STAGE_BYTES);
         sm100::tma_load_2d(sA + i * Cfg::A_BYTES, &tmW, &full[i], (kb0 + i) * BK, n_blk * 128);
       }
+#ifdef SSD200_DEC_L2PF
+      // the k-blocks beyond the ring: into L2 now, so that after the wait they
+      // come from L2 rather than DRAM
+      for (int kb = kb0 + pre; kb < kb1; ++kb) sm100::tma_prefetch_l2_2d(&tmW, kb * BK, n_blk * 128);
+#endif
       griddep_wait();  // X comes from the predecessor (and out is free once it is done)
+      SSD200_TRACE_MARK(a.trace, 1);
+      if (a.zero_ctr && blockIdx.x == 0) *a.zero_ctr = 0u;
       for (int i = 0; i < pre; ++i)
         sm100::tma_load_2d(sB + i * Cfg::B_BYTES, &tmX, &full[i], (kb0 + i) * BK, 0);
       int s = pre % STAGES;
@@ -159,6 +169,7 @@ __global__ void __launch_bounds__(192, 1)
     sm100::tc_fence_after();
     sm100::tmem_dealloc<Cfg::TMEM_COLS>(tmem);
   }
+  if (threadIdx.x == 0) SSD200_TRACE_MARK(a.trace, 2);
 }
 
 }  // namespace ssd200

@@ -35,7 +35,7 @@ def test_abi_version_and_error_path_without_gpu():
     from paper_2603_09555_b200 import _abi
 
     lib = _abi.lib()
-    assert lib.ssd200_abi_version() == 3
+    assert lib.ssd200_abi_version() == 4
     # argument validation happens before any CUDA call
     rc = lib.ssd200_chunk_scan(0, None, None, None, None, None, None, None, None, None,
                                1, 1, 1, 1, 1, 1, 1, None, 0, None)
