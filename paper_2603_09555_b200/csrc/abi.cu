@@ -44,6 +44,7 @@ int trace_slot(const char *name) {
 __global__ void trace_init_kernel() {
   for (int i = threadIdx.x; i < TRACE_SLOTS; i += blockDim.x)
     for (int k = 0; k < 6; ++k) g_trace[i][k] = (k & 1) ? 0ull : ~0ull;
+  if (threadIdx.x < 16) g_cyc[threadIdx.x] = 0ull;
 }
 #else
 inline int trace_slot(const char *) { return -1; }
@@ -1699,6 +1700,11 @@ int ssd200_trace_read(unsigned long long *out, char *names, int max_slots) {
       cudaSuccess)
     return SSD200_ELAUNCH;
   return n;
+}
+int ssd200_trace_cycles(unsigned long long *out16) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return SSD200_ELAUNCH;
+  return cudaMemcpyFromSymbol(out16, g_cyc, 16 * sizeof(unsigned long long)) == cudaSuccess
+             ? SSD200_OK : SSD200_ELAUNCH;
 }
 #endif
 

@@ -91,8 +91,14 @@ __device__ __forceinline__ void trace_mark(int slot, int k) {
   atomicMax(&g_trace[slot][2 * k + 1], t);
 }
 #define SSD200_TRACE_MARK(slot, k) trace_mark((slot), (k))
+// per-phase SM-cycle sums (a kernel's own breakdown, summed over CTAs and launches)
+__device__ unsigned long long g_cyc[16];
+#define SSD200_CYC_ADD(k, v) atomicAdd(&g_cyc[(k)], (unsigned long long)(v))
+#define SSD200_CYC_NOW() clock64()
 #else
 #define SSD200_TRACE_MARK(slot, k) ((void)0)
+#define SSD200_CYC_ADD(k, v) ((void)0)
+#define SSD200_CYC_NOW() 0ll
 #endif
 
 template <typename T> __device__ __forceinline__ T clamp_(T v, T lo, T hi) {

@@ -164,7 +164,7 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
   __shared__ float red[DSS_MAX_STAGES][CW];
   __shared__ int s_tile[DSS_MAX_STAGES];    // tile index (-1: no more tiles)
   __shared__ int s_nbc[DSS_MAX_STAGES];     // the stage carries a new (row, group)'s B / C
-  __shared__ float s_raw[DSS_MAX_STAGES];   // dt_raw summed over the split-K partials
+  __shared__ float2 s_dt[DSS_MAX_STAGES];   // (dt, e^{a dt}) of the stage's tile
   __shared__ __align__(16) float bcact[2][2 * 256];  // [B N | C N] per (row, group), double buffered
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) SSD200_TRACE_MARK(a.trace, 0);
@@ -264,9 +264,12 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
         for (int q = 0; q < 32 && j0 + q < ns; ++q) v += __shfl_sync(0xffffffffu, x, q);
       }
       if (lane == 0) {
+        // dt = clip(softplus(dt_raw + dt_bias)) and the decay e^{a dt}, once per tile
+        // (decode.py:111-114); the layer's scalars have landed before any fill_rest
+        const float dt = clamp_(softplus(v + s_dtb[h]), a.dt_lo, a.dt_hi);
         s_tile[s] = t;
         s_nbc[s] = nbc ? 1 : 0;
-        s_raw[s] = v;
+        s_dt[s] = make_float2(dt, expf(s_a[h] * dt));
         mbar_arrive_s(&full[s]);
       }
     };
@@ -293,6 +296,7 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
     }
     griddep_wait();  // the in_proj partials (and the zeroed chunk counter)
     SSD200_TRACE_MARK(a.trace, 1);
+    mbar_wait_s(&pbar, 0);  // dt_bias / a for the tile headers
     int nissued = 0;
     bool ended = false;
     for (int s = 0; s < S && !ended; ++s) {
@@ -345,10 +349,12 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
   // ---------------- consumers
   mbar_wait_s(&pbar, 0);
   int bce = 1;
+  long long cy[6] = {0, 0, 0, 0, 0, 0}, ct = SSD200_CYC_NOW();
   for (int li = 0;; ++li) {
     const int s = li % S;
     uint8_t *st = dsm + (size_t)s * a.stage_bytes;
     mbar_wait_s(&full[s], (uint32_t)(li / S) & 1u);
+    { const long long c = SSD200_CYC_NOW(); cy[0] += c - ct; ct = c; }
     if (threadIdx.x == 0 && li == 0) SSD200_TRACE_MARK(a.trace2, 0);
     const int t = s_tile[s];
     if (t < 0) break;
@@ -368,14 +374,15 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
         for (int q = 0; q < ns; ++q) v += rawp[q * N + jj];
         const float *win = reinterpret_cast<const float *>(st + (isc ? L.cw : L.bw)) + jj * 3;
         const float4 cwt = s_bcw[pj];
-        bca[j] = silu(win[0] * cwt.x + win[1] * cwt.y + win[2] * cwt.z + v * cwt.w + s_bcb[pj]);
+        bca[j] = silu_fast(win[0] * cwt.x + win[1] * cwt.y + win[2] * cwt.z + v * cwt.w +
+                           s_bcb[pj]);
       }
       named_barrier_sync(1, CT);
     }
     if (threadIdx.x == 0 && li == 0) SSD200_TRACE_MARK(a.trace2, 1);
-    // dt = clip(softplus(dt_raw + dt_bias)) and the decay e^{a dt} (decode.py:111-114)
-    const float dt = clamp_(softplus(s_raw[s] + s_dtb[h]), a.dt_lo, a.dt_hi);
-    const float decay = expf(s_a[h] * dt), Dh = s_D[h];
+    { const long long c = SSD200_CYC_NOW(); cy[1] += c - ct; ct = c; }
+    const float2 dtd = s_dt[s];
+    const float dt = dtd.x, decay = dtd.y, Dh = s_D[h];
     // this warp's rows need only their own x and z: lanes 0..RPW-1 run the x conv
     // (and roll the x windows, which this tile owns: roll_and_insert, decode.py:65-69),
     // lanes 16..16+RPW-1 sum z over the split-K partials
@@ -388,8 +395,8 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
       const float *win = reinterpret_cast<const float *>(st + L.xw) + p * 3;
       const float4 cwt = reinterpret_cast<const float4 *>(st + L.xcw)[p];
       const float w0 = win[0], w1 = win[1], w2 = win[2];
-      mine = silu(w0 * cwt.x + w1 * cwt.y + w2 * cwt.z + v * cwt.w +
-                  reinterpret_cast<const float *>(st + L.xcb)[p]);
+      mine = silu_fast(w0 * cwt.x + w1 * cwt.y + w2 * cwt.z + v * cwt.w +
+                       reinterpret_cast<const float *>(st + L.xcb)[p]);
       float *co = a.conv_out + ((size_t)b * a.conv_dim + ch) * 3;
       co[0] = w1;
       co[1] = w2;
@@ -402,6 +409,7 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
     float xrow[RPW];
 #pragma unroll
     for (int r = 0; r < RPW; ++r) xrow[r] = __shfl_sync(0xffffffffu, mine, r);
+    { const long long c = SSD200_CYC_NOW(); cy[2] += c - ct; ct = c; }
     const float4 *hs = reinterpret_cast<const float4 *>(st);
     float4 *ho = reinterpret_cast<float4 *>(a.ssm_out + (size_t)t * P * N);
     const float4 *bs = reinterpret_cast<const float4 *>(bca);
@@ -438,6 +446,7 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
       }
       acc[r] = tt;
     }
+    { const long long c = SSD200_CYC_NOW(); cy[3] += c - ct; ct = c; }
     // y_p = C . h_p: reduce the RPW row sums over the 32 lanes
     float yv;
     int prow;
@@ -473,7 +482,7 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
     const float zv = __shfl_sync(0xffffffffu, mine, 16 + prow - warp * RPW);
     if (owner) {
       const float y = yv + Dh * xv;  // decode.py:132
-      const float uv = y * silu(zv);
+      const float uv = y * silu_fast(zv);
       a.u[(size_t)b * a.d_inner + h * P + prow] = __float2bfloat16_rn(uv);
       uu = uv * uv;
     }
@@ -481,8 +490,12 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
     if (lane == 0) red[s][warp] = uu;
     __syncwarp();
     if (lane == 0) mbar_arrive_s(&done[s]);
+    { const long long c = SSD200_CYC_NOW(); cy[4] += c - ct; ct = c; cy[5] += 1; }
   }
-  if (threadIdx.x == 0) SSD200_TRACE_MARK(a.trace2, 2);
+  if (threadIdx.x == 0) {
+    SSD200_TRACE_MARK(a.trace2, 2);
+    for (int k = 0; k < 6; ++k) SSD200_CYC_ADD(k, cy[k]);
+  }
 }
 
 // hidden += rsqrt(sum_h ssq[b, h] / d_inner + eps) * sum_s part[s, b, :]
@@ -538,11 +551,24 @@ __global__ __launch_bounds__(256) void dec_out_finish(DecFinishArgs a) {
     co[2] = v;
     return;
   }
-  // the split-K partials are requested before the row's norm reduction
+  // every load of the block in flight together: warp 0's sum u^2 terms (up to 8
+  // heads per lane, more in a second pass), then the split-K partials
+  constexpr int QH = 8;
+  float sq[QH];
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int k = 0; k < QH; ++k) {
+      const int h = threadIdx.x + 32 * k;
+      sq[k] = h < a.H ? a.ssq[(long)b * a.H + h] : 0.f;
+    }
+  }
   const float acc = live ? sum_splits(a.part + (long)b * a.d_model + n, a.sstride, a.nsplit) : 0.f;
   if (threadIdx.x < 32) {
     float t = 0.f;
-    for (int h = threadIdx.x; h < a.H; h += 32) t += a.ssq[(long)b * a.H + h];
+#pragma unroll
+    for (int k = 0; k < QH; ++k)
+      if (threadIdx.x + 32 * k < a.H) t += sq[k];
+    for (int h = threadIdx.x + 32 * QH; h < a.H; h += 32) t += a.ssq[(long)b * a.H + h];
     t = warp_sum(t);  // fixed shuffle tree: deterministic
     if (threadIdx.x == 0) {
       sc = 1.f / sqrtf(t * a.inv_d + a.eps);

@@ -87,11 +87,6 @@ __global__ void __launch_bounds__(192, 1)
         sm100::mbar_arrive_expect_tx(&full[i], Cfg::STAGE_BYTES);
         sm100::tma_load_2d(sA + i * Cfg::A_BYTES, &tmW, &full[i], (kb0 + i) * BK, n_blk * 128);
       }
-#ifdef SSD200_DEC_L2PF
-      // the k-blocks beyond the ring: into L2 now, so that after the wait they
-      // come from L2 rather than DRAM
-      for (int kb = kb0 + pre; kb < kb1; ++kb) sm100::tma_prefetch_l2_2d(&tmW, kb * BK, n_blk * 128);
-#endif
       griddep_wait();  // X comes from the predecessor (and out is free once it is done)
       SSD200_TRACE_MARK(a.trace, 1);
       if (a.zero_ctr && blockIdx.x == 0) *a.zero_ctr = 0u;

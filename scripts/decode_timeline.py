@@ -70,6 +70,14 @@ def run(args):
     step_ms = ev0.elapsed_time(ev1)
     n2 = lib.ssd200_trace_read(out.ctypes.data, names, n_max)
     assert n2 == n
+    cyc = np.zeros(16, dtype=np.uint64)
+    if hasattr(lib, "ssd200_trace_cycles"):
+        lib.ssd200_trace_cycles.argtypes = [ctypes.c_void_p]
+        lib.ssd200_trace_cycles(cyc.ctypes.data)
+        nt = max(int(cyc[5]), 1)
+        print(f"# state stream consumer (warp 0), SM cycles per tile over {nt} tiles: "
+              f"wait {cyc[0] / nt:.0f}, B/C conv {cyc[1] / nt:.0f}, x conv + z {cyc[2] / nt:.0f}, "
+              f"state rows {cyc[3] / nt:.0f}, y / u / done {cyc[4] / nt:.0f}")
     rows = out[per:n].astype(np.int64)
     names_c = nm[per:n]
     t0 = rows[:, 0].min()
