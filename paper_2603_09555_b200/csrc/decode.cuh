@@ -377,7 +377,6 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
         bca[j] = silu_fast(win[0] * cwt.x + win[1] * cwt.y + win[2] * cwt.z + v * cwt.w +
                            s_bcb[pj]);
       }
-      named_barrier_sync(1, CT);
     }
     if (threadIdx.x == 0 && li == 0) SSD200_TRACE_MARK(a.trace2, 1);
     { const long long c = SSD200_CYC_NOW(); cy[1] += c - ct; ct = c; }
@@ -406,6 +405,8 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
       const int p = warp * RPW + lane - 16;
       for (int q = 0; q < ns; ++q) mine += zr[q * P + p];
     }
+    // (the x conv above ran before this barrier, overlapping the other warps' B / C work)
+    if (nbc) named_barrier_sync(1, CT);
     float xrow[RPW];
 #pragma unroll
     for (int r = 0; r < RPW; ++r) xrow[r] = __shfl_sync(0xffffffffu, mine, r);
