@@ -21,14 +21,19 @@
 
 namespace ssd200 {
 
-// SMALL: a ~96 KB ring so that two CTAs (this GEMM's and the next kernel's)
+// SMALL: a ~100 KB ring so that two CTAs (this GEMM's and the next kernel's)
 // can share an SM and the next one's weight prefetch overlaps this one's tail
+// (104 KB: 5 stages at BNB <= 32; B = 32 2.22 -> 2.19 ms vs 96 KB, 110 KB (6
+// stages at BNB = 16) moved B = 1 / B = 8 by -1 % / +1 %)
+#ifndef SSD200_DEC_SMALL_KB
+#define SSD200_DEC_SMALL_KB 104u
+#endif
 template <int BNB, bool SMALL = false> struct DgCfg {
   static constexpr int BM = 128, BK = 64;
   static constexpr uint32_t A_BYTES = BM * BK * 2;   // 16 KB weight tile
   static constexpr uint32_t B_BYTES = BNB * BK * 2;  // activation tile
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr uint32_t BUDGET = SMALL ? 96u * 1024u : 192u * 1024u;
+  static constexpr uint32_t BUDGET = SMALL ? SSD200_DEC_SMALL_KB * 1024u : 192u * 1024u;
   static constexpr int STAGES = (int)(BUDGET / STAGE_BYTES) > 8 ? 8 : (int)(BUDGET / STAGE_BYTES);
   static constexpr int TMEM_COLS = BNB < 32 ? 32 : BNB;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
