@@ -780,3 +780,36 @@ def test_pre_norm_block_vs_oracle(comp):
         lp.pre_norm_w = None
     plain, _ = m.prefill(params, toks[:, :299], cfg)
     assert (plain - logits).abs().max().item() > 1e-3
+
+
+@pytest.mark.parametrize("B", [3, 160])
+def test_bf16_decode_groups_and_tile_handout(B):
+    """The decode state stream with n_groups = 2 (B / C shared by 4 of the 8 heads,
+    so a tile sequence crosses (row, group) boundaries inside a CTA) against the
+    oracle, at a small batch (static tile ranges) and at B = 160 (1280 tiles:
+    chunks handed out by the atomic counter).  Which CTA updates a tile must not
+    change its arithmetic: the dynamic hand-out is bitwise equal to static ranges
+    (tuning stream_chunk = -1) and to other chunk sizes."""
+    import paper_2603_09555_b200 as m
+    from paper_2603_09555_b200 import _abi
+
+    cfg = _bf16_cfg(n_groups=2, n_layers=1, vocab_size=512)
+    host = m.random_init_host(cfg, 81)
+    params = m.from_reference(host, cfg)
+    toks = np.random.default_rng(82).integers(0, cfg.vocab_size, size=(B, 12))
+    _, cache = m.prefill(params, toks[:, :11], cfg, logits=None)
+    sl, new = m.decode_step(params, cache, toks[:, 11], cfg)
+    rl, rs, rc = orc.prefill(orc.round_weights_bf16(host), toks, cfg.with_policy(compute="f32"))
+    rel = np.linalg.norm(_np(sl) - rl[:, -1]) / np.linalg.norm(rl[:, -1])
+    report("bf16_decode_groups_logits", rel=float(rel), B=B)
+    assert rel <= BF16_BOUND, rel
+    rs = np.stack(rs)
+    assert np.linalg.norm(_np(new.ssm_all) - rs) / np.linalg.norm(rs) <= BF16_STATE_BOUND
+    rc = np.stack(rc)
+    assert np.linalg.norm(_np(new.conv_all) - rc) / np.linalg.norm(rc) <= BF16_BOUND
+    for chunk in (-1, 1, 3):
+        with _abi.tuning(stream_chunk=chunk):
+            sl2, new2 = m.decode_step(params, cache, toks[:, 11], cfg)
+        assert torch.equal(sl2, sl), chunk
+        assert torch.equal(new2.ssm_all, new.ssm_all), chunk
+        assert torch.equal(new2.conv_all, new.conv_all), chunk
