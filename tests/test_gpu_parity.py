@@ -813,3 +813,18 @@ def test_bf16_decode_groups_and_tile_handout(B):
         assert torch.equal(sl2, sl), chunk
         assert torch.equal(new2.ssm_all, new.ssm_all), chunk
         assert torch.equal(new2.conv_all, new.conv_all), chunk
+
+
+def test_bf16_decode_counter_handout_graph_replays():
+    """The chunk counter of the state stream is zeroed by every layer's in_proj, so
+    replaying the captured token step (the counter is reused by every layer and
+    every step) gives the eager result bitwise, token for token."""
+    import paper_2603_09555_b200 as m
+
+    cfg = _bf16_cfg(n_layers=2, vocab_size=512)
+    params = m.from_reference(m.random_init_host(cfg, 91), cfg)
+    toks = np.random.default_rng(92).integers(0, cfg.vocab_size, size=(160, 10))
+    a = m.generate(params, toks, 6, cfg=cfg, use_graph=True, keep_logits=True)
+    b = m.generate(params, toks, 6, cfg=cfg, use_graph=False, keep_logits=True)
+    assert torch.equal(a.tokens, b.tokens)
+    assert torch.equal(a.per_step_logits, b.per_step_logits)
