@@ -77,6 +77,9 @@ typedef struct ssd200_tuning {
   int stream_chunk;        /* decode state stream tile hand-out: 0 auto (once a CTA's fair share
                               is >= 4 tiles, chunks of 1/12 of it, 1..8 tiles, from an atomic
                               counter), -1 static contiguous ranges, > 0 tiles per chunk */
+  int stream_reg_state;    /* decode state stream with one tile per CTA (2 B x H <= SMs, static
+                              tiles): the state rows go to registers at kernel entry, not through
+                              the smem ring (1) */
 } ssd200_tuning_t;
 
 void ssd200_tuning_defaults(ssd200_tuning_t *t);

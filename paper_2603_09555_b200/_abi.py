@@ -38,7 +38,7 @@ class Tuning(ctypes.Structure):
         "size", "prefill_pdl", "gemm_pair", "pair_min_tiles", "scan_variant",
         "chunkscan_multicast", "out_waves", "dec_pdl", "dec_swap", "dec_small_ring",
         "dec_small_max", "dec_split_in", "dec_split_out", "stream_stages", "stream_cps",
-        "stream_cw", "out_interleave", "gemm_group_m", "gemm_stream", "stream_chunk")]
+        "stream_cw", "out_interleave", "gemm_group_m", "gemm_stream", "stream_chunk", "stream_reg_state")]
 
 
 class Dims(ctypes.Structure):

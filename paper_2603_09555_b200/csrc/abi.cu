@@ -74,6 +74,7 @@ ssd200_tuning_t make_default_tuning() {
   t.gemm_group_m = 0;
   t.gemm_stream = 1;
   t.stream_chunk = 0;
+  t.stream_reg_state = 1;
   return t;
 }
 const ssd200_tuning_t kDefaultTuning = make_default_tuning();
@@ -1094,7 +1095,13 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   sa.ssm_out = ssm_out;
   sa.u = o.normed_lp;
   sa.ssq = o.ssq;
-  const DssLayout lay(d->head_dim, d->d_state, sp.in);
+  // one tile per CTA (static split) -> state in registers (see DecStreamArgs::reg_state);
+  // measured at 1.3B: B = 1 0.964 -> 0.945 ms, B = 2 (128 CTAs) 0.994 -> 1.001 ms, hence
+  // only while the tiles fill at most half of the SMs
+  const bool reg_state = tune().stream_reg_state && tune().stream_chunk <= 0 &&
+                         2 * B * d->n_heads <= num_sms();
+  sa.reg_state = reg_state ? 1 : 0;
+  const DssLayout lay(d->head_dim, d->d_state, sp.in, !reg_state);
   sa.stage_bytes = lay.total;
   sa.trace = trace_slot("dec_ssm_stream");
   sa.trace2 = trace_slot("  stream phases");

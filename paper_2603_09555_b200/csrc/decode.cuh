@@ -111,6 +111,11 @@ struct DecStreamArgs {
   // by this layer's in_proj after its own dependency wait); chunk = 0: static ranges
   int chunk;
   unsigned *ctr;
+  // one tile per CTA (small batches): the consumer threads load their state rows
+  // straight into registers at kernel entry, so the stage holds no state tile and
+  // the CTA is small enough to share an SM with two in_proj CTAs — it launches (and
+  // its state loads start) while the in_proj is still streaming weights
+  int reg_state;
   int trace;  // launch-timeline slot (SSD200_TRACE builds), -1 = none
   int trace2; // consumer sub-phases: first tile landed, B / C conv done, last tile done
 };
@@ -120,8 +125,9 @@ constexpr int DSS_MAX_STAGES = 8;
 // the x conv taps and biases of the tile's head)
 struct DssLayout {
   uint32_t xr, zr, br, cr, xw, bw, cw, xcw, xcb, total;
-  __host__ __device__ DssLayout(int P, int N, int ns) {
-    xr = (uint32_t)P * N * 4;
+  // with_state = false: the state tile is not staged (small batches keep it in registers)
+  __host__ __device__ DssLayout(int P, int N, int ns, bool with_state = true) {
+    xr = with_state ? (uint32_t)P * N * 4 : 0u;
     zr = xr + ns * P * 4;
     br = zr + ns * P * 4;
     cr = br + ns * N * 4;
@@ -171,11 +177,12 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
   const int P = a.P, N = a.N, N4 = N >> 2, H = a.H, G = a.G, ns = a.nsplit;
   const int ntiles = a.B * H;
   const int S = a.stages;
-  const DssLayout L(P, N, ns);
+  const bool regst = a.reg_state != 0;
+  const DssLayout L(P, N, ns, !regst);
   const uint32_t tile_bytes = (uint32_t)P * N * 4;
   // per tile: state + x taps (requested early) and x / z partials + x windows; per new
   // (row, group): B / C partials + windows
-  const uint32_t early_bytes = tile_bytes + P * 20;
+  const uint32_t early_bytes = (regst ? 0u : tile_bytes) + P * 20;
   const uint32_t rest_bytes = (uint32_t)ns * 2 * P * 4 + P * 12;
   const uint32_t bc_bytes = (uint32_t)ns * 2 * N * 4 + 2 * N * 12;
   const int hpg = H / G;
@@ -223,7 +230,7 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
         const int h = t % H;
         uint8_t *st = dsm + (size_t)s * a.stage_bytes;
         mbar_expect_tx_only(&full[s], early_bytes);
-        bulk_g2s(st, a.ssm_in + (size_t)t * P * N, tile_bytes, &full[s]);
+        if (!regst) bulk_g2s(st, a.ssm_in + (size_t)t * P * N, tile_bytes, &full[s]);
         bulk_g2s(st + L.xcw, a.conv_w + (size_t)h * P * 4, P * 16, &full[s]);
         bulk_g2s(st + L.xcb, a.conv_b + (size_t)h * P, P * 4, &full[s]);
       }
@@ -347,6 +354,18 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
     return;
   }
   // ---------------- consumers
+  float4 hreg[RPW][NQ];
+  if (regst) {  // this CTA's single tile (static split, one tile per CTA)
+    const int t = (int)((long)ntiles * blockIdx.x / gridDim.x);
+    if (t < (int)((long)ntiles * (blockIdx.x + 1) / gridDim.x)) {
+      const float4 *hg = reinterpret_cast<const float4 *>(a.ssm_in + (size_t)t * P * N);
+#pragma unroll
+      for (int r = 0; r < RPW; ++r)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+          if (lane + 32 * q < N4) hreg[r][q] = __ldcs(hg + (warp * RPW + r) * N4 + lane + 32 * q);
+    }
+  }
   mbar_wait_s(&pbar, 0);
   int bce = 1;
   long long cy[6] = {0, 0, 0, 0, 0, 0}, ct = SSD200_CYC_NOW();
@@ -433,7 +452,7 @@ __global__ __launch_bounds__(CW * 32 + 32, CW == 8 ? 2 : 1) void dec_ssm_stream(
       for (int q = 0; q < NQ; ++q) {
         const int n4 = lane + 32 * q;
         if (n4 < N4) {
-          float4 v = hs[p * N4 + n4];
+          float4 v = regst ? hreg[r][q] : hs[p * N4 + n4];
           v.x = decay * v.x + dx * bq[q].x;
           v.y = decay * v.y + dx * bq[q].y;
           v.z = decay * v.z + dx * bq[q].z;
