@@ -62,8 +62,8 @@ typedef struct ssd200_tuning {
   int out_waves;           /* output kernel: head groups until >= out_waves x SMs CTAs (1) */
   int dec_pdl;             /* PDL between the decode kernels (1) */
   int dec_swap;            /* decode GEMMs: swapped-operand weight-streaming kernel (1) or tc_gemm (0) */
-  int dec_small_ring;      /* [order] decode GEMMs: ~96 KB ring (1), 192 KB (0), -1 auto (B <= dec_small_max) */
-  int dec_small_max;       /* largest batch on the ~96 KB ring when dec_small_ring is auto (48) */
+  int dec_small_ring;      /* [order] decode GEMMs: ~100 KB ring (1), 192 KB (0), -1 auto (B <= dec_small_max) */
+  int dec_small_max;       /* largest batch on the ~100 KB ring when dec_small_ring is auto (32) */
   int dec_split_in;        /* [order] decode in_proj split-K factor (0 auto) */
   int dec_split_out;       /* [order] decode out_proj split-K factor (0 auto) */
   int stream_stages;       /* decode state stream: ring stages (0 = as many as fit) */

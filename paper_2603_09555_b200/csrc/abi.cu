@@ -64,7 +64,8 @@ ssd200_tuning_t make_default_tuning() {
   t.dec_pdl = 1;
   t.dec_swap = 1;
   t.dec_small_ring = -1;
-  t.dec_small_max = 48;      // small ring B = 32 2.23 -> 2.12 ms, big ring B = 64 3.47 -> 3.37 ms
+  t.dec_small_max = 32;      // 1.3B: small ring B = 32 2.34 -> 2.25 ms, big ring B = 40 2.59 -> 2.49,
+                             // B = 48 2.89 -> 2.75 ms
   t.dec_split_in = 0;
   t.dec_split_out = 0;
   t.stream_stages = 0;

@@ -553,7 +553,7 @@ def test_generate_graph_cache_reuse_is_exact():
 
 def test_bf16_decode_batch_invariance_across_gemm_classes():
     """At production widths (1.3B: d_model 2048) the in_proj split-K differs
-    between the ~96 KB-ring class (B <= 48: split 4) and the 192 KB-ring class
+    between the ~100 KB-ring class (B <= 32: split 4) and the 192 KB-ring class
     (split 2), so the f32 partial sums are added in a different order.  Forcing
     one ring (tuning dec_small_ring) makes the split a function of the widths only: rows are
     then bitwise batch-invariant across B = 2 and B = 64.  Without forcing, rows
