@@ -75,8 +75,8 @@ typedef struct ssd200_tuning {
                               accesses, so they do not evict the operands' L2 reuse: 0 off,
                               1 when the output exceeds 1 GB as f32 (1), 2 always */
   int stream_chunk;        /* decode state stream tile hand-out: 0 auto (once a CTA's fair share
-                              is >= 4 tiles, chunks of 1/12 of it, 1..8 tiles, from an atomic
-                              counter), -1 static contiguous ranges, > 0 tiles per chunk */
+                              is >= 4 tiles, chunks from an atomic counter: 1 tile, 3 from a
+                              share of 8), -1 static contiguous ranges, > 0 tiles per chunk */
   int stream_reg_state;    /* decode state stream with one tile per CTA (2 B x H <= SMs, static
                               tiles): the state rows go to registers at kernel entry, not through
                               the smem ring (1) */

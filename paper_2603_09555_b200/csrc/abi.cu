@@ -1132,8 +1132,10 @@ int decode_layer_big(const ssd200_dims_t *d, const ssd200_layer_t *w, float *hid
   const bool can_dyn = B <= 256 && tune().dec_swap;
   int chunk = 0;
   if (tune().stream_chunk > 0) chunk = tune().stream_chunk;
-  else if (tune().stream_chunk == 0 && per_cta >= 4)  // 1.3B B = 256: 11.1 (static) -> 10.45 ms
-    chunk = per_cta / 12 < 1 ? 1 : (per_cta / 12 > 8 ? 8 : per_cta / 12);
+  else if (tune().stream_chunk == 0 && per_cta >= 4)  // 1.3B B = 256: 11.1 (static) -> 10.3 ms
+    // chunks of 3 from 8 tiles per CTA (1.3B B = 64 3.29 -> 3.22 ms, 780M B = 128 4.27 -> 4.20
+    // ms vs chunks of 1; B = 256 equal to 4)
+    chunk = per_cta >= 8 ? 3 : 1;
   sa.chunk = can_dyn ? chunk : 0;
   sa.ctr = o.ctr;
   const int cw = tune().stream_cw == 16 ? 16 : 8;  // consumer warps
